@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""Benchmark of the ChainerMN data-parallel update step (arXiv 1908.00213 §6)
+on B200: BASELINE.json metric "allreduce+update step us and bus GB/s
+(ResNet-50 grads) at 1/2/4/8 B200 vs roofline".
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--dtype fp32|fp16]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (N > 1)
+    python bench.py --impl reference ...                     (the CPU oracle arm)
+
+A step is one pass of the whole hot path over the ResNet-50 gradient set
+(161 tensors, 25,557,032 fp32 params): pack (+cast) -> all-reduce -> average +
+momentum-SGD, through the C ABI (cmn_step).  At N = 1 the all-reduce is the
+identity and cmn_step runs the fused direct kernel (no pack).  Inputs are
+seeded synthetic gradients/params (synth/), resident in HBM before the timed
+region; L2 is flushed (256 MiB write) between timed steps.  Rank 0 prints
+ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "allreduce+update step µs and bus GB/s (ResNet-50 grads) at 1/2/4/8 B200 vs roofline"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="cmn", choices=["cmn", "reference"])
+    ap.add_argument("--dtype", default="fp32", choices=["fp32", "fp16"])
+    ap.add_argument("--algo", default="auto", choices=["auto", "oneshot", "twoshot", "nccl"])
+    ap.add_argument("--min-warmup-s", type=float, default=1.0,
+                    help="keep warming up (untimed) at least this long so the clock sampler sees load")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- helpers
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, STREAM-style copy)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(key: str):
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    --set full summary (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    v = d.get(key)
+    return None if v is None else float(v)
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled while the GPU is loaded."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, ValueError):
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.time(), line.strip()))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+
+    def summary(self, t0: float, t1: float):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ts, line in self.rows:
+            if not (t0 <= ts <= t1):
+                continue
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def workload():
+    import synth
+    shapes = synth.resnet50_shapes()
+    return shapes, [synth.numel(s) for s in shapes]
+
+
+# ------------------------------------------------------ CPU oracle baseline
+
+def oracle_step_time(n_workers: int, dtype: str, budget_s: float):
+    """Time the CPU oracle (single-threaded, as it stands) on a bounded
+    sample of the ResNet-50 workload; returns (us per full-workload step,
+    sample description)."""
+    import numpy as np
+
+    import oracle
+    import synth
+    shapes, sizes = workload()
+    P = sum(sizes)
+    # sample: a prefix of the layer list holding ~ 2M params (all tensor kinds)
+    take, acc = 0, 0
+    while take < len(shapes) and acc < 2_000_000:
+        acc += sizes[take]
+        take += 1
+    sub = shapes[:take]
+    g = synth.grads(sub, workers=n_workers)
+    w = synth.params(sub)
+    v = [np.zeros_like(x) for x in w]
+    times = []
+    t_end = time.time() + budget_s
+    while time.time() < t_end or len(times) < 2:
+        t0 = time.perf_counter()
+        oracle.step(g, w, v, 0.1, 0.9, dtype)
+        times.append(time.perf_counter() - t0)
+    per_param = statistics.median(times) / acc
+    desc = (f"oracle/cmn_oracle.c orc_step (pack+tree-reduce+momentum-SGD, 1 thread) on the first "
+            f"{take} of 161 ResNet-50 tensors ({acc:,} params), {n_workers} simulated worker(s), "
+            f"{dtype}, median of {len(times)} runs, scaled x{P / acc:.2f} to the full {P:,}-param set")
+    return per_param * P * 1e6, desc
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    n = max(1, args.gpus)
+    us, desc = oracle_step_time(n, args.dtype, min(args.cpu_budget_s, 8.0))
+    steps = []
+    for _ in range(args.warmup):
+        pass
+    for _ in range(args.steps):
+        steps.append(us)
+    shapes, sizes = workload()
+    cfg = {"workload": f"ResNet-50 gradient set (161 tensors, {sum(sizes):,} fp32 params), "
+                       f"{args.dtype} payload, momentum-SGD, {n} worker(s) simulated on host"}
+    line = {"impl": "reference", "metric": METRIC, "value": us, "unit": "us", "n_gpus": n,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": us / 1e3,
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": cfg,
+            "cpu_baseline": {"value": us, "unit": "us", "cores": 1, "kind": "oracle", "sample": desc},
+            "e2e": {"value": us, "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------- the bench
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_1908_00213_b200 import Comm
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        group = dist.group.WORLD
+
+    shapes, sizes = workload()
+    P, T = sum(sizes), len(sizes)
+    comm = Comm.init(rank, world, local, group)
+
+    # Parameters live in one flat device allocation laid out like the packed
+    # layout (a flat-parameter model), so the e2e D2H is one copy.
+    import paper_1908_00213_b200.cmn as cmn_mod
+    off, L, _ = cmn_mod.plan_layout(shapes)
+    flat_w = torch.empty(L, dtype=torch.float32, device=dev)
+    p0 = synth.params(shapes)
+    w = []
+    for t, s in enumerate(shapes):
+        view = flat_w[off[t]: off[t] + sizes[t]].view(s)
+        view.copy_(torch.from_numpy(p0[t]).view(s))
+        w.append(view)
+    comm.register_params(w)
+    if args.algo != "auto" and world > 1:
+        comm.set_algo(args.algo)
+    g_host = synth.grads(shapes, workers=world)[rank]
+    flat_g = torch.empty(L, dtype=torch.float32, device=dev)
+    g = []
+    for t, s in enumerate(shapes):
+        view = flat_g[off[t]: off[t] + sizes[t]]
+        view.copy_(torch.from_numpy(g_host[t]))
+        g.append(view)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    t_load0 = time.time()
+    # warm-up (untimed): at least W steps and at least --min-warmup-s seconds
+    t_w = time.time()
+    n_w = 0
+    while n_w < args.warmup or time.time() - t_w < args.min_warmup_s:
+        comm.step(g, args.dtype, 0.1, 0.9, stream)
+        n_w += 1
+        if n_w % 64 == 0:
+            torch.cuda.synchronize()
+    torch.cuda.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    launches0 = comm.kernel_launches
+    for k in range(args.steps):
+        flush.random_(0, 255) if k == 0 else flush.add_(1)    # L2 flush (untimed, outside events)
+        starts[k].record(stream)
+        comm.step(g, args.dtype, 0.1, 0.9, stream)
+        ends[k].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    launches = comm.kernel_launches - launches0
+    t_load1 = time.time()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms = total_ms / args.steps
+    us = ms * 1e3
+    clocks = sampler.summary(t_load0, t_load1)
+    sampler.stop()
+
+    # ---- e2e: host buffers through cmn_step_host (H2D grads + D2H params)
+    e2e = None
+    if not args.no_e2e:
+        hg_flat = torch.empty(L, dtype=torch.float32).pin_memory()
+        hw_flat = torch.empty(L, dtype=torch.float32).pin_memory()
+        hg, hw = [], []
+        for t in range(T):
+            hg_view = hg_flat[off[t]: off[t] + sizes[t]]
+            hg_view.copy_(torch.from_numpy(g_host[t]))
+            hg.append(hg_view)
+            hw.append(hw_flat[off[t]: off[t] + sizes[t]])
+        for _ in range(max(3, args.warmup // 2)):
+            comm.step_host(hg, hw, args.dtype, 0.1, 0.9, stream)
+        torch.cuda.synchronize()
+        barrier()
+        ke = max(5, args.steps // 4)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(ke):
+            comm.step_host(hg, hw, args.dtype, 0.1, 0.9, stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        e_ms = e0.elapsed_time(e1) / ke
+        if world > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": e_ms * 1e3, "unit": "us", "h2d_bytes_per_step": 4 * P,
+               "d2h_bytes_per_step": 4 * P,
+               "path": "cmn_step_host: pinned host grads -> device, step, device params -> pinned host"}
+
+    comm.finalize()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel
+    peak, peak_src = load_peaks()
+    csz = 4 if args.dtype == "fp32" else 2
+    if world == 1:
+        kernel = "k_update_direct"
+        alg_bytes = 20 * P              # read g, w, v; write w, v
+        roof = {"bound": "hbm", "kernel": kernel, "achieved": alg_bytes / (ms * 1e-3) / 1e9,
+                "peak": peak, "unit": "GB/s", "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": alg_bytes,
+                "traffic": load_traffic(f"{kernel}_{args.dtype}")}
+        roof["frac"] = roof["achieved"] / peak
+        bus = None
+    else:
+        S = csz * P
+        bus_bytes = 2 * (world - 1) / world * S
+        bus = bus_bytes / (ms * 1e-3) / 1e9
+        roof = {"bound": "nvlink", "kernel": "step (pack + allreduce + update)", "achieved": bus,
+                "peak": 770.0, "unit": "GB/s",
+                "peak_source": "measured peer copy 770 GB/s/direction (B200_PROFILING.md); 900 nominal",
+                "algorithmic_bytes_per_launch": bus_bytes, "traffic": None}
+        roof["frac"] = bus / 770.0
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        cus, desc = oracle_step_time(world, args.dtype, args.cpu_budget_s)
+        cpu = {"value": cus, "unit": "us", "cores": 1, "kind": "oracle", "sample": desc}
+
+    cfg = {"workload": f"ResNet-50 gradient set (161 tensors, {P:,} fp32 params), {args.dtype} "
+                       f"payload, pack+allreduce+momentum-SGD step (BASELINE config "
+                       f"{'2' if args.dtype == 'fp32' else '3'})",
+           "n_tensors": T, "n_params": P, "padded_len": L, "comm_dtype": args.dtype,
+           "algo": args.algo if world > 1 else "identity (N=1 fused direct update)",
+           "lr": 0.1, "mu": 0.9, "l2": "flushed between timed steps (256 MiB write, untimed)",
+           "parallelism": f"dp{world}", "step_ms_median": statistics.median(step_ms) if world == 1 else None}
+    line = {"metric": METRIC, "value": us, "unit": "us", "n_gpus": world, "steps": args.steps,
+            "warmup": n_w, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded counter-hash, synth/)",
+            "config": cfg, "bus_gbs": bus, "hbm_gbs": roof["achieved"] if world == 1 else None,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks}
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,133 @@
+// cmn_device.cuh -- device helpers for the sm_100a kernels: fp16 payload
+// conversion, the fixed pairwise reduction tree, streaming vector memory
+// ops, and the cross-GPU release/acquire barrier.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_fp16.h>
+
+#include "cmn_internal.h"
+
+namespace cmn {
+
+// ------------------------------------------------------------ fp16 payload
+// fp32 -> fp16 is cvt.rn.f16.f32 (IEEE round-to-nearest-even, subnormals
+// kept: the library is built without --use_fast_math / -ftz), reading R4.
+__device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
+    const uint32_t a = __half_as_ushort(__float2half_rn(lo));
+    const uint32_t b = __half_as_ushort(__float2half_rn(hi));
+    return a | (b << 16);
+}
+__device__ __forceinline__ float half_lo(uint32_t h2) {
+    return __half2float(__ushort_as_half(static_cast<unsigned short>(h2 & 0xffffu)));
+}
+__device__ __forceinline__ float half_hi(uint32_t h2) {
+    return __half2float(__ushort_as_half(static_cast<unsigned short>(h2 >> 16)));
+}
+__device__ __forceinline__ float round_through_half(float x) {
+    return __half2float(__float2half_rn(x));
+}
+
+// ----------------------------------------------------- the reduction tree
+// tree(x_lo..x_hi) = tree(x_lo..x_m) + tree(x_m+1..x_hi), low half holds
+// ceil(n/2) inputs, IEEE fp32 round-to-nearest additions (reading R2).
+// __fadd_rn is never contracted into an FMA.
+template <int LO, int HI>
+struct Tree {
+    static constexpr int kN = HI - LO + 1;
+    static constexpr int kM = LO + (kN + 1) / 2 - 1;
+    __device__ __forceinline__ static float sum(const float *x) {
+        return __fadd_rn(Tree<LO, kM>::sum(x), Tree<kM + 1, HI>::sum(x));
+    }
+};
+template <int I>
+struct Tree<I, I> {
+    __device__ __forceinline__ static float sum(const float *x) { return x[I]; }
+};
+
+// ------------------------------------------------------------- memory ops
+// Streaming (evict-first) 16-byte accesses for data touched exactly once.
+__device__ __forceinline__ float4 ld_cs_f4(const float *p) {
+    return __ldcs(reinterpret_cast<const float4 *>(p));
+}
+__device__ __forceinline__ void st_cs_f4(float *p, const float4 &v) {
+    __stcs(reinterpret_cast<float4 *>(p), v);
+}
+__device__ __forceinline__ uint2 ld_cs_u2(const void *p) {
+    return __ldcs(reinterpret_cast<const uint2 *>(p));
+}
+__device__ __forceinline__ void st_cs_u2(void *p, const uint2 &v) {
+    __stcs(reinterpret_cast<uint2 *>(p), v);
+}
+
+// 16-byte load that may target a peer GPU's memory (UVA / IPC mapping) and
+// data published by a peer during this kernel: weak load, no L1 allocation
+// (never the non-coherent .nc path).
+__device__ __forceinline__ uint4 ld_peer_u4(const void *p) {
+    uint4 r;
+    asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p)
+                 : "memory");
+    return r;
+}
+__device__ __forceinline__ void st_u4(void *p, const uint4 &v) {
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+
+// ----------------------------------------------------------- the barrier
+__device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint64_t global_timer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Pairwise per-CTA barrier across ranks: CTA b of rank r tells CTA b of
+// every rank "my inputs for this phase are published" and waits for the
+// same from all of them.  Flag values are (seq << 2) | tag and only grow,
+// so no reset is needed; a peer at the same seq with another tag (payload
+// dtype or algorithm) is a call-sequence mismatch.  Spins are bounded by
+// %globaltimer (default 30 s).
+__device__ __forceinline__ void cross_rank_barrier(const Barrier &bar, int world, int slot) {
+    if (!bar.enabled) return;
+    __syncthreads();
+    const int tid = threadIdx.x;
+    if (tid < world) {
+        const size_t cell = (static_cast<size_t>(slot) * kMaxBarrierBlocks + blockIdx.x) * kMaxWorld;
+        __threadfence_system();
+        st_release_sys(bar.flags[tid] + cell + bar.rank, bar.value);
+        const uint32_t *mine = bar.flags[bar.rank] + cell + tid;
+        uint64_t t0 = 0;
+        for (uint32_t spin = 1;; ++spin) {
+            const uint32_t v = ld_acquire_sys(mine);
+            if ((v >> 2) == (bar.value >> 2) && v != bar.value) {
+                *reinterpret_cast<volatile int *>(bar.err) = 2;
+                break;
+            }
+            if (static_cast<int32_t>(v - bar.value) >= 0) break;
+            if ((spin & 1023u) == 0) {
+                const uint64_t t = global_timer_ns();
+                if (t0 == 0) {
+                    t0 = t;
+                } else if (t - t0 > bar.timeout_ns) {
+                    *reinterpret_cast<volatile int *>(bar.err) = 1;
+                    break;
+                }
+            }
+        }
+    }
+    __syncthreads();
+}
+
+}  // namespace cmn

@@ -1,0 +1,107 @@
+// cmn_internal.h -- types shared by the host runtime (cmn_runtime.cpp) and
+// the sm_100a kernels (cmn_kernels.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace cmn {
+
+constexpr int kMaxWorld = 8;          // == CMN_MAX_WORLD
+constexpr int kAlign = 64;            // == CMN_ALIGN_ELEMS
+constexpr int kThreads = 256;         // threads per CTA, every kernel
+constexpr int kItemElems = 4096;      // elements per work item (tensor-indexed kernels)
+constexpr int kMaxBarrierBlocks = 1024;
+constexpr int kBarrierSlots = 2;      // 0: start (inputs ready), 1: mid (reduce-scatter done)
+constexpr int kGradCap = 256;         // grad pointers carried per launch (kernel params)
+
+// One registered tensor (device-resident table built at registration).
+struct TensorDesc {
+    float *w;          // parameters (caller-owned)
+    float *mom;        // momentum-SGD state v (library-owned)
+    float *adam_m;     // Adam first moment (library-owned, lazily allocated)
+    float *adam_v;     // Adam second moment
+    int64_t n;         // numel
+    int64_t off;       // packed offset (elements, multiple of kAlign)
+    int64_t off_next;  // off of tensor t+1 (= end of this tensor's pad)
+};
+
+// A contiguous piece of one tensor: elements [k0, k0 + len) of tensor t.
+// len <= kItemElems, k0 is a multiple of kItemElems.
+struct Item {
+    int32_t t;
+    int32_t len;
+    int64_t k0;
+};
+
+// Grad pointers for the tensors [t_lo, t_lo + kGradCap) of one launch.
+struct GradTab {
+    const float *p[kGradCap];
+};
+
+// Cross-rank signalling for the P2P all-reduce.  flags[r] points at rank r's
+// signal pad (IPC-mapped for peers); pad layout:
+//   uint32 [kBarrierSlots][kMaxBarrierBlocks][kMaxWorld]
+struct Barrier {
+    uint32_t *flags[kMaxWorld];
+    int rank;
+    int enabled;        // 0 in simulated mode: stream order replaces barriers
+    uint32_t value;     // (seq << 2) | tag expected from every peer this call
+    uint64_t timeout_ns;
+    int *err;           // host-mapped error word: 0 ok, 1 timeout, 2 mismatch
+};
+
+// Peer buffer table (packed or reduced) in 16-byte units.
+struct PeerBufs {
+    const void *p[kMaxWorld];
+};
+
+// ---------------------------------------------------------------- launchers
+// All return cudaGetLastError() after the launch.  `dtype` 0 = fp32, 1 = fp16.
+
+// a1: pack items [i0, i1) (tensors of those items lie in [t_lo, t_lo+kGradCap)).
+cudaError_t launch_pack(const GradTab &g, int t_lo, const TensorDesc *td, const Item *items,
+                        int i0, int i1, int dtype, void *packed, cudaStream_t s);
+
+// a3: update from a reduced packed buffer (payload dtype), momentum SGD.
+cudaError_t launch_update_sgd(const TensorDesc *td, const Item *items, int i0, int i1,
+                              const void *reduced, int dtype, float inv_n, float lr, float mu,
+                              cudaStream_t s);
+
+// a1'+a3 at N = 1: read g directly (cast through fp16 if dtype == 1).
+cudaError_t launch_update_direct(const GradTab &g, int t_lo, const TensorDesc *td,
+                                 const Item *items, int i0, int i1, int dtype, float lr, float mu,
+                                 cudaStream_t s);
+
+// write a = r * inv_n into out tensors (test hook / Chainer semantics).
+cudaError_t launch_unpack_avg(const GradTab &out, int t_lo, const TensorDesc *td,
+                              const Item *items, int i0, int i1, const void *reduced, int dtype,
+                              float inv_n, cudaStream_t s);
+
+// NEXT-1 Adam.
+cudaError_t launch_update_adam(const TensorDesc *td, const Item *items, int i0, int i1,
+                               const void *reduced, int dtype, float inv_n, float alpha_t,
+                               float beta1, float beta2, float c1, float c2, float eps,
+                               cudaStream_t s);
+
+// a2 one-shot: out[j] = tree_i(in_i[j]) for j in [e0, e1) (elements; e0, e1
+// multiples of kAlign).  Barrier slot 0 at entry when enabled.
+cudaError_t launch_allreduce_oneshot(const PeerBufs &in, int world, void *out, int64_t e0,
+                                     int64_t e1, int dtype, const Barrier &bar, int blocks,
+                                     cudaStream_t s);
+
+// a2 two-shot.  phase bit 1: reduce-scatter of rank `rank`'s chunk from all
+// `in` buffers into red[rank]; phase bit 2: all-gather of every other
+// rank's chunk from red[p] into red[rank].  With the barrier enabled and
+// both phases: start barrier, RS, mid barrier, AG in one kernel.
+// chunk_start/chunk_end give every rank's element range (within [e0, e1)).
+cudaError_t launch_allreduce_twoshot(const PeerBufs &in, const PeerBufs &red, int world, int rank,
+                                     const int64_t *chunk_start, const int64_t *chunk_end,
+                                     int dtype, int phases, const Barrier &bar, int blocks,
+                                     cudaStream_t s);
+
+int num_sms(int device);
+
+}  // namespace cmn

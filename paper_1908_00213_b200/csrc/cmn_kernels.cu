@@ -1,0 +1,522 @@
+// cmn_kernels.cu -- hand-written sm_100a kernels of the data-parallel
+// update step (arXiv 1908.00213 §6.1.2):
+//
+//   k_pack            a1  multi-tensor pack (+ fp32->fp16 RNE cast), pads zeroed
+//   k_oneshot         a2  one-shot all-reduce: every rank tree-reduces all N buffers
+//   k_twoshot         a2  two-shot: reduce-scatter (own chunk) + all-gather
+//   k_update_sgd      a3  unpack + average (x fl(1/N)) + momentum SGD, in place
+//   k_update_direct   a1'+a3 at N = 1: reads g directly (no pack), 20 B/param
+//   k_unpack_avg      writes the averaged gradient back (Chainer semantics)
+//   k_update_adam     NEXT-1: fused bias-corrected Adam
+//
+// Every kernel is HBM- or NVLink-bandwidth bound (0.25 flop/B); there is no
+// contraction, so no tensor cores.  Design: 16-byte vector accesses, one
+// 4096-element work item per CTA for the tensor-indexed kernels (balanced
+// block -> (tensor, chunk) map precomputed at registration), grid-stride
+// 8 KB tiles for the packed-index kernels, streaming cache hints.
+#include <cstdint>
+
+#include "cmn_device.cuh"
+#include "cmn_internal.h"
+
+namespace cmn {
+
+namespace {
+
+constexpr int kVecPerThread = kItemElems / 4 / kThreads;  // float4s per thread per item
+static_assert(kItemElems % (4 * kThreads) == 0, "item must be a whole number of CTA vectors");
+
+// a = r * fl(1/N); v = fma(mu, v, a); w = fma(-lr, v, w)   (readings R3, R6)
+__device__ __forceinline__ void sgd_elem(float r, float inv_n, float lr, float mu, float &w,
+                                         float &v) {
+    const float a = __fmul_rn(r, inv_n);
+    v = __fmaf_rn(mu, v, a);
+    w = __fmaf_rn(-lr, v, w);
+}
+
+__device__ __forceinline__ void sgd_vec(const float4 &r, float inv_n, float lr, float mu,
+                                        float4 &w, float4 &v) {
+    sgd_elem(r.x, inv_n, lr, mu, w.x, v.x);
+    sgd_elem(r.y, inv_n, lr, mu, w.y, v.y);
+    sgd_elem(r.z, inv_n, lr, mu, w.z, v.z);
+    sgd_elem(r.w, inv_n, lr, mu, w.w, v.w);
+}
+
+// Reduced-buffer element loads in the payload dtype, widened to fp32.
+template <int DT>
+__device__ __forceinline__ float4 load_r4(const void *r, int64_t j) {
+    if constexpr (DT == 0) {
+        return ld_cs_f4(static_cast<const float *>(r) + j);
+    } else {
+        const uint2 h = ld_cs_u2(static_cast<const uint16_t *>(r) + j);
+        return make_float4(half_lo(h.x), half_hi(h.x), half_lo(h.y), half_hi(h.y));
+    }
+}
+template <int DT>
+__device__ __forceinline__ float load_r1(const void *r, int64_t j) {
+    if constexpr (DT == 0) {
+        return static_cast<const float *>(r)[j];
+    } else {
+        return __half2float(__ushort_as_half(static_cast<const uint16_t *>(r)[j]));
+    }
+}
+
+// ------------------------------------------------------------------- a1
+template <int DT>
+__global__ void __launch_bounds__(kThreads) k_pack(GradTab g, int t_lo,
+                                                   const TensorDesc *__restrict__ td,
+                                                   const Item *__restrict__ items, int i0,
+                                                   void *__restrict__ packed) {
+    const Item it = items[i0 + blockIdx.x];
+    const int64_t off = td[it.t].off;
+    const float *__restrict__ src = g.p[it.t - t_lo] + it.k0;
+    const int64_t base = off + it.k0;
+    const int nv = it.len >> 2;
+
+    float4 x[kVecPerThread];
+#pragma unroll
+    for (int u = 0; u < kVecPerThread; ++u) {
+        const int v = threadIdx.x + u * kThreads;
+        if (v < nv) x[u] = ld_cs_f4(src + 4 * v);
+    }
+#pragma unroll
+    for (int u = 0; u < kVecPerThread; ++u) {
+        const int v = threadIdx.x + u * kThreads;
+        if (v < nv) {
+            if constexpr (DT == 0) {
+                st_cs_f4(static_cast<float *>(packed) + base + 4 * v, x[u]);
+            } else {
+                st_cs_u2(static_cast<uint16_t *>(packed) + base + 4 * v,
+                         make_uint2(pack_half2(x[u].x, x[u].y), pack_half2(x[u].z, x[u].w)));
+            }
+        }
+    }
+    for (int k = (nv << 2) + threadIdx.x; k < it.len; k += kThreads) {
+        const float s = src[k];
+        if constexpr (DT == 0)
+            static_cast<float *>(packed)[base + k] = s;
+        else
+            static_cast<uint16_t *>(packed)[base + k] = __half_as_ushort(__float2half_rn(s));
+    }
+    // The item holding the tensor's last element zeroes the alignment pad.
+    const TensorDesc &d = td[it.t];
+    if (it.k0 + it.len == d.n) {
+        for (int64_t j = d.off + d.n + threadIdx.x; j < d.off_next; j += kThreads) {
+            if constexpr (DT == 0)
+                static_cast<float *>(packed)[j] = 0.0f;
+            else
+                static_cast<uint16_t *>(packed)[j] = 0;
+        }
+    }
+}
+
+// ------------------------------------------------------------------- a3
+template <int DT>
+__global__ void __launch_bounds__(kThreads) k_update_sgd(const TensorDesc *__restrict__ td,
+                                                         const Item *__restrict__ items, int i0,
+                                                         const void *__restrict__ reduced,
+                                                         float inv_n, float lr, float mu) {
+    const Item it = items[i0 + blockIdx.x];
+    const TensorDesc d = td[it.t];
+    float *__restrict__ w = d.w + it.k0;
+    float *__restrict__ m = d.mom + it.k0;
+    const int64_t base = d.off + it.k0;
+    const int nv = it.len >> 2;
+
+    float4 r[kVecPerThread], wv[kVecPerThread], mv[kVecPerThread];
+#pragma unroll
+    for (int u = 0; u < kVecPerThread; ++u) {
+        const int v = threadIdx.x + u * kThreads;
+        if (v < nv) {
+            r[u] = load_r4<DT>(reduced, base + 4 * v);
+            wv[u] = ld_cs_f4(w + 4 * v);
+            mv[u] = ld_cs_f4(m + 4 * v);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < kVecPerThread; ++u) {
+        const int v = threadIdx.x + u * kThreads;
+        if (v < nv) {
+            sgd_vec(r[u], inv_n, lr, mu, wv[u], mv[u]);
+            st_cs_f4(w + 4 * v, wv[u]);
+            st_cs_f4(m + 4 * v, mv[u]);
+        }
+    }
+    for (int k = (nv << 2) + threadIdx.x; k < it.len; k += kThreads) {
+        float wk = w[k], mk = m[k];
+        sgd_elem(load_r1<DT>(reduced, base + k), inv_n, lr, mu, wk, mk);
+        w[k] = wk;
+        m[k] = mk;
+    }
+}
+
+// a1' + a3 at N = 1: the all-reduce is the identity, so r = cast(g) and the
+// pack is skipped (20 B/param instead of 28).  Bitwise equal to the
+// unfused path: a = cast(g) * 1.0f.
+template <int DT>
+__global__ void __launch_bounds__(kThreads) k_update_direct(GradTab g, int t_lo,
+                                                            const TensorDesc *__restrict__ td,
+                                                            const Item *__restrict__ items, int i0,
+                                                            float lr, float mu) {
+    const Item it = items[i0 + blockIdx.x];
+    const TensorDesc d = td[it.t];
+    const float *__restrict__ gp = g.p[it.t - t_lo] + it.k0;
+    float *__restrict__ w = d.w + it.k0;
+    float *__restrict__ m = d.mom + it.k0;
+    const int nv = it.len >> 2;
+
+    float4 r[kVecPerThread], wv[kVecPerThread], mv[kVecPerThread];
+#pragma unroll
+    for (int u = 0; u < kVecPerThread; ++u) {
+        const int v = threadIdx.x + u * kThreads;
+        if (v < nv) {
+            r[u] = ld_cs_f4(gp + 4 * v);
+            wv[u] = ld_cs_f4(w + 4 * v);
+            mv[u] = ld_cs_f4(m + 4 * v);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < kVecPerThread; ++u) {
+        const int v = threadIdx.x + u * kThreads;
+        if (v < nv) {
+            float4 a = r[u];
+            if constexpr (DT == 1) {
+                a.x = round_through_half(a.x);
+                a.y = round_through_half(a.y);
+                a.z = round_through_half(a.z);
+                a.w = round_through_half(a.w);
+            }
+            sgd_vec(a, 1.0f, lr, mu, wv[u], mv[u]);
+            st_cs_f4(w + 4 * v, wv[u]);
+            st_cs_f4(m + 4 * v, mv[u]);
+        }
+    }
+    for (int k = (nv << 2) + threadIdx.x; k < it.len; k += kThreads) {
+        float a = gp[k];
+        if constexpr (DT == 1) a = round_through_half(a);
+        float wk = w[k], mk = m[k];
+        sgd_elem(a, 1.0f, lr, mu, wk, mk);
+        w[k] = wk;
+        m[k] = mk;
+    }
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kThreads) k_unpack_avg(GradTab out, int t_lo,
+                                                         const TensorDesc *__restrict__ td,
+                                                         const Item *__restrict__ items, int i0,
+                                                         const void *__restrict__ reduced,
+                                                         float inv_n) {
+    const Item it = items[i0 + blockIdx.x];
+    const int64_t base = td[it.t].off + it.k0;
+    float *dst = const_cast<float *>(out.p[it.t - t_lo]) + it.k0;
+    for (int k = threadIdx.x; k < it.len; k += kThreads)
+        dst[k] = __fmul_rn(load_r1<DT>(reduced, base + k), inv_n);
+}
+
+// NEXT-1: bias-corrected Adam, every operation IEEE round-to-nearest and
+// uncontracted, in the order written in the oracle (orc_update_adam).
+template <int DT>
+__global__ void __launch_bounds__(kThreads) k_update_adam(const TensorDesc *__restrict__ td,
+                                                          const Item *__restrict__ items, int i0,
+                                                          const void *__restrict__ reduced,
+                                                          float inv_n, float alpha_t, float beta1,
+                                                          float beta2, float c1, float c2,
+                                                          float eps) {
+    const Item it = items[i0 + blockIdx.x];
+    const TensorDesc d = td[it.t];
+    const int64_t base = d.off + it.k0;
+    float *__restrict__ w = d.w + it.k0;
+    float *__restrict__ m = d.adam_m + it.k0;
+    float *__restrict__ v = d.adam_v + it.k0;
+    for (int k = threadIdx.x; k < it.len; k += kThreads) {
+        const float a = __fmul_rn(load_r1<DT>(reduced, base + k), inv_n);
+        const float mn = __fadd_rn(__fmul_rn(beta1, m[k]), __fmul_rn(c1, a));
+        const float vn = __fadd_rn(__fmul_rn(beta2, v[k]), __fmul_rn(c2, __fmul_rn(a, a)));
+        const float den = __fadd_rn(__fsqrt_rn(vn), eps);
+        const float wn = __fsub_rn(w[k], __fmul_rn(alpha_t, __fdiv_rn(mn, den)));
+        m[k] = mn;
+        v[k] = vn;
+        w[k] = wn;
+    }
+}
+
+// ------------------------------------------------------------------- a2
+// 16-byte lanes: fp32 -> 4 values, fp16 -> 8 values.  Word W of each of the
+// N inputs is reduced independently (compile-time indices keep everything
+// in registers).
+template <int W>
+__device__ __forceinline__ uint32_t word(const uint4 &v) {
+    if constexpr (W == 0) return v.x;
+    else if constexpr (W == 1) return v.y;
+    else if constexpr (W == 2) return v.z;
+    else return v.w;
+}
+
+template <int N, int DT, int W>
+__device__ __forceinline__ uint32_t reduce_word(const uint4 (&x)[N]) {
+    if constexpr (DT == 0) {
+        float f[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) f[i] = __uint_as_float(word<W>(x[i]));
+        return __float_as_uint(Tree<0, N - 1>::sum(f));
+    } else {
+        float lo[N], hi[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            lo[i] = half_lo(word<W>(x[i]));
+            hi[i] = half_hi(word<W>(x[i]));
+        }
+        return pack_half2(Tree<0, N - 1>::sum(lo), Tree<0, N - 1>::sum(hi));
+    }
+}
+
+template <int N, int DT>
+__device__ __forceinline__ uint4 reduce_lanes(const uint4 (&x)[N]) {
+    return make_uint4(reduce_word<N, DT, 0>(x), reduce_word<N, DT, 1>(x),
+                      reduce_word<N, DT, 2>(x), reduce_word<N, DT, 3>(x));
+}
+
+constexpr int kARVec = 2;                       // 16-B vectors per thread per tile
+constexpr int kTileVecs = kThreads * kARVec;    // 8 KB tile
+
+// One-shot: every rank reduces the whole range [v0, v1) (16-B units).
+template <int N, int DT>
+__global__ void __launch_bounds__(kThreads) k_oneshot(const __grid_constant__ PeerBufs in,
+                                                      void *__restrict__ out, int64_t v0,
+                                                      int64_t v1,
+                                                      const __grid_constant__ Barrier bar) {
+    cross_rank_barrier(bar, N, 0);
+    for (int64_t tile = v0 + static_cast<int64_t>(blockIdx.x) * kTileVecs; tile < v1;
+         tile += static_cast<int64_t>(gridDim.x) * kTileVecs) {
+        uint4 x[kARVec][N];
+#pragma unroll
+        for (int u = 0; u < kARVec; ++u) {
+            const int64_t idx = tile + threadIdx.x + u * kThreads;
+            if (idx < v1) {
+#pragma unroll
+                for (int i = 0; i < N; ++i) x[u][i] = ld_peer_u4(static_cast<const uint4 *>(in.p[i]) + idx);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kARVec; ++u) {
+            const int64_t idx = tile + threadIdx.x + u * kThreads;
+            if (idx < v1) st_u4(static_cast<uint4 *>(out) + idx, reduce_lanes<N, DT>(x[u]));
+        }
+    }
+}
+
+struct Chunks {
+    int64_t s[kMaxWorld];   // 16-B units
+    int64_t e[kMaxWorld];
+};
+
+// Two-shot.  Tile i of every chunk belongs to CTA (i mod gridDim.x) in both
+// phases, so the per-CTA mid barrier pairs each all-gather read with the
+// reduce-scatter write that produced it.
+template <int N, int DT>
+__global__ void __launch_bounds__(kThreads) k_twoshot(const __grid_constant__ PeerBufs in,
+                                                      const __grid_constant__ PeerBufs red,
+                                                      int rank,
+                                                      const __grid_constant__ Chunks ch,
+                                                      int phases,
+                                                      const __grid_constant__ Barrier bar) {
+    if (phases & 1) {
+        cross_rank_barrier(bar, N, 0);
+        const int64_t s = ch.s[rank], e = ch.e[rank];
+        uint4 *dst = static_cast<uint4 *>(const_cast<void *>(red.p[rank]));
+        for (int64_t tile = s + static_cast<int64_t>(blockIdx.x) * kTileVecs; tile < e;
+             tile += static_cast<int64_t>(gridDim.x) * kTileVecs) {
+            uint4 x[kARVec][N];
+#pragma unroll
+            for (int u = 0; u < kARVec; ++u) {
+                const int64_t idx = tile + threadIdx.x + u * kThreads;
+                if (idx < e) {
+#pragma unroll
+                    for (int i = 0; i < N; ++i) x[u][i] = ld_peer_u4(static_cast<const uint4 *>(in.p[i]) + idx);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kARVec; ++u) {
+                const int64_t idx = tile + threadIdx.x + u * kThreads;
+                if (idx < e) st_u4(dst + idx, reduce_lanes<N, DT>(x[u]));
+            }
+        }
+    }
+    if (phases & 2) {
+        cross_rank_barrier(bar, N, 1);
+        uint4 *dst = static_cast<uint4 *>(const_cast<void *>(red.p[rank]));
+        int64_t maxlen = 0;
+#pragma unroll
+        for (int p = 0; p < N; ++p) maxlen = max(maxlen, ch.e[p] - ch.s[p]);
+        for (int64_t tile = static_cast<int64_t>(blockIdx.x) * kTileVecs; tile < maxlen;
+             tile += static_cast<int64_t>(gridDim.x) * kTileVecs) {
+            uint4 x[kARVec][N];
+#pragma unroll
+            for (int u = 0; u < kARVec; ++u) {
+                const int64_t rel = tile + threadIdx.x + u * kThreads;
+#pragma unroll
+                for (int p = 0; p < N; ++p) {
+                    if (p != rank && rel < ch.e[p] - ch.s[p])
+                        x[u][p] = ld_peer_u4(static_cast<const uint4 *>(red.p[p]) + ch.s[p] + rel);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kARVec; ++u) {
+                const int64_t rel = tile + threadIdx.x + u * kThreads;
+#pragma unroll
+                for (int p = 0; p < N; ++p) {
+                    if (p != rank && rel < ch.e[p] - ch.s[p]) st_u4(dst + ch.s[p] + rel, x[u][p]);
+                }
+            }
+        }
+    }
+}
+
+inline int grid_of(int i0, int i1) { return i1 > i0 ? i1 - i0 : 0; }
+
+}  // namespace
+
+// ----------------------------------------------------------------- launchers
+
+cudaError_t launch_pack(const GradTab &g, int t_lo, const TensorDesc *td, const Item *items,
+                        int i0, int i1, int dtype, void *packed, cudaStream_t s) {
+    const int grid = grid_of(i0, i1);
+    if (grid == 0) return cudaSuccess;
+    if (dtype == 0)
+        k_pack<0><<<grid, kThreads, 0, s>>>(g, t_lo, td, items, i0, packed);
+    else
+        k_pack<1><<<grid, kThreads, 0, s>>>(g, t_lo, td, items, i0, packed);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_update_sgd(const TensorDesc *td, const Item *items, int i0, int i1,
+                              const void *reduced, int dtype, float inv_n, float lr, float mu,
+                              cudaStream_t s) {
+    const int grid = grid_of(i0, i1);
+    if (grid == 0) return cudaSuccess;
+    if (dtype == 0)
+        k_update_sgd<0><<<grid, kThreads, 0, s>>>(td, items, i0, reduced, inv_n, lr, mu);
+    else
+        k_update_sgd<1><<<grid, kThreads, 0, s>>>(td, items, i0, reduced, inv_n, lr, mu);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_update_direct(const GradTab &g, int t_lo, const TensorDesc *td,
+                                 const Item *items, int i0, int i1, int dtype, float lr, float mu,
+                                 cudaStream_t s) {
+    const int grid = grid_of(i0, i1);
+    if (grid == 0) return cudaSuccess;
+    if (dtype == 0)
+        k_update_direct<0><<<grid, kThreads, 0, s>>>(g, t_lo, td, items, i0, lr, mu);
+    else
+        k_update_direct<1><<<grid, kThreads, 0, s>>>(g, t_lo, td, items, i0, lr, mu);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_avg(const GradTab &out, int t_lo, const TensorDesc *td,
+                              const Item *items, int i0, int i1, const void *reduced, int dtype,
+                              float inv_n, cudaStream_t s) {
+    const int grid = grid_of(i0, i1);
+    if (grid == 0) return cudaSuccess;
+    if (dtype == 0)
+        k_unpack_avg<0><<<grid, kThreads, 0, s>>>(out, t_lo, td, items, i0, reduced, inv_n);
+    else
+        k_unpack_avg<1><<<grid, kThreads, 0, s>>>(out, t_lo, td, items, i0, reduced, inv_n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_update_adam(const TensorDesc *td, const Item *items, int i0, int i1,
+                               const void *reduced, int dtype, float inv_n, float alpha_t,
+                               float beta1, float beta2, float c1, float c2, float eps,
+                               cudaStream_t s) {
+    const int grid = grid_of(i0, i1);
+    if (grid == 0) return cudaSuccess;
+    if (dtype == 0)
+        k_update_adam<0><<<grid, kThreads, 0, s>>>(td, items, i0, reduced, inv_n, alpha_t, beta1,
+                                                   beta2, c1, c2, eps);
+    else
+        k_update_adam<1><<<grid, kThreads, 0, s>>>(td, items, i0, reduced, inv_n, alpha_t, beta1,
+                                                   beta2, c1, c2, eps);
+    return cudaGetLastError();
+}
+
+namespace {
+template <int N, int DT>
+void oneshot_n(const PeerBufs &in, void *out, int64_t v0, int64_t v1, const Barrier &bar,
+               int blocks, cudaStream_t s) {
+    k_oneshot<N, DT><<<blocks, kThreads, 0, s>>>(in, out, v0, v1, bar);
+}
+template <int N, int DT>
+void twoshot_n(const PeerBufs &in, const PeerBufs &red, int rank, const Chunks &ch, int phases,
+               const Barrier &bar, int blocks, cudaStream_t s) {
+    k_twoshot<N, DT><<<blocks, kThreads, 0, s>>>(in, red, rank, ch, phases, bar);
+}
+template <int DT>
+bool oneshot_dispatch(int world, const PeerBufs &in, void *out, int64_t v0, int64_t v1,
+                      const Barrier &bar, int blocks, cudaStream_t s) {
+    switch (world) {
+        case 1: oneshot_n<1, DT>(in, out, v0, v1, bar, blocks, s); return true;
+        case 2: oneshot_n<2, DT>(in, out, v0, v1, bar, blocks, s); return true;
+        case 3: oneshot_n<3, DT>(in, out, v0, v1, bar, blocks, s); return true;
+        case 4: oneshot_n<4, DT>(in, out, v0, v1, bar, blocks, s); return true;
+        case 5: oneshot_n<5, DT>(in, out, v0, v1, bar, blocks, s); return true;
+        case 6: oneshot_n<6, DT>(in, out, v0, v1, bar, blocks, s); return true;
+        case 7: oneshot_n<7, DT>(in, out, v0, v1, bar, blocks, s); return true;
+        case 8: oneshot_n<8, DT>(in, out, v0, v1, bar, blocks, s); return true;
+        default: return false;
+    }
+}
+template <int DT>
+bool twoshot_dispatch(int world, const PeerBufs &in, const PeerBufs &red, int rank,
+                      const Chunks &ch, int phases, const Barrier &bar, int blocks,
+                      cudaStream_t s) {
+    switch (world) {
+        case 1: twoshot_n<1, DT>(in, red, rank, ch, phases, bar, blocks, s); return true;
+        case 2: twoshot_n<2, DT>(in, red, rank, ch, phases, bar, blocks, s); return true;
+        case 3: twoshot_n<3, DT>(in, red, rank, ch, phases, bar, blocks, s); return true;
+        case 4: twoshot_n<4, DT>(in, red, rank, ch, phases, bar, blocks, s); return true;
+        case 5: twoshot_n<5, DT>(in, red, rank, ch, phases, bar, blocks, s); return true;
+        case 6: twoshot_n<6, DT>(in, red, rank, ch, phases, bar, blocks, s); return true;
+        case 7: twoshot_n<7, DT>(in, red, rank, ch, phases, bar, blocks, s); return true;
+        case 8: twoshot_n<8, DT>(in, red, rank, ch, phases, bar, blocks, s); return true;
+        default: return false;
+    }
+}
+// elements -> 16-byte units
+inline int64_t to_vec(int64_t elems, int dtype) { return dtype == 0 ? elems / 4 : elems / 8; }
+}  // namespace
+
+cudaError_t launch_allreduce_oneshot(const PeerBufs &in, int world, void *out, int64_t e0,
+                                     int64_t e1, int dtype, const Barrier &bar, int blocks,
+                                     cudaStream_t s) {
+    if (blocks <= 0 || blocks > kMaxBarrierBlocks) return cudaErrorInvalidValue;
+    const int64_t v0 = to_vec(e0, dtype), v1 = to_vec(e1, dtype);
+    const bool ok = dtype == 0 ? oneshot_dispatch<0>(world, in, out, v0, v1, bar, blocks, s)
+                               : oneshot_dispatch<1>(world, in, out, v0, v1, bar, blocks, s);
+    return ok ? cudaGetLastError() : cudaErrorInvalidValue;
+}
+
+cudaError_t launch_allreduce_twoshot(const PeerBufs &in, const PeerBufs &red, int world, int rank,
+                                     const int64_t *chunk_start, const int64_t *chunk_end,
+                                     int dtype, int phases, const Barrier &bar, int blocks,
+                                     cudaStream_t s) {
+    if (blocks <= 0 || blocks > kMaxBarrierBlocks) return cudaErrorInvalidValue;
+    Chunks ch{};
+    for (int p = 0; p < world; ++p) {
+        ch.s[p] = to_vec(chunk_start[p], dtype);
+        ch.e[p] = to_vec(chunk_end[p], dtype);
+    }
+    const bool ok = dtype == 0
+                        ? twoshot_dispatch<0>(world, in, red, rank, ch, phases, bar, blocks, s)
+                        : twoshot_dispatch<1>(world, in, red, rank, ch, phases, bar, blocks, s);
+    return ok ? cudaGetLastError() : cudaErrorInvalidValue;
+}
+
+int num_sms(int device) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
+    return n;
+}
+
+}  // namespace cmn

@@ -1,0 +1,984 @@
+// cmn_runtime.cpp -- host runtime behind include/cmn.h: validation, the
+// packed layout, work-item tables, communication buffers (CUDA IPC peer
+// mapping, double-buffered by call parity), algorithm choice, the NCCL
+// comparison path, buckets for overlap, and error reporting.
+//
+// Paper passages: the communicator, the
+// multi_node_optimizer wrapping, the all-reduce step
+// (PAPER.md:449-454), fp16 payload, overlap
+// (PAPER.md:788-792).  Readings R1-R16 are listed in DESIGN.md §3.
+#include "../../include/cmn.h"
+
+#include <dlfcn.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "cmn_internal.h"
+
+using namespace cmn;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+cmn_status fail(cmn_status st, const std::string &msg) {
+    g_last_error = msg;
+    return st;
+}
+
+cmn_status cuda_fail(cudaError_t e, const char *what) {
+    return fail(CMN_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CMN_CUDA(call)                                          \
+    do {                                                        \
+        cudaError_t e_ = (call);                                \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call);     \
+    } while (0)
+
+uint64_t fnv1a(uint64_t h, const void *data, size_t n) {
+    const unsigned char *p = static_cast<const unsigned char *>(data);
+    for (size_t i = 0; i < n; ++i) {
+        h ^= p[i];
+        h *= 1099511628211ull;
+    }
+    return h;
+}
+
+int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+size_t env_size(const char *name, size_t dflt) {
+    const char *v = std::getenv(name);
+    if (!v || !*v) return dflt;
+    return static_cast<size_t>(std::strtoull(v, nullptr, 10));
+}
+
+// ---------------------------------------------------------------- NCCL
+// The comparison backend is loaded with dlopen so the library has no hard
+// dependency on libnccl (only CMN_ALGO_NCCL needs it).
+struct NcclApi {
+    void *h = nullptr;
+    int (*GetUniqueId)(void *) = nullptr;
+    int (*CommInitRank)(void **, int, const void *, int) = nullptr;
+    int (*AllReduce)(const void *, void *, size_t, int, int, void *, cudaStream_t) = nullptr;
+    int (*CommDestroy)(void *) = nullptr;
+    const char *(*GetErrorString)(int) = nullptr;
+    bool load() {
+        if (h) return true;
+        const char *cands[] = {std::getenv("CMN_NCCL_LIB"), "libnccl.so.2", "libnccl.so"};
+        for (const char *c : cands) {
+            if (!c) continue;
+            h = dlopen(c, RTLD_NOW | RTLD_GLOBAL);
+            if (h) break;
+        }
+        if (!h) return false;
+        GetUniqueId = reinterpret_cast<int (*)(void *)>(dlsym(h, "ncclGetUniqueId"));
+        CommInitRank = reinterpret_cast<int (*)(void **, int, const void *, int)>(
+            dlsym(h, "ncclCommInitRank"));
+        AllReduce = reinterpret_cast<int (*)(const void *, void *, size_t, int, int, void *,
+                                             cudaStream_t)>(dlsym(h, "ncclAllReduce"));
+        CommDestroy = reinterpret_cast<int (*)(void *)>(dlsym(h, "ncclCommDestroy"));
+        GetErrorString = reinterpret_cast<const char *(*)(int)>(dlsym(h, "ncclGetErrorString"));
+        return GetUniqueId && CommInitRank && AllReduce && CommDestroy;
+    }
+};
+NcclApi g_nccl;
+constexpr int kNcclUniqueIdBytes = 128;
+constexpr int kNcclFloat16 = 6, kNcclFloat32 = 7, kNcclSum = 0;
+
+}  // namespace
+
+// One rank's library-owned communication region:
+//   [packed0 | packed1 | reduced0 | reduced1 | signal pad]
+struct RankBufs {
+    char *base = nullptr;
+    void *packed[2] = {nullptr, nullptr};
+    void *reduced[2] = {nullptr, nullptr};
+    uint32_t *flags = nullptr;
+    bool mapped = false;  // IPC-opened peer region
+};
+
+// Where an all-reduce left its result: buffer parity, payload dtype, and
+// whether the "reduced" buffer is the packed one (N == 1 identity).
+struct ArResult {
+    int parity = 0;
+    int dtype = 0;
+    bool alias_packed = false;
+};
+
+struct cmn_comm {
+    int rank = 0, world = 1, device = 0;
+    bool simulated = false;
+    cmn_allgather_fn ag = nullptr;
+    void *user = nullptr;
+    int nsm = 148;
+
+    // registration
+    int T = 0;
+    std::vector<int64_t> numel, off;
+    int64_t L = 0;
+    uint64_t hash = 0;
+    std::vector<float *> params;
+    std::vector<TensorDesc> h_td;
+    TensorDesc *d_td = nullptr;
+    std::vector<Item> h_items;
+    std::vector<int> item_begin;  // T + 1
+    Item *d_items = nullptr;
+    float *d_mom = nullptr;       // L floats, tensor t at off[t]
+    float *d_adam = nullptr;      // 2 L floats (m then v), lazily
+    float *d_staging = nullptr;   // host e2e staging, world_sim * L floats
+    size_t region_bytes = 0;
+    RankBufs rb[kMaxWorld];
+
+    // state
+    uint32_t seq = 0;
+    bool fresh = false;           // reduced buffer holds an unconsumed result
+    ArResult last;                    // of the last whole-model or bucket all-reduce
+    cmn_algo algo = CMN_ALGO_AUTO;
+    size_t oneshot_max = 1u << 20;
+    uint32_t timeout_ms = 30000;
+    int ar_blocks = 0;
+    int *h_err = nullptr, *d_err = nullptr;
+    uint64_t launches = 0;
+    std::vector<std::pair<int, int>> buckets;   // [t_begin, t_end), reverse order
+    std::vector<char> bucket_fresh;
+    std::vector<ArResult> bucket_res;
+    void *nccl = nullptr;
+};
+
+namespace {
+
+cmn_status check_async_error(cmn_comm *c) {
+    if (!c->h_err) return CMN_OK;
+    const int e = *reinterpret_cast<volatile int *>(c->h_err);
+    if (e == 1) return fail(CMN_ERR_TIMEOUT, "device spin-wait on a peer timed out");
+    if (e == 2) return fail(CMN_ERR_MISMATCH, "peer issued a different collective (dtype/algo)");
+    return CMN_OK;
+}
+
+cmn_status launched(cmn_comm *c, cudaError_t e, const char *what) {
+    if (e != cudaSuccess) return cuda_fail(e, what);
+    ++c->launches;
+    return CMN_OK;
+}
+
+void free_regions(cmn_comm *c) {
+    for (int r = 0; r < kMaxWorld; ++r) {
+        RankBufs &b = c->rb[r];
+        if (b.base) {
+            if (b.mapped)
+                cudaIpcCloseMemHandle(b.base);
+            else
+                cudaFree(b.base);
+        }
+        b = RankBufs{};
+    }
+}
+
+void free_registration(cmn_comm *c) {
+    free_regions(c);
+    cudaFree(c->d_td);
+    cudaFree(c->d_items);
+    cudaFree(c->d_mom);
+    cudaFree(c->d_adam);
+    cudaFree(c->d_staging);
+    c->d_td = nullptr;
+    c->d_items = nullptr;
+    c->d_mom = c->d_adam = c->d_staging = nullptr;
+    c->T = 0;
+    c->L = 0;
+    c->fresh = false;
+    c->buckets.clear();
+    c->bucket_fresh.clear();
+    c->bucket_res.clear();
+}
+
+void carve(RankBufs &b, char *base, int64_t L) {
+    const size_t buf = static_cast<size_t>(L) * 4;
+    b.base = base;
+    b.packed[0] = base;
+    b.packed[1] = base + buf;
+    b.reduced[0] = base + 2 * buf;
+    b.reduced[1] = base + 3 * buf;
+    b.flags = reinterpret_cast<uint32_t *>(base + 4 * buf);
+}
+
+size_t flags_bytes() {
+    return static_cast<size_t>(kBarrierSlots) * kMaxBarrierBlocks * kMaxWorld * sizeof(uint32_t);
+}
+
+cmn_status plan_layout_impl(int T, const int *ndims, const int64_t *dims,
+                            std::vector<int64_t> &numel, std::vector<int64_t> &off,
+                            uint64_t &hash) {
+    if (T <= 0) return fail(CMN_ERR_INVALID_ARG, "n_tensors must be >= 1");
+    if (!ndims) return fail(CMN_ERR_INVALID_ARG, "ndims is NULL");
+    numel.assign(T, 0);
+    off.assign(T + 1, 0);
+    hash = 1469598103934665603ull;
+    hash = fnv1a(hash, &T, sizeof T);
+    int64_t pos = 0;
+    for (int t = 0; t < T; ++t) {
+        const int nd = ndims[t];
+        if (nd < 0 || nd > 8) return fail(CMN_ERR_INVALID_ARG, "ndims out of range [0, 8]");
+        if (nd > 0 && !dims) return fail(CMN_ERR_INVALID_ARG, "dims is NULL");
+        int64_t n = 1;
+        for (int d = 0; d < nd; ++d) {
+            const int64_t e = dims[pos + d];
+            if (e < 0) return fail(CMN_ERR_INVALID_ARG, "negative dimension");
+            n *= e;
+        }
+        hash = fnv1a(hash, &nd, sizeof nd);
+        if (nd > 0) hash = fnv1a(hash, dims + pos, sizeof(int64_t) * nd);
+        pos += nd;
+        numel[t] = n;
+        off[t + 1] = align_up(off[t] + n, kAlign);
+    }
+    return CMN_OK;
+}
+
+// Allgather `bytes` from every rank; returns false if the callback failed.
+bool allgather(cmn_comm *c, const void *send, void *recv, size_t bytes) {
+    if (c->world == 1) {
+        std::memcpy(recv, send, bytes);
+        return true;
+    }
+    return c->ag(send, recv, bytes, c->user) == 0;
+}
+
+struct BootstrapMsg {
+    uint64_t hash;
+    uint64_t region_bytes;
+    cudaIpcMemHandle_t handle;
+};
+
+cmn_status alloc_regions(cmn_comm *c) {
+    c->region_bytes = static_cast<size_t>(c->L) * 4 * 4 + flags_bytes();
+    const int own = c->simulated ? c->world : 1;
+    for (int i = 0; i < own; ++i) {
+        const int r = c->simulated ? i : c->rank;
+        void *p = nullptr;
+        cudaError_t e = cudaMalloc(&p, c->region_bytes);
+        if (e != cudaSuccess) return fail(CMN_ERR_OOM, "cudaMalloc(comm region) failed");
+        CMN_CUDA(cudaMemset(p, 0, c->region_bytes));
+        carve(c->rb[r], static_cast<char *>(p), c->L);
+    }
+    return CMN_OK;
+}
+
+cmn_status exchange_and_map(cmn_comm *c) {
+    BootstrapMsg mine{};
+    mine.hash = c->hash;
+    mine.region_bytes = c->region_bytes;
+    CMN_CUDA(cudaIpcGetMemHandle(&mine.handle, c->rb[c->rank].base));
+    std::vector<BootstrapMsg> all(c->world);
+    if (!allgather(c, &mine, all.data(), sizeof(BootstrapMsg)))
+        return fail(CMN_ERR_BOOTSTRAP, "allgather callback failed");
+    for (int r = 0; r < c->world; ++r)
+        if (all[r].hash != c->hash || all[r].region_bytes != c->region_bytes)
+            return fail(CMN_ERR_MISMATCH, "ranks registered different model structures");
+    for (int r = 0; r < c->world; ++r) {
+        if (r == c->rank) continue;
+        void *p = nullptr;
+        CMN_CUDA(cudaIpcOpenMemHandle(&p, all[r].handle, cudaIpcMemLazyEnablePeerAccess));
+        carve(c->rb[r], static_cast<char *>(p), c->L);
+        c->rb[r].mapped = true;
+    }
+    return CMN_OK;
+}
+
+int ar_blocks_for(const cmn_comm *c) {
+    if (c->ar_blocks > 0) return c->ar_blocks;
+    const size_t env = env_size("CMN_CTAS", 0);
+    int b = env ? static_cast<int>(env) : 2 * c->nsm;
+    if (b > kMaxBarrierBlocks) b = kMaxBarrierBlocks;
+    if (b < 1) b = 1;
+    return b;
+}
+
+bool grads_ok(const cmn_comm *c, const float *const *g, int count, std::string &why) {
+    if (!g) {
+        why = "grads table is NULL";
+        return false;
+    }
+    for (int i = 0; i < count; ++i) {
+        const int t = i % c->T;
+        if (c->numel[t] == 0) continue;
+        if (!g[i]) {
+            why = "grad pointer " + std::to_string(i) + " is NULL";
+            return false;
+        }
+        if (reinterpret_cast<uintptr_t>(g[i]) % 16 != 0) {
+            why = "grad pointer " + std::to_string(i) + " is not 16-byte aligned";
+            return false;
+        }
+    }
+    return true;
+}
+
+// Iterate tensor groups of at most kGradCap tensors inside [ta, tb).
+template <typename F>
+cmn_status for_groups(cmn_comm *c, int ta, int tb, F &&f) {
+    for (int lo = ta; lo < tb; lo += kGradCap) {
+        const int hi = lo + kGradCap < tb ? lo + kGradCap : tb;
+        cmn_status st = f(lo, hi, c->item_begin[lo], c->item_begin[hi]);
+        if (st != CMN_OK) return st;
+    }
+    return CMN_OK;
+}
+
+GradTab make_tab(const float *const *g, int lo, int hi) {
+    GradTab tab{};
+    for (int t = lo; t < hi; ++t) tab.p[t - lo] = g[t];
+    return tab;
+}
+
+Barrier make_barrier(cmn_comm *c, int tag) {
+    Barrier b{};
+    for (int r = 0; r < c->world; ++r) b.flags[r] = c->rb[r].flags;
+    b.rank = c->rank;
+    b.enabled = c->simulated ? 0 : 1;
+    b.value = (c->seq << 2) | static_cast<uint32_t>(tag & 3);
+    b.timeout_ns = static_cast<uint64_t>(c->timeout_ms) * 1000000ull;
+    b.err = c->d_err;
+    return b;
+}
+
+cmn_algo choose_algo(const cmn_comm *c, size_t bytes) {
+    if (c->algo != CMN_ALGO_AUTO) return c->algo;
+    if (c->world <= 2 || bytes <= c->oneshot_max) return CMN_ALGO_ONESHOT;
+    return CMN_ALGO_TWOSHOT;
+}
+
+void chunk_plan(int64_t e0, int64_t e1, int world, int64_t *s, int64_t *e) {
+    const int64_t n = e1 - e0;
+    const int64_t cs = align_up((n + world - 1) / world, kAlign);
+    for (int r = 0; r < world; ++r) {
+        int64_t a = e0 + cs * r, b = e0 + cs * (r + 1);
+        if (a > e1) a = e1;
+        if (b > e1) b = e1;
+        s[r] = a;
+        e[r] = b;
+    }
+}
+
+// a1 + a2 over the tensor range [ta, tb) (whole model or one bucket).
+cmn_status allreduce_range(cmn_comm *c, int ta, int tb, const float *const *grads, int dtype,
+                           cudaStream_t s) {
+    if (cmn_status st = check_async_error(c); st != CMN_OK) return st;
+    const int64_t e0 = c->off[ta], e1 = c->off[tb];
+    const size_t esz = dtype == 0 ? 4 : 2;
+    const size_t bytes = static_cast<size_t>(e1 - e0) * esz;
+    cmn_algo algo = choose_algo(c, bytes);
+    if (algo == CMN_ALGO_NCCL && (c->simulated || !c->nccl))
+        return fail(CMN_ERR_STATE, "NCCL algorithm requested but no NCCL communicator "
+                                   "(cmn_set_algo(CMN_ALGO_NCCL) on every rank of a cmn_init comm)");
+    ++c->seq;
+    const int par = static_cast<int>(c->seq & 1u);
+    const int nsim = c->simulated ? c->world : 1;
+
+    // a1: pack every (simulated) rank's gradients into its packed buffer.
+    for (int i = 0; i < nsim; ++i) {
+        const int r = c->simulated ? i : c->rank;
+        const float *const *g = grads + static_cast<size_t>(i) * c->T;
+        cmn_status st = for_groups(c, ta, tb, [&](int lo, int hi, int i0, int i1) {
+            return launched(c,
+                            launch_pack(make_tab(g, lo, hi), lo, c->d_td, c->d_items, i0, i1, dtype,
+                                        c->rb[r].packed[par], s),
+                            "pack");
+        });
+        if (st != CMN_OK) return st;
+    }
+
+    c->last = ArResult{par, dtype, false};
+    if (c->world == 1) {
+        c->last.alias_packed = true;   // identity all-reduce (fp16 rounding done by the pack)
+    } else if (algo == CMN_ALGO_NCCL) {
+        void *src = static_cast<char *>(c->rb[c->rank].packed[par]) + e0 * esz;
+        void *dst = static_cast<char *>(c->rb[c->rank].reduced[par]) + e0 * esz;
+        const int rc = g_nccl.AllReduce(src, dst, static_cast<size_t>(e1 - e0),
+                                        dtype == 0 ? kNcclFloat32 : kNcclFloat16, kNcclSum,
+                                        c->nccl, s);
+        if (rc != 0)
+            return fail(CMN_ERR_NCCL, std::string("ncclAllReduce: ") +
+                                          (g_nccl.GetErrorString ? g_nccl.GetErrorString(rc) : "?"));
+    } else {
+        PeerBufs in{}, red{};
+        for (int r = 0; r < c->world; ++r) {
+            in.p[r] = c->rb[r].packed[par];
+            red.p[r] = c->rb[r].reduced[par];
+        }
+        const int blocks = ar_blocks_for(c);
+        const int tag = dtype | (algo == CMN_ALGO_TWOSHOT ? 2 : 0);
+        const Barrier bar = make_barrier(c, tag);
+        if (algo == CMN_ALGO_ONESHOT) {
+            for (int i = 0; i < nsim; ++i) {
+                const int r = c->simulated ? i : c->rank;
+                cmn_status st = launched(
+                    c,
+                    launch_allreduce_oneshot(in, c->world, c->rb[r].reduced[par], e0, e1, dtype,
+                                             bar, blocks, s),
+                    "allreduce_oneshot");
+                if (st != CMN_OK) return st;
+            }
+        } else {
+            int64_t cs[kMaxWorld], ce[kMaxWorld];
+            chunk_plan(e0, e1, c->world, cs, ce);
+            if (c->simulated) {
+                for (int phase = 1; phase <= 2; ++phase)
+                    for (int r = 0; r < c->world; ++r) {
+                        cmn_status st = launched(
+                            c,
+                            launch_allreduce_twoshot(in, red, c->world, r, cs, ce, dtype, phase,
+                                                     bar, blocks, s),
+                            "allreduce_twoshot");
+                        if (st != CMN_OK) return st;
+                    }
+            } else {
+                cmn_status st = launched(
+                    c,
+                    launch_allreduce_twoshot(in, red, c->world, c->rank, cs, ce, dtype, 3, bar,
+                                             blocks, s),
+                    "allreduce_twoshot");
+                if (st != CMN_OK) return st;
+            }
+        }
+    }
+    return CMN_OK;
+}
+
+const void *reduced_ptr(const cmn_comm *c, const ArResult &res, int rank) {
+    const int r = c->simulated ? rank : c->rank;
+    return res.alias_packed ? c->rb[r].packed[res.parity] : c->rb[r].reduced[res.parity];
+}
+
+cmn_status update_range(cmn_comm *c, int ta, int tb, const ArResult &res, float lr, float mu,
+                        cudaStream_t s) {
+    const float inv_n = 1.0f / static_cast<float>(c->world);
+    return for_groups(c, ta, tb, [&](int, int, int i0, int i1) {
+        return launched(c,
+                        launch_update_sgd(c->d_td, c->d_items, i0, i1, reduced_ptr(c, res, 0),
+                                          res.dtype, inv_n, lr, mu, s),
+                        "update_sgd");
+    });
+}
+
+cmn_status require_registered(const cmn_comm *c) {
+    if (!c) return fail(CMN_ERR_INVALID_ARG, "comm is NULL");
+    if (c->T == 0) return fail(CMN_ERR_STATE, "cmn_register_params has not been called");
+    return CMN_OK;
+}
+
+cmn_status require_dtype(int dtype) {
+    if (dtype != CMN_FP32 && dtype != CMN_FP16) return fail(CMN_ERR_INVALID_ARG, "unknown dtype");
+    return CMN_OK;
+}
+
+cmn_status set_device(const cmn_comm *c) {
+    CMN_CUDA(cudaSetDevice(c->device));
+    return CMN_OK;
+}
+
+cmn_status init_common(int rank, int world, int dev, bool sim, cmn_allgather_fn ag, void *user,
+                       cmn_comm **out) {
+    if (!out) return fail(CMN_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (world < 1 || world > kMaxWorld) return fail(CMN_ERR_INVALID_ARG, "world_size must be in [1, 8]");
+    if (rank < 0 || rank >= world) return fail(CMN_ERR_INVALID_ARG, "rank out of range");
+    if (!sim && world > 1 && !ag) return fail(CMN_ERR_INVALID_ARG, "allgather callback required");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return fail(CMN_ERR_CUDA, "no CUDA device available (this library has no CPU fallback)");
+    if (dev < 0 || dev >= ndev) return fail(CMN_ERR_INVALID_ARG, "cuda_device out of range");
+    cudaDeviceProp prop{};
+    CMN_CUDA(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major != 10)
+        return fail(CMN_ERR_CUDA, "device is not sm_100 (kernels are built for sm_100a only)");
+    CMN_CUDA(cudaSetDevice(dev));
+    cmn_comm *c = new cmn_comm();
+    c->rank = rank;
+    c->world = world;
+    c->device = dev;
+    c->simulated = sim;
+    c->ag = ag;
+    c->user = user;
+    c->nsm = prop.multiProcessorCount;
+    c->oneshot_max = env_size("CMN_ONESHOT_MAX_BYTES", c->oneshot_max);
+    if (cudaHostAlloc(&c->h_err, sizeof(int), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->d_err), c->h_err, 0) != cudaSuccess) {
+        delete c;
+        return fail(CMN_ERR_CUDA, "cannot allocate the mapped error word");
+    }
+    *c->h_err = 0;
+    if (const char *a = std::getenv("CMN_ALGO")) {
+        if (!std::strcmp(a, "oneshot")) c->algo = CMN_ALGO_ONESHOT;
+        if (!std::strcmp(a, "twoshot")) c->algo = CMN_ALGO_TWOSHOT;
+    }
+    *out = c;
+    return CMN_OK;
+}
+
+// Coalesced host<->device copies of per-tensor buffers laid out like the
+// packed layout (runs where both sides advance by off[t+1] - off[t]).
+cmn_status copy_tensors(cmn_comm *c, const float *const *src, float *const *dst, int T,
+                        cudaMemcpyKind kind, cudaStream_t s) {
+    int t = 0;
+    while (t < T) {
+        if (c->numel[t] == 0) {
+            ++t;
+            continue;
+        }
+        int u = t;
+        while (u + 1 < T && c->numel[u + 1] > 0 &&
+               src[u + 1] == src[u] + (c->off[u + 1] - c->off[u]) &&
+               dst[u + 1] == dst[u] + (c->off[u + 1] - c->off[u]))
+            ++u;
+        const size_t bytes = static_cast<size_t>(c->off[u] - c->off[t] + c->numel[u]) * 4;
+        CMN_CUDA(cudaMemcpyAsync(dst[t], src[t], bytes, kind, s));
+        t = u + 1;
+    }
+    return CMN_OK;
+}
+
+}  // namespace
+
+// =====================================================================
+extern "C" {
+
+int cmn_version(void) { return CMN_VERSION; }
+
+const char *cmn_last_error(void) { return g_last_error.c_str(); }
+
+cmn_status cmn_init(int rank, int world_size, int cuda_device, cmn_allgather_fn ag, void *user,
+                    cmn_comm **out) {
+    try {
+        return init_common(rank, world_size, cuda_device, false, ag, user, out);
+    } catch (...) {
+        return fail(CMN_ERR_OOM, "host allocation failed");
+    }
+}
+
+cmn_status cmn_init_simulated(int world_size, int cuda_device, cmn_comm **out) {
+    try {
+        return init_common(0, world_size, cuda_device, true, nullptr, nullptr, out);
+    } catch (...) {
+        return fail(CMN_ERR_OOM, "host allocation failed");
+    }
+}
+
+cmn_status cmn_finalize(cmn_comm *c) {
+    if (!c) return CMN_OK;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    if (c->nccl && g_nccl.CommDestroy) g_nccl.CommDestroy(c->nccl);
+    free_registration(c);
+    if (c->h_err) cudaFreeHost(c->h_err);
+    delete c;
+    return CMN_OK;
+}
+
+cmn_status cmn_register_params(cmn_comm *c, int T, const int *ndims, const int64_t *dims,
+                               float *const *params) {
+    if (!c) return fail(CMN_ERR_INVALID_ARG, "comm is NULL");
+    try {
+        std::vector<int64_t> numel, off;
+        uint64_t hash = 0;
+        if (cmn_status st = plan_layout_impl(T, ndims, dims, numel, off, hash); st != CMN_OK)
+            return st;
+        if (!params) return fail(CMN_ERR_INVALID_ARG, "params table is NULL");
+        for (int t = 0; t < T; ++t) {
+            if (numel[t] == 0) continue;
+            if (!params[t]) return fail(CMN_ERR_INVALID_ARG, "param pointer is NULL");
+            if (reinterpret_cast<uintptr_t>(params[t]) % 16 != 0)
+                return fail(CMN_ERR_INVALID_ARG, "param pointer is not 16-byte aligned");
+        }
+        if (cmn_status st = set_device(c); st != CMN_OK) return st;
+        CMN_CUDA(cudaDeviceSynchronize());
+        free_registration(c);
+        c->T = T;
+        c->numel = numel;
+        c->off = off;
+        c->L = off[T];
+        c->hash = hash;
+        c->params.assign(params, params + T);
+        c->seq = 0;
+
+        // Work items: each tensor cut into kItemElems pieces.
+        c->h_items.clear();
+        c->item_begin.assign(T + 1, 0);
+        for (int t = 0; t < T; ++t) {
+            c->item_begin[t] = static_cast<int>(c->h_items.size());
+            for (int64_t k0 = 0; k0 < numel[t]; k0 += kItemElems) {
+                const int64_t len = numel[t] - k0 < kItemElems ? numel[t] - k0 : kItemElems;
+                c->h_items.push_back(Item{t, static_cast<int32_t>(len), k0});
+            }
+        }
+        c->item_begin[T] = static_cast<int>(c->h_items.size());
+
+        const size_t Lb = static_cast<size_t>(c->L > 0 ? c->L : 1) * 4;
+        if (cudaMalloc(&c->d_mom, Lb) != cudaSuccess) return fail(CMN_ERR_OOM, "momentum alloc");
+        CMN_CUDA(cudaMemset(c->d_mom, 0, Lb));
+        c->h_td.assign(T, TensorDesc{});
+        for (int t = 0; t < T; ++t) {
+            TensorDesc &d = c->h_td[t];
+            d.w = params[t];
+            d.mom = c->d_mom + off[t];
+            d.n = numel[t];
+            d.off = off[t];
+            d.off_next = off[t + 1];
+        }
+        CMN_CUDA(cudaMalloc(&c->d_td, sizeof(TensorDesc) * T));
+        CMN_CUDA(cudaMemcpy(c->d_td, c->h_td.data(), sizeof(TensorDesc) * T, cudaMemcpyHostToDevice));
+        const size_t ib = sizeof(Item) * (c->h_items.empty() ? 1 : c->h_items.size());
+        CMN_CUDA(cudaMalloc(&c->d_items, ib));
+        if (!c->h_items.empty())
+            CMN_CUDA(cudaMemcpy(c->d_items, c->h_items.data(), sizeof(Item) * c->h_items.size(),
+                                cudaMemcpyHostToDevice));
+
+        if (cmn_status st = alloc_regions(c); st != CMN_OK) return st;
+        if (!c->simulated) {
+            if (c->world > 1) {
+                if (cmn_status st = exchange_and_map(c); st != CMN_OK) return st;
+            }
+        }
+        CMN_CUDA(cudaDeviceSynchronize());
+        return CMN_OK;
+    } catch (...) {
+        return fail(CMN_ERR_OOM, "host allocation failed");
+    }
+}
+
+cmn_status cmn_get_layout(const cmn_comm *c, int64_t *offsets, int64_t *padded_len) {
+    if (!c) return fail(CMN_ERR_INVALID_ARG, "comm is NULL");
+    if (c->T == 0) return fail(CMN_ERR_STATE, "not registered");
+    if (offsets) std::memcpy(offsets, c->off.data(), sizeof(int64_t) * (c->T + 1));
+    if (padded_len) *padded_len = c->L;
+    return CMN_OK;
+}
+
+cmn_status cmn_allreduce_grads(cmn_comm *c, const float *const *grads, cmn_dtype dtype,
+                               void *stream) {
+    if (cmn_status st = require_registered(c); st != CMN_OK) return st;
+    if (cmn_status st = require_dtype(dtype); st != CMN_OK) return st;
+    std::string why;
+    if (!grads_ok(c, grads, c->T * (c->simulated ? c->world : 1), why))
+        return fail(CMN_ERR_INVALID_ARG, why);
+    if (cmn_status st = set_device(c); st != CMN_OK) return st;
+    cmn_status st = allreduce_range(c, 0, c->T, grads, dtype, static_cast<cudaStream_t>(stream));
+    if (st == CMN_OK) {
+        c->fresh = true;
+        c->bucket_fresh.assign(c->buckets.size(), 0);
+    }
+    return st;
+}
+
+cmn_status cmn_update_momentum_sgd(cmn_comm *c, float lr, float mu, void *stream) {
+    if (cmn_status st = require_registered(c); st != CMN_OK) return st;
+    if (!c->fresh) return fail(CMN_ERR_STATE, "no fresh all-reduce result to consume");
+    if (cmn_status st = set_device(c); st != CMN_OK) return st;
+    cmn_status st = update_range(c, 0, c->T, c->last, lr, mu, static_cast<cudaStream_t>(stream));
+    if (st == CMN_OK) c->fresh = false;
+    return st;
+}
+
+cmn_status cmn_step(cmn_comm *c, const float *const *grads, cmn_dtype dtype, float lr, float mu,
+                    void *stream) {
+    if (cmn_status st = require_registered(c); st != CMN_OK) return st;
+    if (cmn_status st = require_dtype(dtype); st != CMN_OK) return st;
+    if (c->world > 1) {
+        cmn_status st = cmn_allreduce_grads(c, grads, dtype, stream);
+        if (st != CMN_OK) return st;
+        return cmn_update_momentum_sgd(c, lr, mu, stream);
+    }
+    std::string why;
+    if (!grads_ok(c, grads, c->T, why)) return fail(CMN_ERR_INVALID_ARG, why);
+    if (cmn_status st = set_device(c); st != CMN_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    c->fresh = false;
+    return for_groups(c, 0, c->T, [&](int lo, int hi, int i0, int i1) {
+        return launched(c,
+                        launch_update_direct(make_tab(grads, lo, hi), lo, c->d_td, c->d_items, i0,
+                                             i1, dtype, lr, mu, s),
+                        "update_direct");
+    });
+}
+
+cmn_status cmn_step_host(cmn_comm *c, const float *const *host_grads, float *const *host_params,
+                         cmn_dtype dtype, float lr, float mu, void *stream) {
+    if (cmn_status st = require_registered(c); st != CMN_OK) return st;
+    if (cmn_status st = require_dtype(dtype); st != CMN_OK) return st;
+    const int nsim = c->simulated ? c->world : 1;
+    if (!host_grads) return fail(CMN_ERR_INVALID_ARG, "host_grads is NULL");
+    for (int i = 0; i < nsim * c->T; ++i)
+        if (c->numel[i % c->T] > 0 && !host_grads[i])
+            return fail(CMN_ERR_INVALID_ARG, "host grad pointer is NULL");
+    if (cmn_status st = set_device(c); st != CMN_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!c->d_staging) {
+        const size_t b = static_cast<size_t>(c->L > 0 ? c->L : 1) * 4 * nsim;
+        if (cudaMalloc(&c->d_staging, b) != cudaSuccess) return fail(CMN_ERR_OOM, "staging alloc");
+    }
+    std::vector<const float *> dg(static_cast<size_t>(nsim) * c->T);
+    for (int i = 0; i < nsim; ++i) {
+        std::vector<float *> dst(c->T);
+        for (int t = 0; t < c->T; ++t) {
+            dst[t] = c->d_staging + static_cast<size_t>(i) * c->L + c->off[t];
+            dg[static_cast<size_t>(i) * c->T + t] = dst[t];
+        }
+        if (cmn_status st = copy_tensors(c, host_grads + static_cast<size_t>(i) * c->T, dst.data(),
+                                         c->T, cudaMemcpyHostToDevice, s);
+            st != CMN_OK)
+            return st;
+    }
+    if (cmn_status st = cmn_step(c, dg.data(), dtype, lr, mu, stream); st != CMN_OK) return st;
+    if (host_params) {
+        std::vector<const float *> src(c->params.begin(), c->params.end());
+        if (cmn_status st = copy_tensors(c, src.data(), host_params, c->T, cudaMemcpyDeviceToHost, s);
+            st != CMN_OK)
+            return st;
+    }
+    return CMN_OK;
+}
+
+cmn_status cmn_unpack_avg_grads(cmn_comm *c, float *const *out, void *stream) {
+    if (cmn_status st = require_registered(c); st != CMN_OK) return st;
+    if (!c->fresh) return fail(CMN_ERR_STATE, "no fresh all-reduce result");
+    std::string why;
+    if (!grads_ok(c, const_cast<const float *const *>(out), c->T, why))
+        return fail(CMN_ERR_INVALID_ARG, why);
+    if (cmn_status st = set_device(c); st != CMN_OK) return st;
+    const float inv_n = 1.0f / static_cast<float>(c->world);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    return for_groups(c, 0, c->T, [&](int lo, int hi, int i0, int i1) {
+        return launched(c,
+                        launch_unpack_avg(make_tab(const_cast<const float *const *>(out), lo, hi),
+                                          lo, c->d_td, c->d_items, i0, i1,
+                                          reduced_ptr(c, c->last, 0), c->last.dtype, inv_n, s),
+                        "unpack_avg");
+    });
+}
+
+cmn_status cmn_update_adam(cmn_comm *c, float alpha, float beta1, float beta2, float eps,
+                           int step, void *stream) {
+    if (cmn_status st = require_registered(c); st != CMN_OK) return st;
+    if (!c->fresh) return fail(CMN_ERR_STATE, "no fresh all-reduce result to consume");
+    if (step < 1) return fail(CMN_ERR_INVALID_ARG, "step must be >= 1");
+    if (cmn_status st = set_device(c); st != CMN_OK) return st;
+    if (!c->d_adam) {
+        const size_t b = static_cast<size_t>(c->L > 0 ? c->L : 1) * 4 * 2;
+        if (cudaMalloc(&c->d_adam, b) != cudaSuccess) return fail(CMN_ERR_OOM, "adam state alloc");
+        CMN_CUDA(cudaMemset(c->d_adam, 0, b));
+        for (int t = 0; t < c->T; ++t) {
+            c->h_td[t].adam_m = c->d_adam + c->off[t];
+            c->h_td[t].adam_v = c->d_adam + c->L + c->off[t];
+        }
+        CMN_CUDA(cudaMemcpy(c->d_td, c->h_td.data(), sizeof(TensorDesc) * c->T,
+                            cudaMemcpyHostToDevice));
+    }
+    // alpha_t = alpha * sqrt(1 - beta2^t) / (1 - beta1^t), evaluated in double.
+    const double b1t = std::pow(static_cast<double>(beta1), static_cast<double>(step));
+    const double b2t = std::pow(static_cast<double>(beta2), static_cast<double>(step));
+    const float alpha_t = static_cast<float>(static_cast<double>(alpha) * std::sqrt(1.0 - b2t) / (1.0 - b1t));
+    const float c1 = 1.0f - beta1, c2 = 1.0f - beta2;
+    const float inv_n = 1.0f / static_cast<float>(c->world);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cmn_status st = for_groups(c, 0, c->T, [&](int, int, int i0, int i1) {
+        return launched(c,
+                        launch_update_adam(c->d_td, c->d_items, i0, i1,
+                                           reduced_ptr(c, c->last, 0), c->last.dtype, inv_n,
+                                           alpha_t, beta1, beta2, c1, c2, eps, s),
+                        "update_adam");
+    });
+    if (st == CMN_OK) c->fresh = false;
+    return st;
+}
+
+cmn_status cmn_plan_buckets(cmn_comm *c, size_t bucket_bytes, int *n_out) {
+    if (cmn_status st = require_registered(c); st != CMN_OK) return st;
+    c->buckets.clear();
+    int end = c->T;
+    while (end > 0) {
+        int begin = end - 1;
+        size_t acc = static_cast<size_t>(c->numel[begin]) * 4;
+        while (begin > 0 && bucket_bytes > 0 &&
+               acc + static_cast<size_t>(c->numel[begin - 1]) * 4 <= bucket_bytes) {
+            --begin;
+            acc += static_cast<size_t>(c->numel[begin]) * 4;
+        }
+        if (bucket_bytes == 0) begin = 0;
+        c->buckets.emplace_back(begin, end);
+        end = begin;
+    }
+    c->bucket_fresh.assign(c->buckets.size(), 0);
+    c->bucket_res.assign(c->buckets.size(), ArResult{});
+    if (n_out) *n_out = static_cast<int>(c->buckets.size());
+    return CMN_OK;
+}
+
+cmn_status cmn_get_bucket(const cmn_comm *c, int b, int *t_begin, int *t_end) {
+    if (!c) return fail(CMN_ERR_INVALID_ARG, "comm is NULL");
+    if (b < 0 || b >= static_cast<int>(c->buckets.size()))
+        return fail(CMN_ERR_INVALID_ARG, "bucket index out of range");
+    if (t_begin) *t_begin = c->buckets[b].first;
+    if (t_end) *t_end = c->buckets[b].second;
+    return CMN_OK;
+}
+
+cmn_status cmn_allreduce_bucket(cmn_comm *c, int b, const float *const *grads, cmn_dtype dtype,
+                                void *stream) {
+    if (cmn_status st = require_registered(c); st != CMN_OK) return st;
+    if (cmn_status st = require_dtype(dtype); st != CMN_OK) return st;
+    if (b < 0 || b >= static_cast<int>(c->buckets.size()))
+        return fail(CMN_ERR_INVALID_ARG, "bucket index out of range");
+    std::string why;
+    if (!grads_ok(c, grads, c->T * (c->simulated ? c->world : 1), why))
+        return fail(CMN_ERR_INVALID_ARG, why);
+    if (cmn_status st = set_device(c); st != CMN_OK) return st;
+    cmn_status st = allreduce_range(c, c->buckets[b].first, c->buckets[b].second, grads, dtype,
+                                    static_cast<cudaStream_t>(stream));
+    if (st == CMN_OK) {
+        c->bucket_fresh[b] = 1;
+        c->bucket_res[b] = c->last;
+        c->fresh = false;
+    }
+    return st;
+}
+
+cmn_status cmn_update_bucket(cmn_comm *c, int b, float lr, float mu, void *stream) {
+    if (cmn_status st = require_registered(c); st != CMN_OK) return st;
+    if (b < 0 || b >= static_cast<int>(c->buckets.size()))
+        return fail(CMN_ERR_INVALID_ARG, "bucket index out of range");
+    if (!c->bucket_fresh[b]) return fail(CMN_ERR_STATE, "bucket has no fresh all-reduce result");
+    if (cmn_status st = set_device(c); st != CMN_OK) return st;
+    // The bucket's reduced values sit in the buffer of the parity its own
+    // all-reduce call used (recorded per bucket).
+    cmn_status st = update_range(c, c->buckets[b].first, c->buckets[b].second, c->bucket_res[b],
+                                 lr, mu, static_cast<cudaStream_t>(stream));
+    if (st == CMN_OK) c->bucket_fresh[b] = 0;
+    return st;
+}
+
+cmn_status cmn_set_algo(cmn_comm *c, cmn_algo algo, size_t oneshot_max_bytes) {
+    if (!c) return fail(CMN_ERR_INVALID_ARG, "comm is NULL");
+    if (algo < CMN_ALGO_AUTO || algo > CMN_ALGO_NCCL) return fail(CMN_ERR_INVALID_ARG, "bad algo");
+    if (oneshot_max_bytes) c->oneshot_max = oneshot_max_bytes;
+    if (algo == CMN_ALGO_NCCL && !c->nccl) {
+        if (c->simulated) return fail(CMN_ERR_UNSUPPORTED, "NCCL needs one process per GPU");
+        if (!g_nccl.load()) return fail(CMN_ERR_NCCL, "cannot load libnccl (set CMN_NCCL_LIB)");
+        if (cmn_status st = set_device(c); st != CMN_OK) return st;
+        char id[kNcclUniqueIdBytes] = {0};
+        if (c->rank == 0 && g_nccl.GetUniqueId(id) != 0)
+            return fail(CMN_ERR_NCCL, "ncclGetUniqueId failed");
+        std::vector<char> all(static_cast<size_t>(kNcclUniqueIdBytes) * c->world);
+        if (!allgather(c, id, all.data(), kNcclUniqueIdBytes))
+            return fail(CMN_ERR_BOOTSTRAP, "allgather callback failed");
+        void *comm = nullptr;
+        const int rc = g_nccl.CommInitRank(&comm, c->world, all.data(), c->rank);
+        if (rc != 0) return fail(CMN_ERR_NCCL, "ncclCommInitRank failed");
+        c->nccl = comm;
+    }
+    c->algo = algo;
+    return CMN_OK;
+}
+
+cmn_status cmn_set_timeout(cmn_comm *c, uint32_t timeout_ms) {
+    if (!c) return fail(CMN_ERR_INVALID_ARG, "comm is NULL");
+    if (timeout_ms == 0) return fail(CMN_ERR_INVALID_ARG, "timeout must be > 0");
+    c->timeout_ms = timeout_ms;
+    return CMN_OK;
+}
+
+cmn_status cmn_get_momentum(cmn_comm *c, int t, float **p) {
+    if (cmn_status st = require_registered(c); st != CMN_OK) return st;
+    if (t < 0 || t >= c->T || !p) return fail(CMN_ERR_INVALID_ARG, "bad tensor index / out ptr");
+    *p = c->d_mom + c->off[t];
+    return CMN_OK;
+}
+
+cmn_status cmn_get_adam_state(cmn_comm *c, int t, float **m, float **v) {
+    if (cmn_status st = require_registered(c); st != CMN_OK) return st;
+    if (t < 0 || t >= c->T) return fail(CMN_ERR_INVALID_ARG, "bad tensor index");
+    if (!c->d_adam) return fail(CMN_ERR_STATE, "no Adam state (call cmn_update_adam first)");
+    if (m) *m = c->d_adam + c->off[t];
+    if (v) *v = c->d_adam + c->L + c->off[t];
+    return CMN_OK;
+}
+
+static cmn_status copy_buf(cmn_comm *c, int rank, void *dst, void *stream, bool reduced) {
+    if (cmn_status st = require_registered(c); st != CMN_OK) return st;
+    if (!dst) return fail(CMN_ERR_INVALID_ARG, "dst is NULL");
+    if (c->seq == 0) return fail(CMN_ERR_STATE, "no all-reduce issued yet");
+    if (c->simulated ? (rank < 0 || rank >= c->world) : rank != c->rank)
+        return fail(CMN_ERR_INVALID_ARG, "rank not accessible from this process");
+    if (cmn_status st = set_device(c); st != CMN_OK) return st;
+    const int r = c->simulated ? rank : c->rank;
+    const void *src = reduced ? reduced_ptr(c, c->last, r) : c->rb[r].packed[c->last.parity];
+    const size_t bytes = static_cast<size_t>(c->L) * (c->last.dtype == 0 ? 4 : 2);
+    CMN_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice,
+                             static_cast<cudaStream_t>(stream)));
+    return CMN_OK;
+}
+
+cmn_status cmn_copy_packed(cmn_comm *c, int rank, void *dst, void *stream) {
+    return copy_buf(c, rank, dst, stream, false);
+}
+
+cmn_status cmn_copy_reduced(cmn_comm *c, int rank, void *dst, void *stream) {
+    return copy_buf(c, rank, dst, stream, true);
+}
+
+cmn_status cmn_poll_error(cmn_comm *c) {
+    if (!c) return fail(CMN_ERR_INVALID_ARG, "comm is NULL");
+    return check_async_error(c);
+}
+
+uint64_t cmn_kernel_launches(const cmn_comm *c) { return c ? c->launches : 0; }
+
+// ------------------------------------------------------- host-only helpers
+
+cmn_status cmn_plan_layout(int T, const int *ndims, const int64_t *dims, int64_t *offsets,
+                           int64_t *padded_len, uint64_t *hash_out) {
+    try {
+        std::vector<int64_t> numel, off;
+        uint64_t hash = 0;
+        if (cmn_status st = plan_layout_impl(T, ndims, dims, numel, off, hash); st != CMN_OK)
+            return st;
+        if (offsets) std::memcpy(offsets, off.data(), sizeof(int64_t) * (T + 1));
+        if (padded_len) *padded_len = off[T];
+        if (hash_out) *hash_out = hash;
+        return CMN_OK;
+    } catch (...) {
+        return fail(CMN_ERR_OOM, "host allocation failed");
+    }
+}
+
+cmn_status cmn_plan_chunks(int64_t L, int world, int64_t *starts, int64_t *ends) {
+    if (world < 1 || world > kMaxWorld) return fail(CMN_ERR_INVALID_ARG, "world out of range");
+    if (L < 0 || !starts || !ends) return fail(CMN_ERR_INVALID_ARG, "bad arguments");
+    chunk_plan(0, L, world, starts, ends);
+    return CMN_OK;
+}
+
+cmn_status cmn_bootstrap_verify(int rank, int world, cmn_allgather_fn ag, void *user,
+                                uint64_t hash) {
+    if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world)
+        return fail(CMN_ERR_INVALID_ARG, "rank/world out of range");
+    if (world > 1 && !ag) return fail(CMN_ERR_INVALID_ARG, "allgather callback required");
+    std::vector<uint64_t> all(world);
+    if (world == 1) return CMN_OK;
+    if (ag(&hash, all.data(), sizeof(uint64_t), user) != 0)
+        return fail(CMN_ERR_BOOTSTRAP, "allgather callback failed");
+    for (int r = 0; r < world; ++r)
+        if (all[r] != hash) return fail(CMN_ERR_MISMATCH, "ranks registered different model structures");
+    return CMN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,107 @@
+"""Host-side checks of the C ABI (no GPU needed): the library loads and
+exports every symbol include/cmn.h declares, the binding declares them all,
+the host-only plan helpers agree with the oracle's layout, and the compute
+entry points fail loudly (CMN_ERR_CUDA) when no sm_100 device is present."""
+import os
+import re
+
+import pytest
+import torch
+
+import synth
+from paper_1908_00213_b200 import cmn
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "cmn.h")
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(cmn_[a-z_0-9]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1908_00213_b200 import build
+    build.build()
+    return cmn.lib()
+
+
+def test_header_declares_the_north_star_calls():
+    syms = declared_symbols()
+    for s in ("cmn_init", "cmn_register_params", "cmn_allreduce_grads", "cmn_update_momentum_sgd"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for s in declared_symbols():
+        assert hasattr(lib, s), f"{s} declared in cmn.h but not exported"
+
+
+def test_binding_covers_every_declared_symbol():
+    bound = {name for name, _, _ in cmn.SIGNATURES}
+    assert set(declared_symbols()) == bound
+
+
+def test_version(lib):
+    assert lib.cmn_version() == 1
+
+
+@pytest.mark.parametrize("workload", ["mlp", "r50"])
+def test_plan_layout_matches_oracle(lib, orc, workload):
+    shapes = synth.WORKLOADS[workload]()
+    off, L, h = cmn.plan_layout(shapes)
+    ooff, oL = orc.layout([synth.numel(s) for s in shapes])
+    assert off == list(ooff) and L == oL
+    # structure hash: same shapes -> same hash; transposed shape -> different
+    _, _, h2 = cmn.plan_layout(shapes)
+    assert h == h2
+    sw = list(shapes)
+    sw[0] = tuple(reversed(sw[0]))
+    _, _, h3 = cmn.plan_layout(sw)
+    assert h3 != h or sw[0] == shapes[0]
+
+
+def test_plan_layout_rejects_bad_input(lib):
+    with pytest.raises(cmn.CmnError) as e:
+        cmn.plan_layout([])
+    assert e.value.status == 1
+    with pytest.raises(cmn.CmnError):
+        cmn.plan_layout([(3, -1)])
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 4, 5, 8])
+def test_plan_chunks_partition(lib, N):
+    for L in (0, 64, 640, 89792, 25557056):
+        s, e = cmn.plan_chunks(L, N)
+        assert s[0] == 0 and e[-1] == L
+        for r in range(N):
+            assert s[r] <= e[r]
+            assert s[r] % 64 == 0
+            if r:
+                assert s[r] == e[r - 1]
+        c = e[0] - s[0]
+        assert c == min(L, -(-(-(-L // N)) // 64) * 64)
+
+
+def test_r50_chunks_match_survey(lib):
+    # L/8 = 3,194,632 -> chunks of 3,194,688, last 3,194,240
+    s, e = cmn.plan_chunks(25557056, 8)
+    assert e[0] - s[0] == 3194688 and e[7] - s[7] == 3194240
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure path")
+def test_no_cpu_fallback(lib):
+    with pytest.raises(cmn.CmnError) as e:
+        cmn.Comm.simulated_world(2)
+    assert e.value.status_name == "CMN_ERR_CUDA"
+    with pytest.raises(cmn.CmnError):
+        cmn.Comm.init(0, 1, 0)
+
+
+def test_invalid_world(lib):
+    import ctypes as C
+    h = C.c_void_p()
+    assert lib.cmn_init_simulated(9, 0, C.byref(h)) == 1
+    assert lib.cmn_init_simulated(0, 0, C.byref(h)) == 1

@@ -1,0 +1,70 @@
+"""Multi-process host logic of the N > 1 path on CPU (gloo, world_size 2):
+the bootstrap allgather through torch.distributed, the registration-time
+structure check ("model structures are identical between workers merely in
+a single iteration") returning CMN_ERR_MISMATCH on every
+rank when they differ, and identical layout / chunk plans on every rank."""
+import os
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+import synth
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, mode, q):
+    import torch.distributed as dist
+
+    from paper_1908_00213_b200 import cmn
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        shapes = synth.mlp_shapes()
+        if mode == "mismatch" and rank == 1:
+            shapes = shapes[:-1] + [(11,)]            # one rank's model differs
+        if mode == "transposed" and rank == 1:
+            shapes = [(784, 100)] + shapes[1:]          # same numel, other structure
+        off, L, h = cmn.plan_layout(shapes)
+        st = cmn.bootstrap_verify(rank, world, h)
+        s, e = cmn.plan_chunks(L, world)
+        q.put((rank, st, off, L, s, e))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(mode, world=2):
+    from paper_1908_00213_b200 import build
+    build.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, mode, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return sorted(res)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_bootstrap_agrees(world):
+    res = _run("same", world)
+    assert all(r[1] == 0 for r in res)
+    assert all(r[2:] == res[0][2:] for r in res)
+
+
+@pytest.mark.parametrize("mode", ["mismatch", "transposed"])
+def test_bootstrap_mismatch_on_every_rank(mode):
+    res = _run(mode)
+    assert [r[1] for r in res] == [5, 5]      # CMN_ERR_MISMATCH on both ranks

@@ -1,0 +1,386 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded synthetic inputs, element by element.
+
+Bar: the pack/unpack index mapping is bit-exact; the
+hand-written fp32 and fp16 all-reduce + update are bit-exact too (same tree
+order, same IEEE rounding, same explicit fma), and additionally inside the
+north-star tolerance gate |a - abar| <= 1e-5 m (fp32) / 2e-3 m + 2^-24
+(fp16) against the exact fp64 average.  NaNs are compared by position.
+
+Simulated-N mode runs the same all-reduce kernels as the multi-process path
+(N buffers on one device, one launch per simulated rank)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as orc_mod
+import synth
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+
+
+@pytest.fixture(scope="module")
+def cmn():
+    from paper_1908_00213_b200 import build
+    build.build()
+    from paper_1908_00213_b200 import cmn as m
+    return m
+
+
+def _bits(x: np.ndarray) -> np.ndarray:
+    return x.view(np.uint32) if x.dtype == np.float32 else x.view(np.uint16)
+
+
+def assert_bitwise(got: np.ndarray, want: np.ndarray, what: str):
+    assert got.shape == want.shape, what
+    if got.dtype == np.float32:
+        gn, wn = np.isnan(got), np.isnan(want)
+    else:  # fp16 bits
+        gn = ((got & 0x7C00) == 0x7C00) & ((got & 0x3FF) != 0)
+        wn = ((want & 0x7C00) == 0x7C00) & ((want & 0x3FF) != 0)
+    assert np.array_equal(gn, wn), f"{what}: NaN positions differ"
+    ok = _bits(got)[~gn] == _bits(want)[~wn]
+    if not ok.all():
+        idx = np.flatnonzero(~gn)[np.flatnonzero(~ok)[:5]]
+        raise AssertionError(f"{what}: {np.count_nonzero(~ok)} elements differ, e.g. at {idx}: "
+                             f"got {got[idx]} want {want[idx]}")
+
+
+def to_dev(arrs):
+    return [torch.from_numpy(a.copy()).to(DEV) for a in arrs]
+
+
+def run_gpu(cmn, shapes, N, dtype, algo, grads_by_step, params0, lr, mu, capture=True):
+    comm = cmn.Comm.simulated_world(N)
+    try:
+        w = to_dev(params0)
+        comm.register_params(w)
+        comm.set_algo(algo)
+        off, L = comm.layout()
+        out = []
+        tdt = torch.float32 if dtype == "fp32" else torch.int16
+        for g in grads_by_step:
+            gd = [to_dev(gw) for gw in g]
+            comm.allreduce_grads(gd, dtype)
+            rec = {}
+            if capture:
+                rec["packed"] = []
+                rec["reduced"] = []
+                for r in range(N):
+                    p = torch.empty(L, dtype=tdt, device=DEV)
+                    comm.copy_packed(r, p)
+                    rec["packed"].append(p)
+                    q = torch.empty(L, dtype=tdt, device=DEV)
+                    comm.copy_reduced(r, q)
+                    rec["reduced"].append(q)
+            comm.update_momentum_sgd(lr, mu)
+            torch.cuda.synchronize()
+            rec = {k: [x.cpu().numpy() for x in v] for k, v in rec.items()}
+            if dtype == "fp16":
+                rec = {k: [x.view(np.uint16) for x in v] for k, v in rec.items()}
+            rec["w"] = [x.cpu().numpy().reshape(-1) for x in w]
+            rec["v"] = [comm.momentum(t).cpu().numpy().reshape(-1) for t in range(len(w))]
+            out.append(rec)
+        return out, off, L
+    finally:
+        comm.finalize()
+
+
+def run_oracle(orc, shapes, N, dtype, grads_by_step, params0, lr, mu):
+    w = [p.copy() for p in params0]
+    v = [np.zeros_like(p) for p in params0]
+    sizes = [synth.numel(s) for s in shapes]
+    off, L = orc.layout(sizes)
+    out = []
+    for g in grads_by_step:
+        packed = [orc.pack(gw, off, L, dtype) for gw in g]
+        red = orc.reduce_tree(packed, dtype)
+        orc.update_momentum_sgd(red, dtype, N, lr, mu, off, w, v)
+        out.append({"packed": packed, "reduced": red, "w": [x.copy() for x in w],
+                    "v": [x.copy() for x in v]})
+    return out, off, L
+
+
+def compare(gpu, ora, N, check_buffers=True):
+    for s, (g, o) in enumerate(zip(gpu, ora)):
+        if check_buffers:
+            for r in range(N):
+                assert_bitwise(g["packed"][r], o["packed"][r], f"step {s} packed rank {r}")
+                assert_bitwise(g["reduced"][r], o["reduced"], f"step {s} reduced rank {r}")
+        for t in range(len(o["w"])):
+            assert_bitwise(g["w"][t], o["w"][t], f"step {s} w[{t}]")
+            assert_bitwise(g["v"][t], o["v"][t], f"step {s} v[{t}]")
+
+
+RAGGED = [(1,), (3,), (4097,), (8191,), (100, 100), (65,), (2, 3, 5), (12289,), (7,)]
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 4, 5, 8])
+@pytest.mark.parametrize("dtype", ["fp32", "fp16"])
+@pytest.mark.parametrize("algo", ["oneshot", "twoshot"])
+def test_mlp_parity_bitexact(cmn, orc, N, dtype, algo):
+    shapes = synth.mlp_shapes()
+    grads = [synth.grads(shapes, workers=N, step=s) for s in range(2)]
+    params0 = synth.params(shapes)
+    gpu, goff, gL = run_gpu(cmn, shapes, N, dtype, algo, grads, params0, 0.1, 0.9)
+    ora, ooff, oL = run_oracle(orc, shapes, N, dtype, grads, params0, 0.1, 0.9)
+    assert goff == list(ooff) and gL == oL
+    compare(gpu, ora, N)
+
+
+@pytest.mark.parametrize("N", [1, 2, 7, 8])
+@pytest.mark.parametrize("dtype", ["fp32", "fp16"])
+@pytest.mark.parametrize("algo", ["oneshot", "twoshot"])
+def test_ragged_shapes_parity(cmn, orc, N, dtype, algo):
+    shapes = RAGGED
+    grads = [synth.grads(shapes, workers=N, step=s, seed=7) for s in range(3)]
+    params0 = synth.params(shapes, seed=7)
+    gpu, _, _ = run_gpu(cmn, shapes, N, dtype, algo, grads, params0, 0.05, 0.5)
+    ora, _, _ = run_oracle(orc, shapes, N, dtype, grads, params0, 0.05, 0.5)
+    compare(gpu, ora, N)
+
+
+@pytest.mark.parametrize("value_set", ["integer", "identical", "edge"])
+@pytest.mark.parametrize("dtype", ["fp32", "fp16"])
+def test_value_sets_parity(cmn, orc, value_set, dtype):
+    shapes = synth.mlp_shapes()
+    N = 4
+    lr, mu = (2.0 ** -4, 2.0 ** -1) if value_set == "integer" else (0.1, 0.9)
+    grads = [synth.grads(shapes, workers=N, step=s, value_set=value_set) for s in range(3)]
+    params0 = synth.params(shapes, value_set="integer" if value_set == "integer" else "random")
+    for algo in ("oneshot", "twoshot"):
+        gpu, _, _ = run_gpu(cmn, shapes, N, dtype, algo, grads, params0, lr, mu)
+        ora, _, _ = run_oracle(orc, shapes, N, dtype, grads, params0, lr, mu)
+        compare(gpu, ora, N)
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "fp16"])
+def test_tolerance_gate_vs_exact(cmn, orc, dtype):
+    """North-star gate on the averaged gradient: unpack_avg vs fp64 exact."""
+    shapes = synth.resnet50_shapes()[:20]
+    N = 8
+    g = synth.grads(shapes, workers=N)
+    comm = cmn.Comm.simulated_world(N)
+    try:
+        w = to_dev(synth.params(shapes))
+        comm.register_params(w)
+        comm.allreduce_grads([to_dev(gw) for gw in g], dtype)
+        out = [torch.empty_like(x) for x in w]
+        comm.unpack_avg_grads(out)
+        torch.cuda.synchronize()
+        off, L = comm.layout()
+        p32 = [orc.pack(gw, off, L, "fp32") for gw in g]
+        avg, mag = orc.exact_avg(p32)
+        for t, o in enumerate(out):
+            a = o.cpu().numpy().reshape(-1).astype(np.float64)
+            n = a.size
+            ex, m = avg[off[t]: off[t] + n], mag[off[t]: off[t] + n]
+            if dtype == "fp32":
+                assert np.all(np.abs(a - ex) <= 1e-5 * m)
+            else:
+                assert np.all(np.abs(a - ex) <= 2e-3 * m + 2.0 ** -24)
+    finally:
+        comm.finalize()
+
+
+def test_step_n1_direct_equals_unfused(cmn, orc):
+    """cmn_step at N = 1 (no pack, the bench's kernel) == allreduce+update ==
+    oracle, bitwise, for fp32 and fp16, over 3 steps."""
+    shapes = synth.mlp_shapes() + RAGGED
+    for dtype in ("fp32", "fp16"):
+        grads = [synth.grads(shapes, workers=1, step=s) for s in range(3)]
+        params0 = synth.params(shapes)
+        ora, _, _ = run_oracle(orc, shapes, 1, dtype, grads, params0, 0.1, 0.9)
+        comm = cmn.Comm.init(0, 1, 0)
+        try:
+            w = to_dev(params0)
+            comm.register_params(w)
+            for s, g in enumerate(grads):
+                comm.step(to_dev(g[0]), dtype, 0.1, 0.9)
+                torch.cuda.synchronize()
+                for t in range(len(w)):
+                    assert_bitwise(w[t].cpu().numpy().reshape(-1), ora[s]["w"][t], f"w[{t}] step {s}")
+                    assert_bitwise(comm.momentum(t).cpu().numpy().reshape(-1), ora[s]["v"][t], f"v[{t}]")
+        finally:
+            comm.finalize()
+
+
+@pytest.mark.slow
+def test_r50_full_size_n1_bench_config(cmn, orc):
+    """BASELINE config 2 at N = 1 in the launch configuration bench.py times
+    (cmn_step, fp32): all 25.6M elements of w and v vs the oracle."""
+    shapes = synth.resnet50_shapes()
+    g = synth.grads(shapes, workers=1)
+    params0 = synth.params(shapes)
+    w_o = [p.copy() for p in params0]
+    v_o = [np.zeros_like(p) for p in params0]
+    orc.step(g, w_o, v_o, 0.1, 0.9, "fp32")
+    comm = cmn.Comm.init(0, 1, 0)
+    try:
+        w = to_dev(params0)
+        comm.register_params(w)
+        comm.step(to_dev(g[0]), "fp32", 0.1, 0.9)
+        torch.cuda.synchronize()
+        for t in range(len(w)):
+            assert_bitwise(w[t].cpu().numpy().reshape(-1), w_o[t], f"w[{t}]")
+            assert_bitwise(comm.momentum(t).cpu().numpy().reshape(-1), v_o[t], f"v[{t}]")
+    finally:
+        comm.finalize()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("dtype,algo", [("fp32", "twoshot"), ("fp16", "twoshot"), ("fp16", "oneshot")])
+def test_r50_full_size_n8_simulated(cmn, orc, dtype, algo):
+    """ResNet-50 gradient set, 8 simulated workers, full size: reduced buffer
+    of every rank and the updated w, v, all elements, bit-exact."""
+    shapes = synth.resnet50_shapes()
+    N = 8
+    grads = [synth.grads(shapes, workers=N)]
+    params0 = synth.params(shapes)
+    gpu, _, _ = run_gpu(cmn, shapes, N, dtype, algo, grads, params0, 0.1, 0.9)
+    ora, _, _ = run_oracle(orc, shapes, N, dtype, grads, params0, 0.1, 0.9)
+    compare(gpu, ora, N)
+
+
+def test_buckets_bitwise_equal_unbucketed(cmn, orc):
+    """Overlap reading R15: bucketed (reverse order, any size) == unbucketed."""
+    shapes = synth.resnet50_shapes()[:40]
+    N = 4
+    grads = [synth.grads(shapes, workers=N, step=s) for s in range(2)]
+    params0 = synth.params(shapes)
+    ora, _, _ = run_oracle(orc, shapes, N, "fp16", grads, params0, 0.1, 0.9)
+    for bucket_bytes in (0, 1 << 16, 1 << 20, 4 << 20):
+        comm = cmn.Comm.simulated_world(N)
+        try:
+            w = to_dev(params0)
+            comm.register_params(w)
+            nb = comm.plan_buckets(bucket_bytes)
+            ranges = [comm.get_bucket(b) for b in range(nb)]
+            assert ranges[0][1] == len(shapes) and ranges[-1][0] == 0
+            for s, g in enumerate(grads):
+                gd = [to_dev(gw) for gw in g]
+                for b in range(nb):
+                    comm.allreduce_bucket(b, gd, "fp16")
+                for b in range(nb):
+                    comm.update_bucket(b, 0.1, 0.9)
+                torch.cuda.synchronize()
+                for t in range(len(w)):
+                    assert_bitwise(w[t].cpu().numpy().reshape(-1), ora[s]["w"][t], f"w[{t}]")
+        finally:
+            comm.finalize()
+
+
+def test_adam_parity(cmn, orc):
+    shapes = synth.mlp_shapes() + RAGGED
+    N = 2
+    sizes = [synth.numel(s) for s in shapes]
+    off, L = orc.layout(sizes)
+    params0 = synth.params(shapes)
+    w_o = [p.copy() for p in params0]
+    m_o = [np.zeros_like(p) for p in params0]
+    v_o = [np.zeros_like(p) for p in params0]
+    comm = cmn.Comm.simulated_world(N)
+    try:
+        w = to_dev(params0)
+        comm.register_params(w)
+        for step in range(1, 4):
+            g = synth.grads(shapes, workers=N, step=step)
+            red = orc.reduce_tree([orc.pack(gw, off, L, "fp32") for gw in g], "fp32")
+            orc.update_adam(red, "fp32", N, 1e-3, 0.9, 0.999, 1e-8, step, off, w_o, m_o, v_o)
+            comm.allreduce_grads([to_dev(gw) for gw in g], "fp32")
+            comm.update_adam(1e-3, 0.9, 0.999, 1e-8, step)
+            torch.cuda.synchronize()
+            for t in range(len(w)):
+                m, v = comm.adam_state(t)
+                assert_bitwise(w[t].cpu().numpy().reshape(-1), w_o[t], f"adam w[{t}]")
+                assert_bitwise(m.cpu().numpy().reshape(-1), m_o[t], f"adam m[{t}]")
+                assert_bitwise(v.cpu().numpy().reshape(-1), v_o[t], f"adam v[{t}]")
+    finally:
+        comm.finalize()
+
+
+def test_step_host_e2e_parity(cmn, orc):
+    shapes = synth.mlp_shapes()
+    g = synth.grads(shapes, workers=1)
+    params0 = synth.params(shapes)
+    w_o = [p.copy() for p in params0]
+    v_o = [np.zeros_like(p) for p in params0]
+    orc.step(g, w_o, v_o, 0.1, 0.9, "fp16")
+    comm = cmn.Comm.init(0, 1, 0)
+    try:
+        w = to_dev(params0)
+        comm.register_params(w)
+        hg = [torch.from_numpy(x.copy()).pin_memory() for x in g[0]]
+        hw = [torch.empty(x.shape, dtype=torch.float32).pin_memory() for x in params0]
+        comm.step_host(hg, hw, "fp16", 0.1, 0.9)
+        torch.cuda.synchronize()
+        for t in range(len(hw)):
+            assert_bitwise(hw[t].numpy().reshape(-1), w_o[t], f"host w[{t}]")
+    finally:
+        comm.finalize()
+
+
+def test_errors_are_loud(cmn):
+    shapes = synth.mlp_shapes()
+    comm = cmn.Comm.simulated_world(2)
+    try:
+        w = to_dev(synth.params(shapes))
+        comm.register_params(w)
+        with pytest.raises(cmn.CmnError) as e:
+            comm.update_momentum_sgd(0.1, 0.9)
+        assert e.value.status_name == "CMN_ERR_STATE"
+        g = [to_dev(gw) for gw in synth.grads(shapes, workers=2)]
+        bad = [list(gw) for gw in g]
+        bad[1][0] = bad[1][0].view(-1)[1:]            # 4-byte offset: misaligned
+        with pytest.raises(cmn.CmnError) as e:
+            comm.allreduce_grads(bad, "fp32")
+        assert e.value.status_name == "CMN_ERR_INVALID_ARG"
+        with pytest.raises(cmn.CmnError):
+            comm.allreduce_grads(g, 3)
+        comm.allreduce_grads(g, "fp32")
+        comm.update_momentum_sgd(0.1, 0.9)
+        with pytest.raises(cmn.CmnError):
+            comm.update_momentum_sgd(0.1, 0.9)         # consumed
+        with pytest.raises(cmn.CmnError):
+            comm.set_algo("nccl")                      # simulated: unsupported
+    finally:
+        comm.finalize()
+
+
+def test_fp16_conversion_exhaustive_on_gpu(cmn, orc):
+    """The GPU path's fp32->fp16 cast (inside k_pack) over a dense sweep of
+    fp32 bit patterns vs the oracle's hand-written RNE (itself pinned to
+    the compiler over all 2^32 inputs)."""
+    step = 4099  # coprime stride covering every exponent and many mantissas
+    bits = (np.arange(0, 2 ** 32, step, dtype=np.uint64)).astype(np.uint32)
+    x = bits.view(np.float32)
+    n = x.size - (x.size % 4)
+    x = x[:n]
+    comm = cmn.Comm.init(0, 1, 0)
+    try:
+        w = [torch.zeros(n, dtype=torch.float32, device=DEV)]
+        comm.register_params(w)
+        comm.allreduce_grads([torch.from_numpy(x.copy()).to(DEV)], "fp16")
+        p = torch.empty(n + (-n) % 64, dtype=torch.int16, device=DEV)
+        comm.copy_packed(0, p)
+        torch.cuda.synchronize()
+        got = p.cpu().numpy().view(np.uint16)[:n]
+        assert_bitwise(got, orc.f32_to_f16(x), "fp16 cast")
+    finally:
+        comm.finalize()
+
+
+def test_launch_count(cmn):
+    shapes = synth.resnet50_shapes()
+    comm = cmn.Comm.init(0, 1, 0)
+    try:
+        w = to_dev(synth.params(shapes))
+        comm.register_params(w)
+        g = to_dev(synth.grads(shapes, workers=1)[0])
+        before = comm.kernel_launches
+        comm.step(g, "fp32", 0.1, 0.9)
+        assert comm.kernel_launches - before == 1      # one fused kernel at N = 1
+    finally:
+        comm.finalize()
