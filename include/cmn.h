@@ -140,7 +140,7 @@ cmn_status cmn_finalize(cmn_comm *comm);
  *   params     T device pointers to contiguous fp32 parameters, each 16-byte
  *              aligned, caller-owned; they must stay valid and unmoved until
  *              finalize or re-registration.
- * Computes the packed layout (off_t aligned to CMN_ALGO_ALIGN elements),
+ * Computes the packed layout (off_t aligned to CMN_ALIGN_ELEMS elements),
  * allocates and zeroes the momentum buffers (library-owned), and the
  * communication buffers.  With world_size > 1 the layout hash is allgathered
  * and every rank returns CMN_ERR_MISMATCH if any rank differs (PAPER.md:495
@@ -196,6 +196,18 @@ cmn_status cmn_step(cmn_comm *comm, const float *const *grads, cmn_dtype dtype,
 cmn_status cmn_step_host(cmn_comm *comm, const float *const *host_grads,
                          float *const *host_params, cmn_dtype dtype,
                          float lr, float mu, void *stream);
+
+/* cmn_step_host_packed -- cmn_step_host with each side given as ONE host
+ * buffer in the packed layout: host_grads holds L floats per (simulated)
+ * rank (gradient t at offset off_t, pads ignored), host_params (NULL or L
+ * floats) receives the updated parameters at the same offsets.  At N == 1
+ * the call pipelines the host->device copy, the update and the
+ * device->host copy over ~8 tensor ranges on two internal copy streams
+ * (joined back into `stream`), so the step costs about one PCIe transfer
+ * instead of two.  If the registered params are views of one allocation in
+ * the packed layout, the device->host copies are contiguous. */
+cmn_status cmn_step_host_packed(cmn_comm *comm, const float *host_grads, float *host_params,
+                                cmn_dtype dtype, float lr, float mu, void *stream);
 
 /* cmn_unpack_avg_grads -- writes the averaged gradient a = r * fl(1/N)
  * back into `out` (n_tensors device fp32 pointers; may alias the grads),

@@ -38,6 +38,7 @@ SIGNATURES = [
     ("cmn_update_momentum_sgd", C.c_int, [_P, C.c_float, C.c_float, _P]),
     ("cmn_step", C.c_int, [_P, _PP, C.c_int, C.c_float, C.c_float, _P]),
     ("cmn_step_host", C.c_int, [_P, _PP, _PP, C.c_int, C.c_float, C.c_float, _P]),
+    ("cmn_step_host_packed", C.c_int, [_P, _P, _P, C.c_int, C.c_float, C.c_float, _P]),
     ("cmn_unpack_avg_grads", C.c_int, [_P, _PP, _P]),
     ("cmn_update_adam", C.c_int, [_P, C.c_float, C.c_float, C.c_float, C.c_float, C.c_int, _P]),
     ("cmn_plan_buckets", C.c_int, [_P, C.c_size_t, C.POINTER(C.c_int)]),
@@ -264,6 +265,14 @@ class Comm:
         g = self._grad_table(host_grads)
         p = _ptr_array(_data_ptrs(host_params)) if host_params is not None else None
         _check(lib().cmn_step_host(self._h, g, p, _dt(dtype), lr, mu, _stream(stream)), "cmn_step_host")
+
+    def step_host_packed(self, host_grads_flat, host_params_flat=None, dtype="fp32", lr=0.1, mu=0.9,
+                         stream=None):
+        """host_grads_flat: pinned float32 tensor of L (x world, simulated) elements in the
+        packed layout; host_params_flat: None or L elements receiving the new params."""
+        hp = host_params_flat.data_ptr() if host_params_flat is not None else None
+        _check(lib().cmn_step_host_packed(self._h, host_grads_flat.data_ptr(), hp, _dt(dtype), lr, mu,
+                                          _stream(stream)), "cmn_step_host_packed")
 
     def unpack_avg_grads(self, out, stream=None):
         _check(lib().cmn_unpack_avg_grads(self._h, _ptr_array(_data_ptrs(out)), _stream(stream)),

@@ -383,6 +383,7 @@ cudaError_t launch_pack(const GradTab &g, int t_lo, const TensorDesc *td, const 
                         int i0, int i1, int dtype, void *packed, cudaStream_t s) {
     const int grid = grid_of(i0, i1);
     if (grid == 0) return cudaSuccess;
+    (void)cudaGetLastError();  // report this launch's error, not a stale one
     if (dtype == 0)
         k_pack<0><<<grid, kThreads, 0, s>>>(g, t_lo, td, items, i0, packed);
     else
@@ -395,6 +396,7 @@ cudaError_t launch_update_sgd(const TensorDesc *td, const Item *items, int i0, i
                               cudaStream_t s) {
     const int grid = grid_of(i0, i1);
     if (grid == 0) return cudaSuccess;
+    (void)cudaGetLastError();  // report this launch's error, not a stale one
     if (dtype == 0)
         k_update_sgd<0><<<grid, kThreads, 0, s>>>(td, items, i0, reduced, inv_n, lr, mu);
     else
@@ -407,6 +409,7 @@ cudaError_t launch_update_direct(const GradTab &g, int t_lo, const TensorDesc *t
                                  cudaStream_t s) {
     const int grid = grid_of(i0, i1);
     if (grid == 0) return cudaSuccess;
+    (void)cudaGetLastError();  // report this launch's error, not a stale one
     if (dtype == 0)
         k_update_direct<0><<<grid, kThreads, 0, s>>>(g, t_lo, td, items, i0, lr, mu);
     else
@@ -419,6 +422,7 @@ cudaError_t launch_unpack_avg(const GradTab &out, int t_lo, const TensorDesc *td
                               float inv_n, cudaStream_t s) {
     const int grid = grid_of(i0, i1);
     if (grid == 0) return cudaSuccess;
+    (void)cudaGetLastError();  // report this launch's error, not a stale one
     if (dtype == 0)
         k_unpack_avg<0><<<grid, kThreads, 0, s>>>(out, t_lo, td, items, i0, reduced, inv_n);
     else
@@ -432,6 +436,7 @@ cudaError_t launch_update_adam(const TensorDesc *td, const Item *items, int i0, 
                                cudaStream_t s) {
     const int grid = grid_of(i0, i1);
     if (grid == 0) return cudaSuccess;
+    (void)cudaGetLastError();  // report this launch's error, not a stale one
     if (dtype == 0)
         k_update_adam<0><<<grid, kThreads, 0, s>>>(td, items, i0, reduced, inv_n, alpha_t, beta1,
                                                    beta2, c1, c2, eps);
@@ -491,6 +496,7 @@ cudaError_t launch_allreduce_oneshot(const PeerBufs &in, int world, void *out, i
                                      int64_t e1, int dtype, const Barrier &bar, int blocks,
                                      cudaStream_t s) {
     if (blocks <= 0 || blocks > kMaxBarrierBlocks) return cudaErrorInvalidValue;
+    (void)cudaGetLastError();
     const int64_t v0 = to_vec(e0, dtype), v1 = to_vec(e1, dtype);
     const bool ok = dtype == 0 ? oneshot_dispatch<0>(world, in, out, v0, v1, bar, blocks, s)
                                : oneshot_dispatch<1>(world, in, out, v0, v1, bar, blocks, s);
@@ -502,6 +508,7 @@ cudaError_t launch_allreduce_twoshot(const PeerBufs &in, const PeerBufs &red, in
                                      int dtype, int phases, const Barrier &bar, int blocks,
                                      cudaStream_t s) {
     if (blocks <= 0 || blocks > kMaxBarrierBlocks) return cudaErrorInvalidValue;
+    (void)cudaGetLastError();
     Chunks ch{};
     for (int p = 0; p < world; ++p) {
         ch.s[p] = to_vec(chunk_start[p], dtype);

@@ -93,6 +93,7 @@ struct NcclApi {
 NcclApi g_nccl;
 constexpr int kNcclUniqueIdBytes = 128;
 constexpr int kNcclFloat16 = 6, kNcclFloat32 = 7, kNcclSum = 0;
+constexpr int kE2EPieces = 8;   // pipeline depth of the host-buffer step
 
 }  // namespace
 
@@ -152,6 +153,9 @@ struct cmn_comm {
     std::vector<char> bucket_fresh;
     std::vector<ArResult> bucket_res;
     void *nccl = nullptr;
+    bool params_flat = false;             // params are views of one packed-layout allocation
+    cudaStream_t h2d = nullptr, d2h = nullptr;   // e2e copy streams (lazily)
+    std::vector<cudaEvent_t> ev;
 };
 
 namespace {
@@ -526,26 +530,77 @@ cmn_status init_common(int rank, int world, int dev, bool sim, cmn_allgather_fn 
     return CMN_OK;
 }
 
-// Coalesced host<->device copies of per-tensor buffers laid out like the
-// packed layout (runs where both sides advance by off[t+1] - off[t]).
-cmn_status copy_tensors(cmn_comm *c, const float *const *src, float *const *dst, int T,
+// Per-tensor host<->device copies (no coalescing across tensors: separate
+// host allocations may happen to be adjacent, and one cudaMemcpy may not span
+// two of them).
+cmn_status copy_tensors(cmn_comm *c, const float *const *src, float *const *dst, int ta, int tb,
                         cudaMemcpyKind kind, cudaStream_t s) {
-    int t = 0;
-    while (t < T) {
-        if (c->numel[t] == 0) {
-            ++t;
-            continue;
-        }
-        int u = t;
-        while (u + 1 < T && c->numel[u + 1] > 0 &&
-               src[u + 1] == src[u] + (c->off[u + 1] - c->off[u]) &&
-               dst[u + 1] == dst[u] + (c->off[u + 1] - c->off[u]))
-            ++u;
-        const size_t bytes = static_cast<size_t>(c->off[u] - c->off[t] + c->numel[u]) * 4;
-        CMN_CUDA(cudaMemcpyAsync(dst[t], src[t], bytes, kind, s));
-        t = u + 1;
+    for (int t = ta; t < tb; ++t) {
+        if (c->numel[t] == 0) continue;
+        CMN_CUDA(cudaMemcpyAsync(dst[t], src[t], static_cast<size_t>(c->numel[t]) * 4, kind, s));
     }
     return CMN_OK;
+}
+
+// Are the registered params views of ONE device allocation laid out like the
+// packed layout (params[t] == params[0] + off[t])?  Then host<->device copies
+// of parameter ranges may be single cudaMemcpys.  Verified with the driver's
+// cuMemGetAddressRange so adjacency by accident is not mistaken for it.
+bool params_are_flat(const cmn_comm *c) {
+    if (c->T == 0 || !c->params[0]) return false;
+    for (int t = 0; t < c->T; ++t)
+        if (c->numel[t] > 0 && c->params[t] != c->params[0] + c->off[t]) return false;
+    using Fn = int (*)(unsigned long long *, size_t *, unsigned long long);
+    void *fp = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fp, cudaEnableDefault, &q) != cudaSuccess ||
+        !fp)
+        return false;
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (reinterpret_cast<Fn>(fp)(&base, &size, reinterpret_cast<unsigned long long>(c->params[0])) != 0)
+        return false;
+    const unsigned long long lo = reinterpret_cast<unsigned long long>(c->params[0]);
+    int last = c->T - 1;
+    while (last > 0 && c->numel[last] == 0) --last;
+    const unsigned long long hi =
+        reinterpret_cast<unsigned long long>(c->params[last] + c->numel[last]);
+    return lo >= base && hi <= base + size;
+}
+
+cmn_status ensure_staging(cmn_comm *c) {
+    if (c->d_staging) return CMN_OK;
+    const int nsim = c->simulated ? c->world : 1;
+    const size_t b = static_cast<size_t>(c->L > 0 ? c->L : 1) * 4 * nsim;
+    if (cudaMalloc(&c->d_staging, b) != cudaSuccess) return fail(CMN_ERR_OOM, "staging alloc");
+    return CMN_OK;
+}
+
+cmn_status ensure_side_streams(cmn_comm *c) {
+    if (c->h2d) return CMN_OK;
+    CMN_CUDA(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+    CMN_CUDA(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+    c->ev.resize(3 * kE2EPieces + 2);
+    for (auto &e : c->ev) CMN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return CMN_OK;
+}
+
+// Tensor ranges of roughly equal bytes for the pipelined e2e step.
+std::vector<std::pair<int, int>> e2e_pieces(const cmn_comm *c) {
+    std::vector<std::pair<int, int>> out;
+    const int64_t target = (c->L + kE2EPieces - 1) / kE2EPieces;
+    int t = 0;
+    while (t < c->T) {
+        int u = t;
+        int64_t acc = 0;
+        while (u < c->T && (acc < target || static_cast<int>(out.size()) + 1 == kE2EPieces)) {
+            acc += c->numel[u];
+            ++u;
+        }
+        out.emplace_back(t, u);
+        t = u;
+    }
+    return out;
 }
 
 }  // namespace
@@ -579,6 +634,9 @@ cmn_status cmn_finalize(cmn_comm *c) {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     if (c->nccl && g_nccl.CommDestroy) g_nccl.CommDestroy(c->nccl);
+    for (auto e : c->ev) cudaEventDestroy(e);
+    if (c->h2d) cudaStreamDestroy(c->h2d);
+    if (c->d2h) cudaStreamDestroy(c->d2h);
     free_registration(c);
     if (c->h_err) cudaFreeHost(c->h_err);
     delete c;
@@ -609,6 +667,7 @@ cmn_status cmn_register_params(cmn_comm *c, int T, const int *ndims, const int64
         c->L = off[T];
         c->hash = hash;
         c->params.assign(params, params + T);
+        c->params_flat = params_are_flat(c);
         c->seq = 0;
 
         // Work items: each tensor cut into kItemElems pieces.
@@ -721,11 +780,8 @@ cmn_status cmn_step_host(cmn_comm *c, const float *const *host_grads, float *con
         if (c->numel[i % c->T] > 0 && !host_grads[i])
             return fail(CMN_ERR_INVALID_ARG, "host grad pointer is NULL");
     if (cmn_status st = set_device(c); st != CMN_OK) return st;
+    if (cmn_status st = ensure_staging(c); st != CMN_OK) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (!c->d_staging) {
-        const size_t b = static_cast<size_t>(c->L > 0 ? c->L : 1) * 4 * nsim;
-        if (cudaMalloc(&c->d_staging, b) != cudaSuccess) return fail(CMN_ERR_OOM, "staging alloc");
-    }
     std::vector<const float *> dg(static_cast<size_t>(nsim) * c->T);
     for (int i = 0; i < nsim; ++i) {
         std::vector<float *> dst(c->T);
@@ -734,17 +790,104 @@ cmn_status cmn_step_host(cmn_comm *c, const float *const *host_grads, float *con
             dg[static_cast<size_t>(i) * c->T + t] = dst[t];
         }
         if (cmn_status st = copy_tensors(c, host_grads + static_cast<size_t>(i) * c->T, dst.data(),
-                                         c->T, cudaMemcpyHostToDevice, s);
+                                         0, c->T, cudaMemcpyHostToDevice, s);
             st != CMN_OK)
             return st;
     }
     if (cmn_status st = cmn_step(c, dg.data(), dtype, lr, mu, stream); st != CMN_OK) return st;
     if (host_params) {
         std::vector<const float *> src(c->params.begin(), c->params.end());
-        if (cmn_status st = copy_tensors(c, src.data(), host_params, c->T, cudaMemcpyDeviceToHost, s);
+        if (cmn_status st = copy_tensors(c, src.data(), host_params, 0, c->T,
+                                         cudaMemcpyDeviceToHost, s);
             st != CMN_OK)
             return st;
     }
+    return CMN_OK;
+}
+
+cmn_status cmn_step_host_packed(cmn_comm *c, const float *host_grads, float *host_params,
+                                cmn_dtype dtype, float lr, float mu, void *stream) {
+    if (cmn_status st = require_registered(c); st != CMN_OK) return st;
+    if (cmn_status st = require_dtype(dtype); st != CMN_OK) return st;
+    if (!host_grads) return fail(CMN_ERR_INVALID_ARG, "host_grads is NULL");
+    if (cmn_status st = set_device(c); st != CMN_OK) return st;
+    if (cmn_status st = ensure_staging(c); st != CMN_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int nsim = c->simulated ? c->world : 1;
+    std::vector<const float *> dg(static_cast<size_t>(nsim) * c->T);
+    for (int i = 0; i < nsim; ++i)
+        for (int t = 0; t < c->T; ++t)
+            dg[static_cast<size_t>(i) * c->T + t] = c->d_staging + static_cast<size_t>(i) * c->L + c->off[t];
+    std::string why;
+    if (!grads_ok(c, dg.data(), nsim * c->T, why)) return fail(CMN_ERR_INVALID_ARG, why);
+
+    if (c->world > 1 || c->simulated) {
+        // Unpipelined: the all-reduce needs every gradient first.
+        CMN_CUDA(cudaMemcpyAsync(c->d_staging, host_grads, static_cast<size_t>(c->L) * 4 * nsim,
+                                 cudaMemcpyHostToDevice, s));
+        if (cmn_status st = cmn_step(c, dg.data(), dtype, lr, mu, stream); st != CMN_OK) return st;
+        if (host_params) {
+            if (c->params_flat) {
+                CMN_CUDA(cudaMemcpyAsync(host_params, c->params[0], static_cast<size_t>(c->L) * 4,
+                                         cudaMemcpyDeviceToHost, s));
+            } else {
+                std::vector<float *> hp(c->T);
+                for (int t = 0; t < c->T; ++t) hp[t] = host_params + c->off[t];
+                std::vector<const float *> src(c->params.begin(), c->params.end());
+                if (cmn_status st = copy_tensors(c, src.data(), hp.data(), 0, c->T,
+                                                 cudaMemcpyDeviceToHost, s);
+                    st != CMN_OK)
+                    return st;
+            }
+        }
+        return CMN_OK;
+    }
+
+    // N = 1: pipeline H2D(piece p+1) || update(piece p) || D2H(piece p-1) on
+    // two copy engines and the caller's stream.
+    if (cmn_status st = ensure_side_streams(c); st != CMN_OK) return st;
+    const auto pieces = e2e_pieces(c);
+    cudaEvent_t entry = c->ev[0], done_d2h = c->ev[1];
+    CMN_CUDA(cudaEventRecord(entry, s));
+    CMN_CUDA(cudaStreamWaitEvent(c->h2d, entry, 0));
+    CMN_CUDA(cudaStreamWaitEvent(c->d2h, entry, 0));
+    c->fresh = false;
+    for (size_t p = 0; p < pieces.size(); ++p) {
+        const int ta = pieces[p].first, tb = pieces[p].second;
+        const int64_t e0 = c->off[ta], e1 = c->off[tb];
+        cudaEvent_t ev_in = c->ev[2 + 3 * p], ev_upd = c->ev[3 + 3 * p];
+        CMN_CUDA(cudaMemcpyAsync(c->d_staging + e0, host_grads + e0, static_cast<size_t>(e1 - e0) * 4,
+                                 cudaMemcpyHostToDevice, c->h2d));
+        CMN_CUDA(cudaEventRecord(ev_in, c->h2d));
+        CMN_CUDA(cudaStreamWaitEvent(s, ev_in, 0));
+        cmn_status st = for_groups(c, ta, tb, [&](int lo, int hi, int i0, int i1) {
+            return launched(c,
+                            launch_update_direct(make_tab(dg.data(), lo, hi), lo, c->d_td,
+                                                 c->d_items, i0, i1, dtype, lr, mu, s),
+                            "update_direct");
+        });
+        if (st != CMN_OK) return st;
+        if (host_params) {
+            CMN_CUDA(cudaEventRecord(ev_upd, s));
+            CMN_CUDA(cudaStreamWaitEvent(c->d2h, ev_upd, 0));
+            if (c->params_flat) {
+                CMN_CUDA(cudaMemcpyAsync(host_params + e0, c->params[0] + e0,
+                                         static_cast<size_t>(e1 - e0) * 4, cudaMemcpyDeviceToHost,
+                                         c->d2h));
+            } else {
+                std::vector<float *> hp(c->T);
+                for (int t = ta; t < tb; ++t) hp[t] = host_params + c->off[t];
+                std::vector<const float *> src(c->params.begin(), c->params.end());
+                if (cmn_status st2 = copy_tensors(c, src.data(), hp.data(), ta, tb,
+                                                  cudaMemcpyDeviceToHost, c->d2h);
+                    st2 != CMN_OK)
+                    return st2;
+            }
+        }
+    }
+    CMN_CUDA(cudaEventRecord(done_d2h, c->d2h));
+    CMN_CUDA(cudaStreamWaitEvent(s, done_d2h, 0));
+    // the H2D stream is joined through the per-piece waits already
     return CMN_OK;
 }
 

@@ -1,0 +1,103 @@
+"""The real multi-process path (cmn_init: CUDA-IPC peer mapping, per-CTA
+release/acquire barriers across processes) with 2 and 3 ranks sharing one
+GPU (the only configuration gpurun offers): each process owns its buffers,
+peers read them through IPC mappings exactly as over NVSwitch.  Results are
+compared bit-exact with the oracle and across ranks (replica consistency,
+SPEC.md:608).  Contexts time-slice on one device, so barriers are slow but
+correct; every spin is bounded by the device timeout."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, dtype, algo, steps, q, mode):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1908_00213_b200 import cmn
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    try:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        shapes = synth.mlp_shapes()
+        if mode == "mismatch" and rank == 1:
+            shapes = shapes[:-1] + [(11,)]
+        comm = cmn.Comm.init(rank, world, 0, dist.group.WORLD)
+        comm.set_timeout(60000)
+        w = [torch.from_numpy(p).cuda() for p in synth.params(shapes)]
+        try:
+            comm.register_params(w)
+        except cmn.CmnError as e:
+            q.put((rank, "error", e.status_name))
+            return
+        comm.set_algo(algo)
+        for s in range(steps):
+            g = [torch.from_numpy(x).cuda() for x in synth.grads(shapes, workers=world, step=s)[rank]]
+            comm.allreduce_grads(g, dtype)
+            comm.update_momentum_sgd(0.1, 0.9)
+        torch.cuda.synchronize()
+        comm.poll_error()
+        wb = np.concatenate([x.cpu().numpy().reshape(-1) for x in w])
+        vb = np.concatenate([comm.momentum(t).cpu().numpy().reshape(-1) for t in range(len(w))])
+        q.put((rank, "ok", wb.tobytes(), vb.tobytes()))
+        comm.finalize()
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, "exc", repr(e)))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def _run(world, dtype, algo, steps=2, mode="same"):
+    from paper_1908_00213_b200 import build
+    build.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, dtype, algo, steps, q, mode))
+          for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=120)
+    return sorted(res, key=lambda r: r[0])
+
+
+@pytest.mark.parametrize("world,dtype,algo", [(2, "fp32", "oneshot"), (2, "fp16", "twoshot"),
+                                              (3, "fp32", "twoshot"), (3, "fp16", "oneshot")])
+def test_ipc_multiprocess_parity(orc, world, dtype, algo):
+    res = _run(world, dtype, algo)
+    assert all(r[1] == "ok" for r in res), res
+    shapes = synth.mlp_shapes()
+    w = synth.params(shapes)
+    v = [np.zeros_like(x) for x in w]
+    for s in range(2):
+        orc.step(synth.grads(shapes, workers=world, step=s), w, v, 0.1, 0.9, dtype)
+    want_w = np.concatenate(w).view(np.uint32)
+    want_v = np.concatenate(v).view(np.uint32)
+    for r in res:
+        assert np.array_equal(np.frombuffer(r[2], np.uint32), want_w), f"rank {r[0]} w"
+        assert np.array_equal(np.frombuffer(r[3], np.uint32), want_v), f"rank {r[0]} v"
+
+
+def test_ipc_structure_mismatch_detected():
+    res = _run(2, "fp32", "oneshot", mode="mismatch")
+    assert [r[1] for r in res] == ["error", "error"]
+    assert all(r[2] == "CMN_ERR_MISMATCH" for r in res)

@@ -322,6 +322,70 @@ def test_step_host_e2e_parity(cmn, orc):
         comm.finalize()
 
 
+@pytest.mark.parametrize("flat_params", [True, False])
+@pytest.mark.parametrize("dtype", ["fp32", "fp16"])
+def test_step_host_packed_pipelined_parity(cmn, orc, flat_params, dtype):
+    """cmn_step_host_packed at N = 1 (pipelined over tensor ranges, two copy
+    streams) over 3 steps, params as one flat allocation or separate ones."""
+    shapes = synth.resnet50_shapes()[:60]
+    sizes = [synth.numel(s) for s in shapes]
+    off, L = orc.layout(sizes)
+    params0 = synth.params(shapes)
+    w_o = [p.copy() for p in params0]
+    v_o = [np.zeros_like(p) for p in params0]
+    comm = cmn.Comm.init(0, 1, 0)
+    try:
+        if flat_params:
+            flat = torch.zeros(L, dtype=torch.float32, device=DEV)
+            w = [flat[off[t]: off[t] + sizes[t]].view(shapes[t]) for t in range(len(shapes))]
+            for t in range(len(w)):
+                w[t].copy_(torch.from_numpy(params0[t]).view(shapes[t]))
+        else:
+            w = [torch.from_numpy(p.copy()).to(DEV) for p in params0]
+        comm.register_params(w)
+        hg = torch.zeros(L, dtype=torch.float32).pin_memory()
+        hw = torch.full((L,), float("nan"), dtype=torch.float32).pin_memory()
+        for s in range(3):
+            g = synth.grads(shapes, workers=1, step=s)
+            for t in range(len(g[0])):
+                hg[off[t]: off[t] + sizes[t]].copy_(torch.from_numpy(g[0][t]))
+            orc.step(g, w_o, v_o, 0.1, 0.9, dtype)
+            comm.step_host_packed(hg, hw, dtype, 0.1, 0.9)
+            torch.cuda.synchronize()
+            hwn = hw.numpy()
+            for t in range(len(w_o)):
+                assert_bitwise(hwn[off[t]: off[t] + sizes[t]].copy(), w_o[t], f"host w[{t}] step {s}")
+    finally:
+        comm.finalize()
+
+
+def test_step_host_packed_simulated(cmn, orc):
+    shapes = synth.mlp_shapes()
+    N = 4
+    sizes = [synth.numel(s) for s in shapes]
+    off, L = orc.layout(sizes)
+    g = synth.grads(shapes, workers=N)
+    params0 = synth.params(shapes)
+    w_o = [p.copy() for p in params0]
+    v_o = [np.zeros_like(p) for p in params0]
+    orc.step(g, w_o, v_o, 0.1, 0.9, "fp32")
+    comm = cmn.Comm.simulated_world(N)
+    try:
+        w = to_dev(params0)
+        comm.register_params(w)
+        hg = torch.zeros(N * L, dtype=torch.float32).pin_memory()
+        for i in range(N):
+            for t in range(len(sizes)):
+                hg[i * L + off[t]: i * L + off[t] + sizes[t]].copy_(torch.from_numpy(g[i][t]))
+        hw = torch.empty(L, dtype=torch.float32).pin_memory()
+        comm.step_host_packed(hg, hw, "fp32", 0.1, 0.9)
+        torch.cuda.synchronize()
+        for t in range(len(sizes)):
+            assert_bitwise(hw.numpy()[off[t]: off[t] + sizes[t]].copy(), w_o[t], f"w[{t}]")
+    finally:
+        comm.finalize()
+
+
 def test_errors_are_loud(cmn):
     shapes = synth.mlp_shapes()
     comm = cmn.Comm.simulated_world(2)
