@@ -130,6 +130,19 @@ def _data_ptrs(tensors) -> list:
     return out
 
 
+class PtrTable:
+    """Pre-marshalled pointer table (gradients registered once and reused
+    every step, as a framework's persistent .grad buffers are): building it
+    costs ~1 us per tensor in Python, so hot loops build it once."""
+
+    def __init__(self, tensors):
+        if tensors and isinstance(tensors[0], (list, tuple)):
+            tensors = [g for gw in tensors for g in gw]
+        self.tensors = list(tensors)          # keep the storage alive
+        self.n = len(self.tensors)
+        self.arr = _ptr_array(_data_ptrs(self.tensors))
+
+
 class _DevArray:
     """Zero-copy __cuda_array_interface__ wrapper for library-owned memory."""
 
@@ -243,7 +256,13 @@ class Comm:
         return list(off), L.value
 
     # the step ---------------------------------------------------------------
+    def prepare(self, grads) -> PtrTable:
+        """Marshal a gradient table once (see PtrTable)."""
+        return PtrTable(grads)
+
     def _grad_table(self, grads):
+        if isinstance(grads, PtrTable):
+            return grads.arr
         if self.simulated and grads and isinstance(grads[0], (list, tuple)):
             flat = [g for gw in grads for g in gw]
         else:

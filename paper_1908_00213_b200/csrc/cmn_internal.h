@@ -28,12 +28,17 @@ struct TensorDesc {
     int64_t off_next;  // off of tensor t+1 (= end of this tensor's pad)
 };
 
-// A contiguous piece of one tensor: elements [k0, k0 + len) of tensor t.
-// len <= kItemElems, k0 is a multiple of kItemElems.
+// A contiguous piece of one tensor: elements [k0, k0 + len) of tensor t,
+// packed at [base, base + len) (base = off_t + k0).  len <= kItemElems, k0 is
+// a multiple of kItemElems; pad > 0 only on a tensor's last item: the number
+// of alignment-pad elements that follow it in the packed layout.
 struct Item {
     int32_t t;
     int32_t len;
     int64_t k0;
+    int64_t base;
+    int32_t pad;
+    int32_t reserved;
 };
 
 // Grad pointers for the tensors [t_lo, t_lo + kGradCap) of one launch.

@@ -62,50 +62,64 @@ __device__ __forceinline__ float load_r1(const void *r, int64_t j) {
 }
 
 // ------------------------------------------------------------------- a1
+// Each CTA packs kPackItems consecutive items; all of their loads are issued
+// before the first store (16 x 16 B in flight per thread), so the short
+// load->store lifetime of a CTA does not leave HBM idle.
+constexpr int kPackItems = 4;
+
+template <int DT>
+__device__ __forceinline__ void pack_store(void *packed, int64_t j, const float4 &x) {
+    if constexpr (DT == 0) {
+        st_cs_f4(static_cast<float *>(packed) + j, x);
+    } else {
+        st_cs_u2(static_cast<uint16_t *>(packed) + j,
+                 make_uint2(pack_half2(x.x, x.y), pack_half2(x.z, x.w)));
+    }
+}
+
 template <int DT>
 __global__ void __launch_bounds__(kThreads) k_pack(GradTab g, int t_lo,
-                                                   const TensorDesc *__restrict__ td,
-                                                   const Item *__restrict__ items, int i0,
+                                                   const Item *__restrict__ items, int i0, int i1,
                                                    void *__restrict__ packed) {
-    const Item it = items[i0 + blockIdx.x];
-    const int64_t off = td[it.t].off;
-    const float *__restrict__ src = g.p[it.t - t_lo] + it.k0;
-    const int64_t base = off + it.k0;
-    const int nv = it.len >> 2;
-
-    float4 x[kVecPerThread];
+    const int ib = i0 + blockIdx.x * kPackItems;
+    float4 x[kPackItems][kVecPerThread];
 #pragma unroll
-    for (int u = 0; u < kVecPerThread; ++u) {
-        const int v = threadIdx.x + u * kThreads;
-        if (v < nv) x[u] = ld_cs_f4(src + 4 * v);
-    }
+    for (int j = 0; j < kPackItems; ++j) {
+        if (ib + j < i1) {
+            const Item it = items[ib + j];
+            const float *__restrict__ src = g.p[it.t - t_lo] + it.k0;
+            const int nv = it.len >> 2;
 #pragma unroll
-    for (int u = 0; u < kVecPerThread; ++u) {
-        const int v = threadIdx.x + u * kThreads;
-        if (v < nv) {
-            if constexpr (DT == 0) {
-                st_cs_f4(static_cast<float *>(packed) + base + 4 * v, x[u]);
-            } else {
-                st_cs_u2(static_cast<uint16_t *>(packed) + base + 4 * v,
-                         make_uint2(pack_half2(x[u].x, x[u].y), pack_half2(x[u].z, x[u].w)));
+            for (int u = 0; u < kVecPerThread; ++u) {
+                const int v = threadIdx.x + u * kThreads;
+                if (v < nv) x[j][u] = ld_cs_f4(src + 4 * v);
             }
         }
     }
-    for (int k = (nv << 2) + threadIdx.x; k < it.len; k += kThreads) {
-        const float s = src[k];
-        if constexpr (DT == 0)
-            static_cast<float *>(packed)[base + k] = s;
-        else
-            static_cast<uint16_t *>(packed)[base + k] = __half_as_ushort(__float2half_rn(s));
-    }
-    // The item holding the tensor's last element zeroes the alignment pad.
-    const TensorDesc &d = td[it.t];
-    if (it.k0 + it.len == d.n) {
-        for (int64_t j = d.off + d.n + threadIdx.x; j < d.off_next; j += kThreads) {
+#pragma unroll
+    for (int j = 0; j < kPackItems; ++j) {
+        if (ib + j >= i1) break;
+        const Item it = items[ib + j];
+        const int nv = it.len >> 2;
+#pragma unroll
+        for (int u = 0; u < kVecPerThread; ++u) {
+            const int v = threadIdx.x + u * kThreads;
+            if (v < nv) pack_store<DT>(packed, it.base + 4 * v, x[j][u]);
+        }
+        // ragged tail (numel % 4) and the alignment pad after the tensor
+        const float *__restrict__ src = g.p[it.t - t_lo] + it.k0;
+        for (int k = (nv << 2) + threadIdx.x; k < it.len; k += kThreads) {
+            const float sv = src[k];
             if constexpr (DT == 0)
-                static_cast<float *>(packed)[j] = 0.0f;
+                static_cast<float *>(packed)[it.base + k] = sv;
             else
-                static_cast<uint16_t *>(packed)[j] = 0;
+                static_cast<uint16_t *>(packed)[it.base + k] = __half_as_ushort(__float2half_rn(sv));
+        }
+        for (int k = threadIdx.x; k < it.pad; k += kThreads) {
+            if constexpr (DT == 0)
+                static_cast<float *>(packed)[it.base + it.len + k] = 0.0f;
+            else
+                static_cast<uint16_t *>(packed)[it.base + it.len + k] = 0;
         }
     }
 }
@@ -381,13 +395,15 @@ inline int grid_of(int i0, int i1) { return i1 > i0 ? i1 - i0 : 0; }
 
 cudaError_t launch_pack(const GradTab &g, int t_lo, const TensorDesc *td, const Item *items,
                         int i0, int i1, int dtype, void *packed, cudaStream_t s) {
-    const int grid = grid_of(i0, i1);
-    if (grid == 0) return cudaSuccess;
+    const int n = grid_of(i0, i1);
+    if (n == 0) return cudaSuccess;
+    (void)td;
     (void)cudaGetLastError();  // report this launch's error, not a stale one
+    const int grid = (n + kPackItems - 1) / kPackItems;
     if (dtype == 0)
-        k_pack<0><<<grid, kThreads, 0, s>>>(g, t_lo, td, items, i0, packed);
+        k_pack<0><<<grid, kThreads, 0, s>>>(g, t_lo, items, i0, i1, packed);
     else
-        k_pack<1><<<grid, kThreads, 0, s>>>(g, t_lo, td, items, i0, packed);
+        k_pack<1><<<grid, kThreads, 0, s>>>(g, t_lo, items, i0, i1, packed);
     return cudaGetLastError();
 }
 

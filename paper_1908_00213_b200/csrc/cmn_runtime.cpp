@@ -677,7 +677,10 @@ cmn_status cmn_register_params(cmn_comm *c, int T, const int *ndims, const int64
             c->item_begin[t] = static_cast<int>(c->h_items.size());
             for (int64_t k0 = 0; k0 < numel[t]; k0 += kItemElems) {
                 const int64_t len = numel[t] - k0 < kItemElems ? numel[t] - k0 : kItemElems;
-                c->h_items.push_back(Item{t, static_cast<int32_t>(len), k0});
+                const bool last = k0 + len == numel[t];
+                c->h_items.push_back(Item{t, static_cast<int32_t>(len), k0, off[t] + k0,
+                                          last ? static_cast<int32_t>(off[t + 1] - off[t] - numel[t]) : 0,
+                                          0});
             }
         }
         c->item_begin[T] = static_cast<int>(c->h_items.size());

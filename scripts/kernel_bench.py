@@ -1,0 +1,118 @@
+#!/usr/bin/env python
+"""Per-kernel timings of the step's kernels on ONE GPU (simulated-N mode):
+pack (a1), all-reduce (a2, local HBM stands in for NVLink), update (a3), and
+the fused N = 1 step -- each against its HBM roofline (algorithmic bytes /
+CUDA-event time vs MEASURED_PEAKS.json hbm_gbs).  Prints one JSON line per
+measurement; used to fill profiles/ and DESIGN.md §6.
+
+    python scripts/kernel_bench.py [--iters 50]
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+from paper_1908_00213_b200 import Comm  # noqa: E402
+
+
+def timed(fn, iters, stream):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(iters):
+        fn()
+    b.record(stream)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / iters * 1e3   # us
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--iters", type=int, default=50)
+    ap.add_argument("--worlds", default="1,2,4,8")
+    args = ap.parse_args()
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    shapes = synth.resnet50_shapes()
+    sizes = [synth.numel(s) for s in shapes]
+    P = sum(sizes)
+    dev = "cuda:0"
+    stream = torch.cuda.current_stream()
+    params0 = synth.params(shapes)
+    for N in [int(x) for x in args.worlds.split(",")]:
+        g_host = synth.grads(shapes, workers=N)
+        g = [[torch.from_numpy(x).to(dev) for x in gw] for gw in g_host]
+        for dtype in ("fp32", "fp16"):
+            c = 4 if dtype == "fp32" else 2
+            for algo in (("oneshot", "twoshot") if N > 1 else ("identity",)):
+                comm = Comm.simulated_world(N) if N > 1 else Comm.init(0, 1, 0)
+                w = [torch.from_numpy(p.copy()).to(dev) for p in params0]
+                comm.register_params(w)
+                if N > 1:
+                    comm.set_algo(algo)
+                _, L = comm.layout()
+                gg = comm.prepare(g if N > 1 else g[0])
+
+                def ar():
+                    comm.allreduce_grads(gg, dtype)
+
+                def upd():
+                    comm.allreduce_grads(gg, dtype)
+                    comm.update_momentum_sgd(0.1, 0.9)
+
+                t_ar = timed(ar, args.iters, stream)
+                t_both = timed(upd, args.iters, stream)
+                t_upd = t_both - t_ar
+                rec = {"N": N, "dtype": dtype, "algo": algo,
+                       "allreduce_incl_pack_us": t_ar, "update_us": t_upd,
+                       "update_gbs": (16 + c) * P / (t_upd * 1e-6) / 1e9,
+                       "update_frac": (16 + c) * P / (t_upd * 1e-6) / 1e9 / peak}
+                if N == 1:
+                    rec["pack_gbs"] = (4 + c) * P / (t_ar * 1e-6) / 1e9
+                    rec["pack_frac"] = rec["pack_gbs"] / peak
+
+                    def step():
+                        comm.step(gg, dtype, 0.1, 0.9)
+                    t_step = timed(step, args.iters, stream)
+                    import time as _t
+                    torch.cuda.synchronize()
+                    h0 = _t.perf_counter()
+                    for _ in range(args.iters):
+                        comm.step(gg, dtype, 0.1, 0.9)
+                    h1 = _t.perf_counter()
+                    torch.cuda.synchronize()
+                    rec["host_us_per_step_call"] = (h1 - h0) / args.iters * 1e6
+                    # same step captured once into a CUDA graph and replayed
+                    gr = torch.cuda.CUDAGraph()
+                    s2 = torch.cuda.Stream()
+                    s2.wait_stream(stream)
+                    with torch.cuda.stream(s2):
+                        comm.step(gg, dtype, 0.1, 0.9, s2)
+                    torch.cuda.synchronize()
+                    with torch.cuda.graph(gr):
+                        comm.step(gg, dtype, 0.1, 0.9)
+                    t_graph = timed(gr.replay, args.iters, stream)
+                    rec["graph_step_us"] = t_graph
+                    rec["fused_step_us"] = t_step
+                    rec["fused_step_gbs"] = 20 * P / (t_step * 1e-6) / 1e9
+                    rec["fused_step_frac"] = rec["fused_step_gbs"] / peak
+                else:
+                    # simulated: N packs + N (oneshot) or 2N (twoshot) launches, all local HBM
+                    rec["sim_note"] = "all N ranks' kernels on one GPU; local HBM stands in for NVLink"
+                print(json.dumps(rec), flush=True)
+                comm.finalize()
+                del w
+        del g
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
