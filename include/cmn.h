@@ -256,6 +256,15 @@ cmn_status cmn_update_bucket(cmn_comm *comm, int bucket, float lr, float mu, voi
  * (payload bytes; 0 keeps the default).  Takes effect on the next call. */
 cmn_status cmn_set_algo(cmn_comm *comm, cmn_algo algo, size_t oneshot_max_bytes);
 
+/* cmn_set_pipeline -- N > 1 cmn_step schedule: `pieces` >= 2 cuts the model
+ * into that many contiguous, equal-byte tensor ranges, each its own
+ * collective call; packs and updates run on `stream` while the all-reduces
+ * run on an internal high-priority stream, so HBM work overlaps NVLink
+ * transfer (results are bitwise identical: every element's arithmetic is
+ * unchanged).  0 or 1 = unpipelined (pack, all-reduce, update in sequence).
+ * Default 4 (env CMN_PIECES).  Every rank must use the same value. */
+cmn_status cmn_set_pipeline(cmn_comm *comm, int pieces);
+
 /* cmn_set_timeout -- device spin-wait timeout in milliseconds (default
  * 30000). */
 cmn_status cmn_set_timeout(cmn_comm *comm, uint32_t timeout_ms);

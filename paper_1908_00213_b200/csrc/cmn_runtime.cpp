@@ -156,6 +156,11 @@ struct cmn_comm {
     bool params_flat = false;             // params are views of one packed-layout allocation
     cudaStream_t h2d = nullptr, d2h = nullptr;   // e2e copy streams (lazily)
     std::vector<cudaEvent_t> ev;
+    // pipelined N > 1 step: pack(p+1) and update(p-1) on the caller's stream
+    // overlap all-reduce(p) on a high-priority communication stream.
+    int pipe_pieces = 4;
+    cudaStream_t sc = nullptr;
+    std::vector<cudaEvent_t> pev;
 };
 
 namespace {
@@ -373,22 +378,11 @@ void chunk_plan(int64_t e0, int64_t e1, int world, int64_t *s, int64_t *e) {
     }
 }
 
-// a1 + a2 over the tensor range [ta, tb) (whole model or one bucket).
-cmn_status allreduce_range(cmn_comm *c, int ta, int tb, const float *const *grads, int dtype,
-                           cudaStream_t s) {
-    if (cmn_status st = check_async_error(c); st != CMN_OK) return st;
-    const int64_t e0 = c->off[ta], e1 = c->off[tb];
-    const size_t esz = dtype == 0 ? 4 : 2;
-    const size_t bytes = static_cast<size_t>(e1 - e0) * esz;
-    cmn_algo algo = choose_algo(c, bytes);
-    if (algo == CMN_ALGO_NCCL && (c->simulated || !c->nccl))
-        return fail(CMN_ERR_STATE, "NCCL algorithm requested but no NCCL communicator "
-                                   "(cmn_set_algo(CMN_ALGO_NCCL) on every rank of a cmn_init comm)");
-    ++c->seq;
-    const int par = static_cast<int>(c->seq & 1u);
+// a1: pack every (simulated) rank's gradients of tensors [ta, tb) into its
+// packed buffer of parity `par`.
+cmn_status pack_phase(cmn_comm *c, int ta, int tb, const float *const *grads, int dtype, int par,
+                      cudaStream_t s) {
     const int nsim = c->simulated ? c->world : 1;
-
-    // a1: pack every (simulated) rank's gradients into its packed buffer.
     for (int i = 0; i < nsim; ++i) {
         const int r = c->simulated ? i : c->rank;
         const float *const *g = grads + static_cast<size_t>(i) * c->T;
@@ -400,11 +394,19 @@ cmn_status allreduce_range(cmn_comm *c, int ta, int tb, const float *const *grad
         });
         if (st != CMN_OK) return st;
     }
+    return CMN_OK;
+}
 
-    c->last = ArResult{par, dtype, false};
-    if (c->world == 1) {
-        c->last.alias_packed = true;   // identity all-reduce (fp16 rounding done by the pack)
-    } else if (algo == CMN_ALGO_NCCL) {
+// a2 over the packed range of tensors [ta, tb) for the collective call with
+// sequence number `seq` (its buffers have parity seq & 1).
+cmn_status reduce_phase(cmn_comm *c, int ta, int tb, int dtype, uint32_t seq, cmn_algo algo,
+                        cudaStream_t s) {
+    const int par = static_cast<int>(seq & 1u);
+    const int64_t e0 = c->off[ta], e1 = c->off[tb];
+    const size_t esz = dtype == 0 ? 4 : 2;
+    const int nsim = c->simulated ? c->world : 1;
+    if (c->world == 1) return CMN_OK;   // identity (fp16 rounding done by the pack)
+    if (algo == CMN_ALGO_NCCL) {
         void *src = static_cast<char *>(c->rb[c->rank].packed[par]) + e0 * esz;
         void *dst = static_cast<char *>(c->rb[c->rank].reduced[par]) + e0 * esz;
         const int rc = g_nccl.AllReduce(src, dst, static_cast<size_t>(e1 - e0),
@@ -413,48 +415,68 @@ cmn_status allreduce_range(cmn_comm *c, int ta, int tb, const float *const *grad
         if (rc != 0)
             return fail(CMN_ERR_NCCL, std::string("ncclAllReduce: ") +
                                           (g_nccl.GetErrorString ? g_nccl.GetErrorString(rc) : "?"));
-    } else {
-        PeerBufs in{}, red{};
-        for (int r = 0; r < c->world; ++r) {
-            in.p[r] = c->rb[r].packed[par];
-            red.p[r] = c->rb[r].reduced[par];
+        return CMN_OK;
+    }
+    PeerBufs in{}, red{};
+    for (int r = 0; r < c->world; ++r) {
+        in.p[r] = c->rb[r].packed[par];
+        red.p[r] = c->rb[r].reduced[par];
+    }
+    const int blocks = ar_blocks_for(c);
+    const int tag = dtype | (algo == CMN_ALGO_TWOSHOT ? 2 : 0);
+    Barrier bar = make_barrier(c, tag);
+    bar.value = (seq << 2) | static_cast<uint32_t>(tag & 3);
+    if (algo == CMN_ALGO_ONESHOT) {
+        for (int i = 0; i < nsim; ++i) {
+            const int r = c->simulated ? i : c->rank;
+            cmn_status st = launched(c,
+                                     launch_allreduce_oneshot(in, c->world, c->rb[r].reduced[par],
+                                                              e0, e1, dtype, bar, blocks, s),
+                                     "allreduce_oneshot");
+            if (st != CMN_OK) return st;
         }
-        const int blocks = ar_blocks_for(c);
-        const int tag = dtype | (algo == CMN_ALGO_TWOSHOT ? 2 : 0);
-        const Barrier bar = make_barrier(c, tag);
-        if (algo == CMN_ALGO_ONESHOT) {
-            for (int i = 0; i < nsim; ++i) {
-                const int r = c->simulated ? i : c->rank;
-                cmn_status st = launched(
-                    c,
-                    launch_allreduce_oneshot(in, c->world, c->rb[r].reduced[par], e0, e1, dtype,
-                                             bar, blocks, s),
-                    "allreduce_oneshot");
+        return CMN_OK;
+    }
+    int64_t cs[kMaxWorld], ce[kMaxWorld];
+    chunk_plan(e0, e1, c->world, cs, ce);
+    if (c->simulated) {
+        for (int phase = 1; phase <= 2; ++phase)
+            for (int r = 0; r < c->world; ++r) {
+                cmn_status st = launched(c,
+                                         launch_allreduce_twoshot(in, red, c->world, r, cs, ce, dtype,
+                                                                  phase, bar, blocks, s),
+                                         "allreduce_twoshot");
                 if (st != CMN_OK) return st;
             }
-        } else {
-            int64_t cs[kMaxWorld], ce[kMaxWorld];
-            chunk_plan(e0, e1, c->world, cs, ce);
-            if (c->simulated) {
-                for (int phase = 1; phase <= 2; ++phase)
-                    for (int r = 0; r < c->world; ++r) {
-                        cmn_status st = launched(
-                            c,
-                            launch_allreduce_twoshot(in, red, c->world, r, cs, ce, dtype, phase,
-                                                     bar, blocks, s),
-                            "allreduce_twoshot");
-                        if (st != CMN_OK) return st;
-                    }
-            } else {
-                cmn_status st = launched(
-                    c,
+        return CMN_OK;
+    }
+    return launched(c,
                     launch_allreduce_twoshot(in, red, c->world, c->rank, cs, ce, dtype, 3, bar,
                                              blocks, s),
                     "allreduce_twoshot");
-                if (st != CMN_OK) return st;
-            }
-        }
-    }
+}
+
+// Validate and choose the algorithm for one collective over [ta, tb).
+cmn_status begin_collective(cmn_comm *c, int ta, int tb, int dtype, cmn_algo &algo) {
+    if (cmn_status st = check_async_error(c); st != CMN_OK) return st;
+    const size_t esz = dtype == 0 ? 4 : 2;
+    algo = choose_algo(c, static_cast<size_t>(c->off[tb] - c->off[ta]) * esz);
+    if (algo == CMN_ALGO_NCCL && (c->simulated || !c->nccl))
+        return fail(CMN_ERR_STATE, "NCCL algorithm requested but no NCCL communicator "
+                                   "(cmn_set_algo(CMN_ALGO_NCCL) on every rank of a cmn_init comm)");
+    return CMN_OK;
+}
+
+// a1 + a2 over the tensor range [ta, tb) (whole model or one bucket).
+cmn_status allreduce_range(cmn_comm *c, int ta, int tb, const float *const *grads, int dtype,
+                           cudaStream_t s) {
+    cmn_algo algo;
+    if (cmn_status st = begin_collective(c, ta, tb, dtype, algo); st != CMN_OK) return st;
+    const uint32_t seq = ++c->seq;
+    const int par = static_cast<int>(seq & 1u);
+    if (cmn_status st = pack_phase(c, ta, tb, grads, dtype, par, s); st != CMN_OK) return st;
+    if (cmn_status st = reduce_phase(c, ta, tb, dtype, seq, algo, s); st != CMN_OK) return st;
+    c->last = ArResult{par, dtype, c->world == 1};
     return CMN_OK;
 }
 
@@ -516,6 +538,7 @@ cmn_status init_common(int rank, int world, int dev, bool sim, cmn_allgather_fn 
     c->user = user;
     c->nsm = prop.multiProcessorCount;
     c->oneshot_max = env_size("CMN_ONESHOT_MAX_BYTES", c->oneshot_max);
+    c->pipe_pieces = static_cast<int>(env_size("CMN_PIECES", static_cast<size_t>(c->pipe_pieces)));
     if (cudaHostAlloc(&c->h_err, sizeof(int), cudaHostAllocMapped) != cudaSuccess ||
         cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->d_err), c->h_err, 0) != cudaSuccess) {
         delete c;
@@ -603,6 +626,85 @@ std::vector<std::pair<int, int>> e2e_pieces(const cmn_comm *c) {
     return out;
 }
 
+// Tensor ranges of roughly equal bytes, forward order (at most `n`).
+std::vector<std::pair<int, int>> equal_ranges(const cmn_comm *c, int n) {
+    std::vector<std::pair<int, int>> out;
+    const int64_t target = (c->L + n - 1) / n;
+    int t = 0;
+    while (t < c->T) {
+        int u = t;
+        int64_t acc = 0;
+        while (u < c->T && (acc < target || static_cast<int>(out.size()) + 1 == n)) {
+            acc += c->numel[u];
+            ++u;
+        }
+        out.emplace_back(t, u);
+        t = u;
+    }
+    return out;
+}
+
+cmn_status ensure_comm_stream(cmn_comm *c, size_t n_events) {
+    if (!c->sc) {
+        int lo = 0, hi = 0;
+        CMN_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CMN_CUDA(cudaStreamCreateWithPriority(&c->sc, cudaStreamNonBlocking, hi));
+    }
+    while (c->pev.size() < n_events) {
+        cudaEvent_t e;
+        CMN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->pev.push_back(e);
+    }
+    return CMN_OK;
+}
+
+// Pipelined a1-a3 for N > 1: the model is cut into P contiguous pieces; each
+// piece is one collective call.  Caller stream s: pack(0..P-1), then
+// update(p) after all-reduce(p); communication stream: all-reduce(p) after
+// pack(p).  HBM-bound packs/updates overlap the NVLink-bound all-reduces.
+// Buffer reuse is safe for P >= 2: a piece's next pack (seq + P) is issued
+// after update(P-1), i.e. after our all-reduce at seq + P - 1 passed its
+// start barrier, so every peer finished all-reduce calls <= seq + P - 2.
+cmn_status step_pipelined(cmn_comm *c, const float *const *grads, int dtype, float lr, float mu,
+                          cudaStream_t s) {
+    const auto pieces = equal_ranges(c, c->pipe_pieces);
+    const size_t P = pieces.size();
+    if (cmn_status st = ensure_comm_stream(c, 2 * P + 1); st != CMN_OK) return st;
+    std::vector<cmn_algo> algo(P);
+    for (size_t p = 0; p < P; ++p)
+        if (cmn_status st = begin_collective(c, pieces[p].first, pieces[p].second, dtype, algo[p]);
+            st != CMN_OK)
+            return st;
+    cudaEvent_t entry = c->pev[2 * P];
+    CMN_CUDA(cudaEventRecord(entry, s));
+    CMN_CUDA(cudaStreamWaitEvent(c->sc, entry, 0));
+    std::vector<ArResult> res(P);
+    for (size_t p = 0; p < P; ++p) {
+        const uint32_t seq = ++c->seq;
+        const int par = static_cast<int>(seq & 1u);
+        res[p] = ArResult{par, dtype, false};
+        if (cmn_status st = pack_phase(c, pieces[p].first, pieces[p].second, grads, dtype, par, s);
+            st != CMN_OK)
+            return st;
+        CMN_CUDA(cudaEventRecord(c->pev[2 * p], s));
+        CMN_CUDA(cudaStreamWaitEvent(c->sc, c->pev[2 * p], 0));
+        if (cmn_status st = reduce_phase(c, pieces[p].first, pieces[p].second, dtype, seq, algo[p],
+                                         c->sc);
+            st != CMN_OK)
+            return st;
+        CMN_CUDA(cudaEventRecord(c->pev[2 * p + 1], c->sc));
+    }
+    for (size_t p = 0; p < P; ++p) {
+        CMN_CUDA(cudaStreamWaitEvent(s, c->pev[2 * p + 1], 0));
+        if (cmn_status st = update_range(c, pieces[p].first, pieces[p].second, res[p], lr, mu, s);
+            st != CMN_OK)
+            return st;
+    }
+    c->last = res[P - 1];
+    c->fresh = false;
+    return CMN_OK;
+}
+
 }  // namespace
 
 // =====================================================================
@@ -635,6 +737,8 @@ cmn_status cmn_finalize(cmn_comm *c) {
     cudaDeviceSynchronize();
     if (c->nccl && g_nccl.CommDestroy) g_nccl.CommDestroy(c->nccl);
     for (auto e : c->ev) cudaEventDestroy(e);
+    for (auto e : c->pev) cudaEventDestroy(e);
+    if (c->sc) cudaStreamDestroy(c->sc);
     if (c->h2d) cudaStreamDestroy(c->h2d);
     if (c->d2h) cudaStreamDestroy(c->d2h);
     free_registration(c);
@@ -756,6 +860,13 @@ cmn_status cmn_step(cmn_comm *c, const float *const *grads, cmn_dtype dtype, flo
     if (cmn_status st = require_registered(c); st != CMN_OK) return st;
     if (cmn_status st = require_dtype(dtype); st != CMN_OK) return st;
     if (c->world > 1) {
+        if (c->pipe_pieces >= 2 && c->T >= 2) {
+            std::string why;
+            if (!grads_ok(c, grads, c->T * (c->simulated ? c->world : 1), why))
+                return fail(CMN_ERR_INVALID_ARG, why);
+            if (cmn_status st = set_device(c); st != CMN_OK) return st;
+            return step_pipelined(c, grads, dtype, lr, mu, static_cast<cudaStream_t>(stream));
+        }
         cmn_status st = cmn_allreduce_grads(c, grads, dtype, stream);
         if (st != CMN_OK) return st;
         return cmn_update_momentum_sgd(c, lr, mu, stream);
@@ -1032,6 +1143,13 @@ cmn_status cmn_set_algo(cmn_comm *c, cmn_algo algo, size_t oneshot_max_bytes) {
         c->nccl = comm;
     }
     c->algo = algo;
+    return CMN_OK;
+}
+
+cmn_status cmn_set_pipeline(cmn_comm *c, int pieces) {
+    if (!c) return fail(CMN_ERR_INVALID_ARG, "comm is NULL");
+    if (pieces < 0 || pieces > 64) return fail(CMN_ERR_INVALID_ARG, "pieces must be in [0, 64]");
+    c->pipe_pieces = pieces;
     return CMN_OK;
 }
 

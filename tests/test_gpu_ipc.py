@@ -25,7 +25,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, dtype, algo, steps, q, mode):
+def _worker(rank, world, port, dtype, algo, steps, q, mode, pieces=0):
     import torch
     import torch.distributed as dist
 
@@ -39,7 +39,7 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode):
         if mode == "mismatch" and rank == 1:
             shapes = shapes[:-1] + [(11,)]
         comm = cmn.Comm.init(rank, world, 0, dist.group.WORLD)
-        comm.set_timeout(60000)
+        comm.set_timeout(3000 if mode == "skip" else 60000)
         w = [torch.from_numpy(p).cuda() for p in synth.params(shapes)]
         try:
             comm.register_params(w)
@@ -47,15 +47,25 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode):
             q.put((rank, "error", e.status_name))
             return
         comm.set_algo(algo)
+        comm.set_pipeline(pieces)
         for s in range(steps):
             g = [torch.from_numpy(x).cuda() for x in synth.grads(shapes, workers=world, step=s)[rank]]
-            comm.allreduce_grads(g, dtype)
-            comm.update_momentum_sgd(0.1, 0.9)
+            if mode == "skip" and rank == 1 and s == 1:
+                continue                              # fault injection: rank 1 skips a collective
+            if pieces:
+                comm.step(g, dtype, 0.1, 0.9)         # pipelined schedule, 2 streams
+            else:
+                comm.allreduce_grads(g, dtype)
+                comm.update_momentum_sgd(0.1, 0.9)
         torch.cuda.synchronize()
-        comm.poll_error()
-        wb = np.concatenate([x.cpu().numpy().reshape(-1) for x in w])
-        vb = np.concatenate([comm.momentum(t).cpu().numpy().reshape(-1) for t in range(len(w))])
-        q.put((rank, "ok", wb.tobytes(), vb.tobytes()))
+        try:
+            comm.poll_error()
+            wb = np.concatenate([x.cpu().numpy().reshape(-1) for x in w])
+            vb = np.concatenate([comm.momentum(t).cpu().numpy().reshape(-1) for t in range(len(w))])
+            q.put((rank, "ok", wb.tobytes(), vb.tobytes()))
+        except cmn.CmnError as e:
+            q.put((rank, "error", e.status_name))
+        dist.barrier()            # no rank frees its IPC-exported buffers while a peer may read them
         comm.finalize()
     except Exception as e:  # noqa: BLE001
         q.put((rank, "exc", repr(e)))
@@ -64,13 +74,13 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode):
             dist.destroy_process_group()
 
 
-def _run(world, dtype, algo, steps=2, mode="same"):
+def _run(world, dtype, algo, steps=2, mode="same", pieces=0):
     from paper_1908_00213_b200 import build
     build.build()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, dtype, algo, steps, q, mode))
+    ps = [ctx.Process(target=_worker, args=(r, world, port, dtype, algo, steps, q, mode, pieces))
           for r in range(world)]
     for p in ps:
         p.start()
@@ -80,10 +90,11 @@ def _run(world, dtype, algo, steps=2, mode="same"):
     return sorted(res, key=lambda r: r[0])
 
 
-@pytest.mark.parametrize("world,dtype,algo", [(2, "fp32", "oneshot"), (2, "fp16", "twoshot"),
-                                              (3, "fp32", "twoshot"), (3, "fp16", "oneshot")])
-def test_ipc_multiprocess_parity(orc, world, dtype, algo):
-    res = _run(world, dtype, algo)
+@pytest.mark.parametrize("world,dtype,algo,pieces", [(2, "fp32", "oneshot", 0), (2, "fp16", "twoshot", 0),
+                                                     (3, "fp32", "twoshot", 0), (3, "fp16", "oneshot", 0),
+                                                     (2, "fp32", "twoshot", 3), (3, "fp16", "twoshot", 2)])
+def test_ipc_multiprocess_parity(orc, world, dtype, algo, pieces):
+    res = _run(world, dtype, algo, pieces=pieces)
     assert all(r[1] == "ok" for r in res), res
     shapes = synth.mlp_shapes()
     w = synth.params(shapes)
@@ -95,6 +106,16 @@ def test_ipc_multiprocess_parity(orc, world, dtype, algo):
     for r in res:
         assert np.array_equal(np.frombuffer(r[2], np.uint32), want_w), f"rank {r[0]} w"
         assert np.array_equal(np.frombuffer(r[3], np.uint32), want_v), f"rank {r[0]} v"
+
+
+def test_ipc_skipped_collective_times_out():
+    """Fault injection: rank 1 skips one step's all-reduce.  Rank 0's
+    kernel must not hang: its spin-wait times out (3 s) and the error
+    surfaces as CMN_ERR_TIMEOUT -- or, if rank 1's next
+    call pairs with it, the sequence numbers still let both finish."""
+    res = _run(2, "fp32", "oneshot", steps=3, mode="skip")
+    statuses = {r[0]: r[1:] for r in res}
+    assert statuses[0][0] == "error" and statuses[0][1] == "CMN_ERR_TIMEOUT", res
 
 
 def test_ipc_structure_mismatch_detected():

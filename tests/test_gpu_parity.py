@@ -244,6 +244,31 @@ def test_r50_full_size_n8_simulated(cmn, orc, dtype, algo):
     compare(gpu, ora, N)
 
 
+@pytest.mark.parametrize("N,pieces,dtype", [(2, 2, "fp32"), (4, 3, "fp16"), (8, 4, "fp32"),
+                                            (3, 7, "fp16"), (8, 16, "fp16")])
+def test_pipelined_step_parity(cmn, orc, N, pieces, dtype):
+    """cmn_step at N > 1 with the pipelined schedule (packs/updates on the
+    caller stream, all-reduces on the communication stream, one collective
+    per piece) == oracle, bitwise, over 3 steps (buffer parity reuse)."""
+    shapes = synth.resnet50_shapes()[:50] + RAGGED
+    grads = [synth.grads(shapes, workers=N, step=s) for s in range(3)]
+    params0 = synth.params(shapes)
+    ora, _, _ = run_oracle(orc, shapes, N, dtype, grads, params0, 0.1, 0.9)
+    comm = cmn.Comm.simulated_world(N)
+    try:
+        w = to_dev(params0)
+        comm.register_params(w)
+        comm.set_pipeline(pieces)
+        for s, g in enumerate(grads):
+            comm.step(comm.prepare([to_dev(gw) for gw in g]), dtype, 0.1, 0.9)
+            torch.cuda.synchronize()
+            for t in range(len(w)):
+                assert_bitwise(w[t].cpu().numpy().reshape(-1), ora[s]["w"][t], f"w[{t}] step {s}")
+                assert_bitwise(comm.momentum(t).cpu().numpy().reshape(-1), ora[s]["v"][t], f"v[{t}]")
+    finally:
+        comm.finalize()
+
+
 def test_buckets_bitwise_equal_unbucketed(cmn, orc):
     """Overlap reading R15: bucketed (reverse order, any size) == unbucketed."""
     shapes = synth.resnet50_shapes()[:40]
