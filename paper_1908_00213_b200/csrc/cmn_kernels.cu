@@ -230,6 +230,17 @@ __global__ void __launch_bounds__(kThreads) k_unpack_avg(GradTab out, int t_lo,
 
 // NEXT-1: bias-corrected Adam, every operation IEEE round-to-nearest and
 // uncontracted, in the order written in the oracle (orc_update_adam).
+// 28 B/param algorithmic (read r, w, m, v; write w, m, v).
+__device__ __forceinline__ void adam_elem(float r, float inv_n, float alpha_t, float beta1,
+                                          float beta2, float c1, float c2, float eps, float &w,
+                                          float &m, float &v) {
+    const float a = __fmul_rn(r, inv_n);
+    m = __fadd_rn(__fmul_rn(beta1, m), __fmul_rn(c1, a));
+    v = __fadd_rn(__fmul_rn(beta2, v), __fmul_rn(c2, __fmul_rn(a, a)));
+    const float den = __fadd_rn(__fsqrt_rn(v), eps);
+    w = __fsub_rn(w, __fmul_rn(alpha_t, __fdiv_rn(m, den)));
+}
+
 template <int DT>
 __global__ void __launch_bounds__(kThreads) k_update_adam(const TensorDesc *__restrict__ td,
                                                           const Item *__restrict__ items, int i0,
@@ -239,19 +250,45 @@ __global__ void __launch_bounds__(kThreads) k_update_adam(const TensorDesc *__re
                                                           float eps) {
     const Item it = items[i0 + blockIdx.x];
     const TensorDesc d = td[it.t];
-    const int64_t base = d.off + it.k0;
     float *__restrict__ w = d.w + it.k0;
     float *__restrict__ m = d.adam_m + it.k0;
     float *__restrict__ v = d.adam_v + it.k0;
-    for (int k = threadIdx.x; k < it.len; k += kThreads) {
-        const float a = __fmul_rn(load_r1<DT>(reduced, base + k), inv_n);
-        const float mn = __fadd_rn(__fmul_rn(beta1, m[k]), __fmul_rn(c1, a));
-        const float vn = __fadd_rn(__fmul_rn(beta2, v[k]), __fmul_rn(c2, __fmul_rn(a, a)));
-        const float den = __fadd_rn(__fsqrt_rn(vn), eps);
-        const float wn = __fsub_rn(w[k], __fmul_rn(alpha_t, __fdiv_rn(mn, den)));
-        m[k] = mn;
-        v[k] = vn;
-        w[k] = wn;
+    const int nv = it.len >> 2;
+    constexpr int U = kVecPerThread / 2;   // two passes keep 4 arrays x 2 float4 in registers
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+        float4 r[U], wv[U], mv[U], vv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int q = threadIdx.x + (pass * U + u) * kThreads;
+            if (q < nv) {
+                r[u] = load_r4<DT>(reduced, it.base + 4 * q);
+                wv[u] = ld_cs_f4(w + 4 * q);
+                mv[u] = ld_cs_f4(m + 4 * q);
+                vv[u] = ld_cs_f4(v + 4 * q);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int q = threadIdx.x + (pass * U + u) * kThreads;
+            if (q < nv) {
+                adam_elem(r[u].x, inv_n, alpha_t, beta1, beta2, c1, c2, eps, wv[u].x, mv[u].x, vv[u].x);
+                adam_elem(r[u].y, inv_n, alpha_t, beta1, beta2, c1, c2, eps, wv[u].y, mv[u].y, vv[u].y);
+                adam_elem(r[u].z, inv_n, alpha_t, beta1, beta2, c1, c2, eps, wv[u].z, mv[u].z, vv[u].z);
+                adam_elem(r[u].w, inv_n, alpha_t, beta1, beta2, c1, c2, eps, wv[u].w, mv[u].w, vv[u].w);
+                st_cs_f4(w + 4 * q, wv[u]);
+                st_cs_f4(m + 4 * q, mv[u]);
+                st_cs_f4(v + 4 * q, vv[u]);
+            }
+        }
+    }
+    for (int k = (nv << 2) + threadIdx.x; k < it.len; k += kThreads) {
+        float wk = w[k], mk = m[k], vk = v[k];
+        adam_elem(load_r1<DT>(reduced, it.base + k), inv_n, alpha_t, beta1, beta2, c1, c2, eps,
+                  wk, mk, vk);
+        w[k] = wk;
+        m[k] = mk;
+        v[k] = vk;
     }
 }
 

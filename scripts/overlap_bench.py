@@ -1,0 +1,186 @@
+#!/usr/bin/env python
+"""BASELINE config 4: ResNet-50 step with the bucketed all-reduce + update
+overlapped with a synthetic backward on separate streams (PAPER.md:788-792,
+"starting all-reduce as soon as the backward computation of a layer is
+completed").
+
+    python scripts/overlap_bench.py --sim 8 [--bwd-ms 1.0] [--bucket-mb 25]
+    torchrun --nproc-per-node 8 scripts/overlap_bench.py --bwd-ms 1.0
+
+Synthetic backward (the producer of the path's input, not part of it): the
+161 tensors are visited in REVERSE registration order; each "layer" runs a
+bf16 matmul whose FLOPs are that layer's share of ResNet-50's backward
+(2 x forward MACs x 2 for dgrad + wgrad, batch 32; shares from SURVEY §8(d)
+d.2: conv1 2.9 %, layer1 16.3 %, layer2 25.1 %, layer3 35.8 %, layer4
+19.8 %, fc 0.1 %), scaled so the whole backward takes --bwd-ms, then copies
+its precomputed gradient into g_t.  After a bucket's last tensor the compute
+stream records an event; the communication stream waits on it and runs
+cmn_allreduce_bucket + cmn_update_bucket.
+
+Reported: T_bwd alone, T_comm alone (all buckets, no backward), T_step
+(overlapped), exposed comm = T_step - T_bwd, overlap efficiency =
+1 - exposed / T_comm.  The bucketed result is checked bitwise against the
+unbucketed cmn_allreduce_grads + cmn_update_momentum_sgd.
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import synth  # noqa: E402
+from paper_1908_00213_b200 import Comm  # noqa: E402
+
+STAGE_SHARE = {"conv1": 0.029, "layer1": 0.163, "layer2": 0.251, "layer3": 0.358,
+               "layer4": 0.198, "fc": 0.001}
+
+
+def stage_of_r50():
+    """Stage name of each of ResNet-50's 161 tensors (parameters() order)."""
+    names = ["conv1"] * 3
+    for st, blocks in (("layer1", 3), ("layer2", 4), ("layer3", 6), ("layer4", 3)):
+        for b in range(blocks):
+            names += [st] * (9 + (3 if b == 0 else 0))
+    names += ["fc", "fc"]
+    return names
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--sim", type=int, default=0, help="simulated ranks on one GPU (0 = torchrun)")
+    ap.add_argument("--bwd-ms", type=float, default=1.0)
+    ap.add_argument("--bucket-mb", type=float, default=25.0)
+    ap.add_argument("--dtype", default="fp32")
+    ap.add_argument("--iters", type=int, default=20)
+    a = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    shapes = synth.resnet50_shapes()
+    sizes = [synth.numel(s) for s in shapes]
+    T = len(shapes)
+    nranks = a.sim if a.sim else world
+    comm = Comm.simulated_world(a.sim) if a.sim else Comm.init(rank, world, local,
+                                                               dist.group.WORLD if world > 1 else None)
+    p0 = synth.params(shapes)
+    w = [torch.from_numpy(p.copy()).cuda() for p in p0]
+    comm.register_params(w)
+    nb = comm.plan_buckets(int(a.bucket_mb * (1 << 20)))
+    buckets = [comm.get_bucket(b) for b in range(nb)]
+    host_g = synth.grads(shapes, workers=nranks)
+    workers = range(nranks) if a.sim else [rank]
+    src = [[torch.from_numpy(host_g[i][t]).cuda() for t in range(T)] for i in workers]
+    g = [[torch.empty_like(x) for x in gw] for gw in src]
+    table = comm.prepare(g if a.sim else g[0])
+
+    # synthetic backward kernels: per-layer bf16 GEMM sized by FLOP share
+    stages = stage_of_r50()
+    per_stage = {s: stages.count(s) for s in STAGE_SHARE}
+    # calibrate: time of one 1024^3 bf16 GEMM
+    A = torch.randn(1024, 1024, device="cuda", dtype=torch.bfloat16)
+    B = torch.randn(1024, 1024, device="cuda", dtype=torch.bfloat16)
+    for _ in range(5):
+        A @ B
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(50):
+        A @ B
+    e1.record()
+    torch.cuda.synchronize()
+    gemm_ms = e0.elapsed_time(e1) / 50
+    reps = [max(0, round(a.bwd_ms * STAGE_SHARE[stages[t]] / per_stage[stages[t]] / gemm_ms))
+            for t in range(T)]
+
+    comp = torch.cuda.current_stream()
+    comm_stream = torch.cuda.Stream(priority=-1)
+    last_of_bucket = {lo: b for b, (lo, hi) in enumerate(buckets)}   # reverse order: bucket ends at lo
+
+    def backward(with_comm: bool):
+        evs = []
+        for t in reversed(range(T)):
+            for _ in range(reps[t]):
+                A @ B
+            for i in range(len(g)):
+                g[i][t].copy_(src[i][t])
+            if with_comm and t in last_of_bucket:
+                ev = torch.cuda.Event()
+                ev.record(comp)
+                evs.append((last_of_bucket[t], ev))
+                b = last_of_bucket[t]
+                comm_stream.wait_event(ev)
+                comm.allreduce_bucket(b, table, a.dtype, comm_stream)
+                comm.update_bucket(b, 0.1, 0.9, comm_stream)
+        if with_comm:
+            comp.wait_stream(comm_stream)
+
+    def comm_only():
+        for b in range(nb):
+            comm.allreduce_bucket(b, table, a.dtype, comp)
+            comm.update_bucket(b, 0.1, 0.9, comp)
+
+    def timed(fn, *args):
+        for _ in range(3):
+            fn(*args)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(comp)
+        for _ in range(a.iters):
+            fn(*args)
+        e.record(comp)
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / a.iters
+        if world > 1:
+            t_ = torch.tensor([ms], dtype=torch.float64)
+            dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+            ms = float(t_.item())
+        return ms
+
+    t_bwd = timed(backward, False)
+    t_comm = timed(comm_only)
+    t_step = timed(backward, True)
+
+    # bitwise: bucketed vs unbucketed from the same state
+    for x, p in zip(w, p0):
+        x.copy_(torch.from_numpy(p))
+    comm.register_params(w)          # resets momentum
+    comm.plan_buckets(int(a.bucket_mb * (1 << 20)))
+    backward(True)
+    torch.cuda.synchronize()
+    wb = torch.cat([x.reshape(-1) for x in w]).clone()
+    for x, p in zip(w, p0):
+        x.copy_(torch.from_numpy(p))
+    comm.register_params(w)
+    comm.allreduce_grads(table, a.dtype)
+    comm.update_momentum_sgd(0.1, 0.9)
+    torch.cuda.synchronize()
+    wu = torch.cat([x.reshape(-1) for x in w])
+    same = bool(torch.equal(wb.view(torch.int32), wu.view(torch.int32)))
+
+    exposed = t_step - t_bwd
+    if rank == 0:
+        print(json.dumps({"config": "BASELINE config 4 (overlap)", "ranks": nranks,
+                          "simulated": bool(a.sim), "dtype": a.dtype, "buckets": nb,
+                          "bucket_mb": a.bucket_mb, "T_bwd_ms": t_bwd, "T_comm_ms": t_comm,
+                          "T_step_ms": t_step, "exposed_comm_ms": exposed,
+                          "overlap_efficiency": 1 - exposed / t_comm if t_comm > 0 else None,
+                          "bucketed_equals_unbucketed_bitwise": same,
+                          "gemm_1024_ms": gemm_ms}))
+    comm.finalize()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
