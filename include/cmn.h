@@ -39,6 +39,9 @@
  *     (cmn_register_params, cmn_allreduce_*, cmn_step*) with the same layout
  *     and dtype ("model structures are
  *     identical between workers merely in a single iteration").
+ *   - CUDA graphs: N == 1 and simulated communicators may be captured.  The
+ *     multi-process collectives pass per-call sequence numbers as kernel
+ *     arguments and refuse capture (CMN_ERR_UNSUPPORTED) rather than race.
  *   - There is no CPU fallback: if the CUDA device or the sm_100a kernels are
  *     unavailable every compute entry point fails with CMN_ERR_CUDA.
  */

@@ -305,8 +305,12 @@ cmn_status exchange_and_map(cmn_comm *c) {
 
 int ar_blocks_for(const cmn_comm *c) {
     if (c->ar_blocks > 0) return c->ar_blocks;
+    // Real ranks: one CTA per SM is ~19 MB of 16-B NVLink loads in flight at
+    // N = 8 (far above the ~1 MB bandwidth-delay product) and leaves room
+    // for the pipelined packs/updates.  Simulated ranks read local HBM:
+    // two CTAs per SM.
     const size_t env = env_size("CMN_CTAS", 0);
-    int b = env ? static_cast<int>(env) : 2 * c->nsm;
+    int b = env ? static_cast<int>(env) : (c->simulated ? 2 : 1) * c->nsm;
     if (b > kMaxBarrierBlocks) b = kMaxBarrierBlocks;
     if (b < 1) b = 1;
     return b;
@@ -457,8 +461,21 @@ cmn_status reduce_phase(cmn_comm *c, int ta, int tb, int dtype, uint32_t seq, cm
 }
 
 // Validate and choose the algorithm for one collective over [ta, tb).
-cmn_status begin_collective(cmn_comm *c, int ta, int tb, int dtype, cmn_algo &algo) {
+// Cross-process collectives carry host-assigned sequence numbers and buffer
+// parities as kernel arguments, which a CUDA graph would freeze: replays
+// would pass barriers early.  Refuse capture loudly instead of racing.
+// (N = 1 and simulated communicators have no cross-process state and may be
+// captured.)
+cmn_status begin_collective(cmn_comm *c, int ta, int tb, int dtype, cmn_algo &algo,
+                            cudaStream_t s) {
     if (cmn_status st = check_async_error(c); st != CMN_OK) return st;
+    if (!c->simulated && c->world > 1) {
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        CMN_CUDA(cudaStreamIsCapturing(s, &cap));
+        if (cap != cudaStreamCaptureStatusNone)
+            return fail(CMN_ERR_UNSUPPORTED,
+                        "multi-process collectives cannot be captured into a CUDA graph");
+    }
     const size_t esz = dtype == 0 ? 4 : 2;
     algo = choose_algo(c, static_cast<size_t>(c->off[tb] - c->off[ta]) * esz);
     if (algo == CMN_ALGO_NCCL && (c->simulated || !c->nccl))
@@ -471,7 +488,7 @@ cmn_status begin_collective(cmn_comm *c, int ta, int tb, int dtype, cmn_algo &al
 cmn_status allreduce_range(cmn_comm *c, int ta, int tb, const float *const *grads, int dtype,
                            cudaStream_t s) {
     cmn_algo algo;
-    if (cmn_status st = begin_collective(c, ta, tb, dtype, algo); st != CMN_OK) return st;
+    if (cmn_status st = begin_collective(c, ta, tb, dtype, algo, s); st != CMN_OK) return st;
     const uint32_t seq = ++c->seq;
     const int par = static_cast<int>(seq & 1u);
     if (cmn_status st = pack_phase(c, ta, tb, grads, dtype, par, s); st != CMN_OK) return st;
@@ -672,7 +689,7 @@ cmn_status step_pipelined(cmn_comm *c, const float *const *grads, int dtype, flo
     if (cmn_status st = ensure_comm_stream(c, 2 * P + 1); st != CMN_OK) return st;
     std::vector<cmn_algo> algo(P);
     for (size_t p = 0; p < P; ++p)
-        if (cmn_status st = begin_collective(c, pieces[p].first, pieces[p].second, dtype, algo[p]);
+        if (cmn_status st = begin_collective(c, pieces[p].first, pieces[p].second, dtype, algo[p], s);
             st != CMN_OK)
             return st;
     cudaEvent_t entry = c->pev[2 * P];

@@ -1,0 +1,137 @@
+"""multi_node_optimizer on top of the C ABI (Fig. 4).
+
+"multi_node_optimizer ... wraps the normal optimizer and exchanges the
+gradient across processes using the all-reduce operation before optimizing
+the model.  It behaves identically as the original optimizer except for the
+communication."  Here the wrapped optimizer is momentum SGD (or Adam), and
+exchange + update are cmn_* calls: this module is bookkeeping only (pointer
+tables, backward hooks, re-registration); every arithmetic step runs in
+libcmn's kernels.
+
+Define-by-Run compatibility: "model structures are
+identical between workers merely in a single iteration ... model structure
+can be changed at any iteration dynamically".  step() compares the current
+parameter set with the registered one and re-registers (a collective call,
+so every rank re-registers in the same iteration) when it changed; the
+registration-time structure check turns a cross-rank divergence into
+CMN_ERR_MISMATCH instead of a hang.
+
+Overlap: with bucket_bytes set, a post-accumulate-grad
+hook counts ready gradients per bucket (buckets are reverse-order contiguous
+tensor ranges) and launches cmn_allreduce_bucket on a communication stream
+as soon as a bucket is complete, while backward keeps running; step() then
+waits and applies cmn_update_bucket per bucket.
+"""
+from __future__ import annotations
+
+import torch
+
+from .cmn import Comm, PtrTable
+
+
+class MultiNodeOptimizer:
+    def __init__(self, params, comm: Comm, lr: float = 0.1, momentum: float = 0.9,
+                 dtype: str = "fp32", bucket_bytes: int | None = None, optimizer: str = "momentum_sgd",
+                 adam=(1e-3, 0.9, 0.999, 1e-8)):
+        self.comm = comm
+        self.lr, self.mu, self.dtype = lr, momentum, dtype
+        self.bucket_bytes = bucket_bytes
+        self.optimizer = optimizer
+        self.adam = adam
+        self.t = 0
+        self.registrations = 0
+        self._hooks = []
+        self._stream = None
+        self._launched = set()
+        self._setup(list(params))
+
+    # -------------------------------------------------------------- structure
+    def _setup(self, params):
+        for h in self._hooks:
+            h.remove()
+        self._hooks = []
+        self.params = params
+        self.comm.register_params(params)
+        self.registrations += 1
+        self.t = 0
+        self._sig = [(id(p), tuple(p.shape)) for p in params]
+        self.buckets = []
+        if self.bucket_bytes:
+            nb = self.comm.plan_buckets(self.bucket_bytes)
+            self.buckets = [self.comm.get_bucket(b) for b in range(nb)]
+            self._bucket_of = {}
+            for b, (lo, hi) in enumerate(self.buckets):
+                for t in range(lo, hi):
+                    self._bucket_of[t] = b
+            self._pending = [hi - lo for lo, hi in self.buckets]
+            if self._stream is None:
+                self._stream = torch.cuda.Stream(priority=-1)
+            for t, p in enumerate(params):
+                self._hooks.append(p.register_post_accumulate_grad_hook(self._make_hook(t)))
+
+    def maybe_reregister(self, params) -> bool:
+        params = list(params)
+        sig = [(id(p), tuple(p.shape)) for p in params]
+        if sig != self._sig:
+            self._setup(params)
+            return True
+        return False
+
+    # ----------------------------------------------------------------- overlap
+    def _make_hook(self, t):
+        def hook(_p):
+            b = self._bucket_of[t]
+            self._pending[b] -= 1
+            if self._pending[b] == 0 and b not in self._launched:
+                lo, hi = self.buckets[b]
+                if all(q.grad is not None for q in self.params[lo:hi]):
+                    ev = torch.cuda.Event()
+                    ev.record(torch.cuda.current_stream())
+                    self._stream.wait_event(ev)
+                    self.comm.allreduce_bucket(b, self._grad_table(), self.dtype, self._stream)
+                    self._launched.add(b)
+        return hook
+
+    def _grad_table(self) -> PtrTable:
+        # Only the bucket's own grads are read; others may be missing yet, so
+        # absent grads point at the parameter (never dereferenced).
+        return PtrTable([p.grad if p.grad is not None else p for p in self.params])
+
+    # -------------------------------------------------------------------- step
+    def step(self, params=None):
+        if params is not None:
+            self.maybe_reregister(params)
+        if any(p.grad is None for p in self.params):
+            raise RuntimeError("multi_node_optimizer: a registered parameter has no gradient")
+        cur = torch.cuda.current_stream()
+        if self.buckets:
+            table = None
+            for b in range(len(self.buckets)):
+                if b not in self._launched:          # hook did not fire (e.g. no backward hooks)
+                    if table is None:
+                        table = self._grad_table()
+                    ev = torch.cuda.Event()
+                    ev.record(cur)
+                    self._stream.wait_event(ev)
+                    self.comm.allreduce_bucket(b, table, self.dtype, self._stream)
+            cur.wait_stream(self._stream)
+            for b in range(len(self.buckets)):
+                self.comm.update_bucket(b, self.lr, self.mu, cur)
+            self._launched.clear()
+            self._pending = [hi - lo for lo, hi in self.buckets]
+        elif self.optimizer == "adam":
+            self.t += 1
+            self.comm.allreduce_grads(self._grad_table(), self.dtype)
+            a, b1, b2, eps = self.adam
+            self.comm.update_adam(a, b1, b2, eps, self.t)
+        else:
+            self.comm.step(self._grad_table(), self.dtype, self.lr, self.mu)
+
+    def zero_grad(self):
+        for p in self.params:
+            p.grad = None
+
+
+def create_multi_node_optimizer(params, comm: Comm, **kw) -> MultiNodeOptimizer:
+    """The paper's create_multi_node_optimizer(optimizer, comm)."""
+    return MultiNodeOptimizer(params, comm, **kw)

@@ -61,7 +61,7 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -103,20 +103,36 @@ def main():
 
     comp = torch.cuda.current_stream()
     comm_stream = torch.cuda.Stream(priority=-1)
-    last_of_bucket = {lo: b for b, (lo, hi) in enumerate(buckets)}   # reverse order: bucket ends at lo
-
-    def backward(with_comm: bool):
-        evs = []
-        for t in reversed(range(T)):
+    # Backward segments: bucket b (reverse order) covers tensors [lo, hi); the
+    # producer for those layers is captured once into a CUDA graph so the
+    # synthetic backward is not bound by Python launch overhead.
+    def produce(lo, hi):
+        for t in reversed(range(lo, hi)):
             for _ in range(reps[t]):
                 A @ B
             for i in range(len(g)):
                 g[i][t].copy_(src[i][t])
-            if with_comm and t in last_of_bucket:
+
+    seg_graphs = []
+    side = torch.cuda.Stream()
+    side.wait_stream(comp)
+    with torch.cuda.stream(side):
+        for lo, hi in buckets:
+            produce(lo, hi)            # warm-up outside capture (cuBLAS workspaces)
+    torch.cuda.synchronize()
+    for lo, hi in buckets:
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            produce(lo, hi)
+        seg_graphs.append(gr)
+    torch.cuda.synchronize()
+
+    def backward(with_comm: bool):
+        for b in range(nb):
+            seg_graphs[b].replay()
+            if with_comm:
                 ev = torch.cuda.Event()
                 ev.record(comp)
-                evs.append((last_of_bucket[t], ev))
-                b = last_of_bucket[t]
                 comm_stream.wait_event(ev)
                 comm.allreduce_bucket(b, table, a.dtype, comm_stream)
                 comm.update_bucket(b, 0.1, 0.9, comm_stream)
