@@ -248,7 +248,7 @@ def main():
     comm.register_params(w)
     if args.algo != "auto" and world > 1:
         comm.set_algo(args.algo)
-    g_host = synth.grads(shapes, workers=world)[rank]
+    g_host = [synth.grad_tensor(n, t, worker=rank) for t, n in enumerate(sizes)]   # this rank's worker
     flat_g = torch.empty(L, dtype=torch.float32, device=dev)
     g = []
     for t, s in enumerate(shapes):
