@@ -189,6 +189,19 @@ cmn_status cmn_update_momentum_sgd(cmn_comm *comm, float lr, float mu, void *str
 cmn_status cmn_step(cmn_comm *comm, const float *const *grads, cmn_dtype dtype,
                     float lr, float mu, void *stream);
 
+/* cmn_step_sharded -- NEXT-4: a1 + reduce-scatter + a3 on the own chunk only
+ * + all-gather of the updated PARAMETERS (instead of the reduced gradients).
+ * Rank r owns the two-shot chunk r (cmn_plan_chunks); it runs the update
+ * (1/N of the replicated update's HBM traffic) and publishes w' in fp32;
+ * peers copy it over NVLink.  w is bitwise equal to cmn_step's on every
+ * rank; the momentum state becomes sharded: after this call tensor t's
+ * momentum (cmn_get_momentum) is current only on the elements the calling
+ * rank owns.  Do not mix with cmn_step on the same communicator unless the
+ * momentum is re-synchronised.  N == 1 is cmn_step.  grads as in
+ * cmn_allreduce_grads. */
+cmn_status cmn_step_sharded(cmn_comm *comm, const float *const *grads, cmn_dtype dtype,
+                            float lr, float mu, void *stream);
+
 /* cmn_step_host -- cmn_step with HOST buffers (end-to-end measurement):
  *   host_grads    n_tensors (or world*n_tensors, simulated) host fp32 pointers;
  *                 pinned memory gives asynchronous copies

@@ -37,6 +37,7 @@ SIGNATURES = [
     ("cmn_allreduce_grads", C.c_int, [_P, _PP, C.c_int, _P]),
     ("cmn_update_momentum_sgd", C.c_int, [_P, C.c_float, C.c_float, _P]),
     ("cmn_step", C.c_int, [_P, _PP, C.c_int, C.c_float, C.c_float, _P]),
+    ("cmn_step_sharded", C.c_int, [_P, _PP, C.c_int, C.c_float, C.c_float, _P]),
     ("cmn_step_host", C.c_int, [_P, _PP, _PP, C.c_int, C.c_float, C.c_float, _P]),
     ("cmn_step_host_packed", C.c_int, [_P, _P, _P, C.c_int, C.c_float, C.c_float, _P]),
     ("cmn_unpack_avg_grads", C.c_int, [_P, _PP, _P]),
@@ -280,6 +281,10 @@ class Comm:
     def step(self, grads, dtype="fp32", lr=0.1, mu=0.9, stream=None):
         _check(lib().cmn_step(self._h, self._grad_table(grads), _dt(dtype), lr, mu, _stream(stream)),
                "cmn_step")
+
+    def step_sharded(self, grads, dtype="fp32", lr=0.1, mu=0.9, stream=None):
+        _check(lib().cmn_step_sharded(self._h, self._grad_table(grads), _dt(dtype), lr, mu,
+                                      _stream(stream)), "cmn_step_sharded")
 
     def step_host(self, host_grads, host_params=None, dtype="fp32", lr=0.1, mu=0.9, stream=None):
         g = self._grad_table(host_grads)

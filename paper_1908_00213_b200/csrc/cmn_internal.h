@@ -38,7 +38,7 @@ struct Item {
     int64_t k0;
     int64_t base;
     int32_t pad;
-    int32_t reserved;
+    int32_t reserved;   // sharded-update item lists: owner rank of the chunk
 };
 
 // Grad pointers for the tensors [t_lo, t_lo + kGradCap) of one launch.
@@ -106,6 +106,18 @@ cudaError_t launch_allreduce_twoshot(const PeerBufs &in, const PeerBufs &red, in
                                      const int64_t *chunk_start, const int64_t *chunk_end,
                                      int dtype, int phases, const Barrier &bar, int blocks,
                                      cudaStream_t s);
+
+// NEXT-4 sharded update: momentum SGD on the items of the own chunk, also
+// writing w' into the fp32 exchange buffer (packed layout).
+cudaError_t launch_update_chunk(const TensorDesc *td, const Item *items, int i0, int i1,
+                                const void *reduced, int dtype, float *exch, float inv_n, float lr,
+                                float mu, cudaStream_t s);
+
+// NEXT-4 all-gather of parameters: start barrier, then copy items [i0, i1)
+// minus [s0, s1) from the owner's exchange buffer (Item.reserved = owner).
+cudaError_t launch_gather_params(const TensorDesc *td, const Item *items, int i0, int i1, int s0,
+                                 int s1, const PeerBufs &exch, int world, const Barrier &bar,
+                                 int blocks, cudaStream_t s);
 
 int num_sms(int device);
 

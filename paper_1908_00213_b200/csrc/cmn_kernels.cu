@@ -424,6 +424,87 @@ __global__ void __launch_bounds__(kThreads) k_twoshot(const __grid_constant__ Pe
     }
 }
 
+// ------------------------------------------------------------ NEXT-4
+// Sharded update (reduce-scatter -> update own chunk -> all-gather params).
+// k_update_chunk: momentum SGD on the items clipped to this rank's chunk,
+// reading the reduce-scatter output (own reduced buffer, packed layout) and
+// publishing the new parameters into the fp32 exchange buffer at the same
+// packed indices.
+template <int DT>
+__global__ void __launch_bounds__(kThreads) k_update_chunk(const TensorDesc *__restrict__ td,
+                                                           const Item *__restrict__ items, int i0,
+                                                           const void *__restrict__ reduced,
+                                                           float *__restrict__ exch, float inv_n,
+                                                           float lr, float mu) {
+    const Item it = items[i0 + blockIdx.x];
+    const TensorDesc d = td[it.t];
+    float *__restrict__ w = d.w + it.k0;
+    float *__restrict__ m = d.mom + it.k0;
+    float *__restrict__ x = exch + it.base;
+    const int nv = it.len >> 2;
+    float4 r[kVecPerThread], wv[kVecPerThread], mv[kVecPerThread];
+#pragma unroll
+    for (int u = 0; u < kVecPerThread; ++u) {
+        const int v = threadIdx.x + u * kThreads;
+        if (v < nv) {
+            r[u] = load_r4<DT>(reduced, it.base + 4 * v);
+            wv[u] = ld_cs_f4(w + 4 * v);
+            mv[u] = ld_cs_f4(m + 4 * v);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < kVecPerThread; ++u) {
+        const int v = threadIdx.x + u * kThreads;
+        if (v < nv) {
+            sgd_vec(r[u], inv_n, lr, mu, wv[u], mv[u]);
+            st_cs_f4(w + 4 * v, wv[u]);
+            st_cs_f4(m + 4 * v, mv[u]);
+            st_u4(x + 4 * v, make_uint4(__float_as_uint(wv[u].x), __float_as_uint(wv[u].y),
+                                        __float_as_uint(wv[u].z), __float_as_uint(wv[u].w)));
+        }
+    }
+    for (int k = (nv << 2) + threadIdx.x; k < it.len; k += kThreads) {
+        float wk = w[k], mk = m[k];
+        sgd_elem(load_r1<DT>(reduced, it.base + k), inv_n, lr, mu, wk, mk);
+        w[k] = wk;
+        m[k] = mk;
+        x[k] = wk;
+    }
+}
+
+// k_gather_params: after a start barrier (every peer has arrived, i.e. its
+// k_update_chunk completed), copy every other rank's updated parameters
+// from its exchange buffer (peer memory) into the local tensors.  Item
+// field `reserved` holds the owner rank; grid-stride over [i0, i1) skipping
+// [s0, s1) (the own chunk's items).
+__global__ void __launch_bounds__(kThreads) k_gather_params(const TensorDesc *__restrict__ td,
+                                                            const Item *__restrict__ items, int i0,
+                                                            int i1, int s0, int s1,
+                                                            const __grid_constant__ PeerBufs exch,
+                                                            int world,
+                                                            const __grid_constant__ Barrier bar) {
+    cross_rank_barrier(bar, world, 0);
+    for (int i = i0 + blockIdx.x; i < i1; i += gridDim.x) {
+        if (i >= s0 && i < s1) continue;
+        const Item it = items[i];
+        float *__restrict__ w = td[it.t].w + it.k0;
+        const float *src = static_cast<const float *>(exch.p[it.reserved]) + it.base;
+        const int nv = it.len >> 2;
+        uint4 x[kVecPerThread];
+#pragma unroll
+        for (int u = 0; u < kVecPerThread; ++u) {
+            const int v = threadIdx.x + u * kThreads;
+            if (v < nv) x[u] = ld_peer_u4(src + 4 * v);
+        }
+#pragma unroll
+        for (int u = 0; u < kVecPerThread; ++u) {
+            const int v = threadIdx.x + u * kThreads;
+            if (v < nv) st_u4(w + 4 * v, x[u]);
+        }
+        for (int k = (nv << 2) + threadIdx.x; k < it.len; k += kThreads) w[k] = src[k];
+    }
+}
+
 inline int grid_of(int i0, int i1) { return i1 > i0 ? i1 - i0 : 0; }
 
 }  // namespace
@@ -571,6 +652,28 @@ cudaError_t launch_allreduce_twoshot(const PeerBufs &in, const PeerBufs &red, in
                         ? twoshot_dispatch<0>(world, in, red, rank, ch, phases, bar, blocks, s)
                         : twoshot_dispatch<1>(world, in, red, rank, ch, phases, bar, blocks, s);
     return ok ? cudaGetLastError() : cudaErrorInvalidValue;
+}
+
+cudaError_t launch_update_chunk(const TensorDesc *td, const Item *items, int i0, int i1,
+                                const void *reduced, int dtype, float *exch, float inv_n, float lr,
+                                float mu, cudaStream_t s) {
+    const int grid = grid_of(i0, i1);
+    if (grid == 0) return cudaSuccess;
+    (void)cudaGetLastError();
+    if (dtype == 0)
+        k_update_chunk<0><<<grid, kThreads, 0, s>>>(td, items, i0, reduced, exch, inv_n, lr, mu);
+    else
+        k_update_chunk<1><<<grid, kThreads, 0, s>>>(td, items, i0, reduced, exch, inv_n, lr, mu);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather_params(const TensorDesc *td, const Item *items, int i0, int i1, int s0,
+                                 int s1, const PeerBufs &exch, int world, const Barrier &bar,
+                                 int blocks, cudaStream_t s) {
+    if (blocks <= 0 || blocks > kMaxBarrierBlocks) return cudaErrorInvalidValue;
+    (void)cudaGetLastError();
+    k_gather_params<<<blocks, kThreads, 0, s>>>(td, items, i0, i1, s0, s1, exch, world, bar);
+    return cudaGetLastError();
 }
 
 int num_sms(int device) {

@@ -159,6 +159,10 @@ struct cmn_comm {
     // pipelined N > 1 step: pack(p+1) and update(p-1) on the caller's stream
     // overlap all-reduce(p) on a high-priority communication stream.
     int pipe_pieces = 4;
+    // NEXT-4 sharded update: items clipped to every rank's two-shot chunk
+    // (Item.reserved = owner), rank r's list is [sitem_begin[r], sitem_begin[r+1]).
+    std::vector<int> sitem_begin;
+    Item *d_sitems = nullptr;
     cudaStream_t sc = nullptr;
     std::vector<cudaEvent_t> pev;
 };
@@ -196,6 +200,8 @@ void free_registration(cmn_comm *c) {
     free_regions(c);
     cudaFree(c->d_td);
     cudaFree(c->d_items);
+    cudaFree(c->d_sitems);
+    c->d_sitems = nullptr;
     cudaFree(c->d_mom);
     cudaFree(c->d_adam);
     cudaFree(c->d_staging);
@@ -722,6 +728,69 @@ cmn_status step_pipelined(cmn_comm *c, const float *const *grads, int dtype, flo
     return CMN_OK;
 }
 
+// NEXT-4: reduce-scatter -> update own chunk -> all-gather parameters.
+// Per rank: pack (HBM) -> RS over NVLink (start barrier, call s) -> momentum
+// SGD on the own chunk only (1/N of the update traffic), publishing w' into
+// the fp32 exchange buffer -> gather of the other chunks' w' (start barrier,
+// call s+1: every peer's chunk update has completed).  Every element gets
+// exactly the arithmetic of the replicated update, so w is bitwise equal;
+// momentum is sharded (valid on the owner rank only).
+cmn_status step_sharded(cmn_comm *c, const float *const *grads, int dtype, float lr, float mu,
+                        cudaStream_t s) {
+    cmn_algo algo;
+    if (cmn_status st = begin_collective(c, 0, c->T, dtype, algo, s); st != CMN_OK) return st;
+    const int nsim = c->simulated ? c->world : 1;
+    const uint32_t seq1 = ++c->seq;
+    const int par = static_cast<int>(seq1 & 1u);
+    if (cmn_status st = pack_phase(c, 0, c->T, grads, dtype, par, s); st != CMN_OK) return st;
+    PeerBufs in{}, red{}, exch{};
+    for (int r = 0; r < c->world; ++r) {
+        in.p[r] = c->rb[r].packed[par];
+        red.p[r] = c->rb[r].reduced[0];
+        exch.p[r] = c->rb[r].reduced[1];
+    }
+    int64_t cs[kMaxWorld], ce[kMaxWorld];
+    chunk_plan(0, c->L, c->world, cs, ce);
+    const int blocks = ar_blocks_for(c);
+    Barrier bar = make_barrier(c, dtype | 2);
+    bar.value = (seq1 << 2) | static_cast<uint32_t>((dtype | 2) & 3);
+    for (int i = 0; i < nsim; ++i) {
+        const int r = c->simulated ? i : c->rank;
+        cmn_status st = launched(c,
+                                 launch_allreduce_twoshot(in, red, c->world, r, cs, ce, dtype, 1, bar,
+                                                          blocks, s),
+                                 "reduce_scatter");
+        if (st != CMN_OK) return st;
+    }
+    const float inv_n = 1.0f / static_cast<float>(c->world);
+    for (int i = 0; i < nsim; ++i) {
+        const int r = c->simulated ? i : c->rank;
+        cmn_status st = launched(c,
+                                 launch_update_chunk(c->d_td, c->d_sitems, c->sitem_begin[r],
+                                                     c->sitem_begin[r + 1], c->rb[r].reduced[0], dtype,
+                                                     static_cast<float *>(c->rb[r].reduced[1]), inv_n,
+                                                     lr, mu, s),
+                                 "update_chunk");
+        if (st != CMN_OK) return st;
+    }
+    const uint32_t seq2 = ++c->seq;
+    Barrier bar2 = make_barrier(c, 3);
+    bar2.value = (seq2 << 2) | 3u;
+    const int total = c->sitem_begin[c->world];
+    const int gblocks = total < blocks ? (total > 0 ? total : 1) : blocks;
+    for (int i = 0; i < nsim; ++i) {
+        const int r = c->simulated ? i : c->rank;
+        cmn_status st = launched(c,
+                                 launch_gather_params(c->d_td, c->d_sitems, 0, total, c->sitem_begin[r],
+                                                      c->sitem_begin[r + 1], exch, c->world, bar2,
+                                                      gblocks, s),
+                                 "gather_params");
+        if (st != CMN_OK) return st;
+    }
+    c->fresh = false;
+    return CMN_OK;
+}
+
 }  // namespace
 
 // =====================================================================
@@ -826,6 +895,27 @@ cmn_status cmn_register_params(cmn_comm *c, int T, const int *ndims, const int64
             CMN_CUDA(cudaMemcpy(c->d_items, c->h_items.data(), sizeof(Item) * c->h_items.size(),
                                 cudaMemcpyHostToDevice));
 
+        // Sharded-update item lists: items clipped to each rank's chunk.
+        {
+            std::vector<Item> sit;
+            int64_t cs[kMaxWorld], ce[kMaxWorld];
+            chunk_plan(0, c->L, c->world, cs, ce);
+            c->sitem_begin.assign(c->world + 1, 0);
+            for (int r = 0; r < c->world; ++r) {
+                c->sitem_begin[r] = static_cast<int>(sit.size());
+                for (const Item &it : c->h_items) {
+                    const int64_t lo = it.base > cs[r] ? it.base : cs[r];
+                    const int64_t hi = it.base + it.len < ce[r] ? it.base + it.len : ce[r];
+                    if (lo >= hi) continue;
+                    sit.push_back(Item{it.t, static_cast<int32_t>(hi - lo), it.k0 + (lo - it.base), lo, 0, r});
+                }
+            }
+            c->sitem_begin[c->world] = static_cast<int>(sit.size());
+            CMN_CUDA(cudaMalloc(&c->d_sitems, sizeof(Item) * (sit.empty() ? 1 : sit.size())));
+            if (!sit.empty())
+                CMN_CUDA(cudaMemcpy(c->d_sitems, sit.data(), sizeof(Item) * sit.size(),
+                                    cudaMemcpyHostToDevice));
+        }
         if (cmn_status st = alloc_regions(c); st != CMN_OK) return st;
         if (!c->simulated) {
             if (c->world > 1) {
@@ -899,6 +989,18 @@ cmn_status cmn_step(cmn_comm *c, const float *const *grads, cmn_dtype dtype, flo
                                              i1, dtype, lr, mu, s),
                         "update_direct");
     });
+}
+
+cmn_status cmn_step_sharded(cmn_comm *c, const float *const *grads, cmn_dtype dtype, float lr,
+                            float mu, void *stream) {
+    if (cmn_status st = require_registered(c); st != CMN_OK) return st;
+    if (cmn_status st = require_dtype(dtype); st != CMN_OK) return st;
+    if (c->world == 1) return cmn_step(c, grads, dtype, lr, mu, stream);
+    std::string why;
+    if (!grads_ok(c, grads, c->T * (c->simulated ? c->world : 1), why))
+        return fail(CMN_ERR_INVALID_ARG, why);
+    if (cmn_status st = set_device(c); st != CMN_OK) return st;
+    return step_sharded(c, grads, dtype, lr, mu, static_cast<cudaStream_t>(stream));
 }
 
 cmn_status cmn_step_host(cmn_comm *c, const float *const *host_grads, float *const *host_params,

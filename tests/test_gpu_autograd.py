@@ -105,7 +105,7 @@ def test_multi_node_optimizer_trains_and_matches_large_batch(cmn):
             loss = torch.nn.functional.cross_entropy(ref(x), y)
             loss.backward()
             opt_ref.step()
-            losses.append(float(loss))
+            losses.append(float(loss.detach()))
         torch.cuda.synchronize()
         for p, q in zip(model.parameters(), ref.parameters()):
             assert torch.allclose(p, q, rtol=1e-4, atol=1e-6), float((p - q).abs().max())

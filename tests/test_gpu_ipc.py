@@ -52,7 +52,9 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode, pieces=0):
             g = [torch.from_numpy(x).cuda() for x in synth.grads(shapes, workers=world, step=s)[rank]]
             if mode == "skip" and rank == 1 and s == 1:
                 continue                              # fault injection: rank 1 skips a collective
-            if pieces:
+            if mode == "sharded":
+                comm.step_sharded(g, dtype, 0.1, 0.9)  # RS -> own-chunk update -> param all-gather
+            elif pieces:
                 comm.step(g, dtype, 0.1, 0.9)         # pipelined schedule, 2 streams
             else:
                 comm.allreduce_grads(g, dtype)
@@ -106,6 +108,34 @@ def test_ipc_multiprocess_parity(orc, world, dtype, algo, pieces):
     for r in res:
         assert np.array_equal(np.frombuffer(r[2], np.uint32), want_w), f"rank {r[0]} w"
         assert np.array_equal(np.frombuffer(r[3], np.uint32), want_v), f"rank {r[0]} v"
+
+
+@pytest.mark.parametrize("world,dtype", [(2, "fp32"), (3, "fp16")])
+def test_ipc_sharded_update(orc, world, dtype):
+    """NEXT-4 across processes: every rank ends with the oracle's w (bitwise);
+    the momentum is current on each rank's own chunk."""
+    from paper_1908_00213_b200 import cmn
+    res = _run(world, dtype, "twoshot", mode="sharded")
+    assert all(r[1] == "ok" for r in res), res
+    shapes = synth.mlp_shapes()
+    w = synth.params(shapes)
+    v = [np.zeros_like(x) for x in w]
+    for s in range(2):
+        orc.step(synth.grads(shapes, workers=world, step=s), w, v, 0.1, 0.9, dtype)
+    want_w = np.concatenate(w).view(np.uint32)
+    sizes = [x.size for x in w]
+    off, L = orc.layout(sizes)
+    starts, ends = cmn.plan_chunks(L, world)
+    vflat = np.concatenate(v).view(np.uint32)
+    for r in res:
+        assert np.array_equal(np.frombuffer(r[2], np.uint32), want_w), f"rank {r[0]} w"
+        got_v = np.frombuffer(r[3], np.uint32)
+        pos = 0
+        for t, n in enumerate(sizes):          # elements (t, k) with packed index in own chunk
+            j = off[t] + np.arange(n)
+            own = (j >= starts[r[0]]) & (j < ends[r[0]])
+            assert np.array_equal(got_v[pos:pos + n][own], vflat[pos:pos + n][own]), f"rank {r[0]} v[{t}]"
+            pos += n
 
 
 def test_ipc_skipped_collective_times_out():

@@ -269,6 +269,29 @@ def test_pipelined_step_parity(cmn, orc, N, pieces, dtype):
         comm.finalize()
 
 
+@pytest.mark.parametrize("N,dtype", [(2, "fp32"), (3, "fp16"), (4, "fp32"), (8, "fp16"), (8, "fp32")])
+def test_sharded_update_parity(cmn, orc, N, dtype):
+    """NEXT-4 (cmn_step_sharded): reduce-scatter, update of the own chunk,
+    all-gather of parameters == oracle bitwise over 3 steps (w, and v, which
+    the simulated ranks together update in full)."""
+    shapes = synth.resnet50_shapes()[:30] + RAGGED
+    grads = [synth.grads(shapes, workers=N, step=s) for s in range(3)]
+    params0 = synth.params(shapes)
+    ora, _, _ = run_oracle(orc, shapes, N, dtype, grads, params0, 0.1, 0.9)
+    comm = cmn.Comm.simulated_world(N)
+    try:
+        w = to_dev(params0)
+        comm.register_params(w)
+        for s, g in enumerate(grads):
+            comm.step_sharded([to_dev(gw) for gw in g], dtype, 0.1, 0.9)
+            torch.cuda.synchronize()
+            for t in range(len(w)):
+                assert_bitwise(w[t].cpu().numpy().reshape(-1), ora[s]["w"][t], f"w[{t}] step {s}")
+                assert_bitwise(comm.momentum(t).cpu().numpy().reshape(-1), ora[s]["v"][t], f"v[{t}]")
+    finally:
+        comm.finalize()
+
+
 def test_buckets_bitwise_equal_unbucketed(cmn, orc):
     """Overlap reading R15: bucketed (reverse order, any size) == unbucketed."""
     shapes = synth.resnet50_shapes()[:40]
