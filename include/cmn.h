@@ -39,9 +39,14 @@
  *     (cmn_register_params, cmn_allreduce_*, cmn_step*) with the same layout
  *     and dtype ("model structures are
  *     identical between workers merely in a single iteration").
- *   - CUDA graphs: N == 1 and simulated communicators may be captured.  The
- *     multi-process collectives pass per-call sequence numbers as kernel
- *     arguments and refuse capture (CMN_ERR_UNSUPPORTED) rather than race.
+ *   - CUDA graphs: barrier values live in device-resident per-CTA epoch
+ *     counters, so collectives replay correctly from a captured graph.  The
+ *     schedules whose buffer reuse does not rely on host-chosen alternation
+ *     -- cmn_step with cmn_set_pipeline >= 2 (the default) and
+ *     cmn_step_sharded -- may be captured; the single-call schedules
+ *     (cmn_allreduce_grads, buckets, unpipelined cmn_step) return
+ *     CMN_ERR_UNSUPPORTED under capture instead of racing.  N == 1 and
+ *     simulated communicators may always be captured.
  *   - There is no CPU fallback: if the CUDA device or the sm_100a kernels are
  *     unavailable every compute entry point fails with CMN_ERR_CUDA.
  */

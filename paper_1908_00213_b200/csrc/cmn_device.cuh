@@ -93,29 +93,47 @@ __device__ __forceinline__ uint64_t global_timer_ns() {
     return t;
 }
 
+// This call's barrier value for the calling CTA: reads and advances the
+// CTA's epoch counter (one increment per collective kernel; the next kernel
+// on the stream starts after this one completes, so reads see the update).
+__device__ __forceinline__ uint32_t barrier_value(const Barrier &bar) {
+    __shared__ uint32_t s_val;
+    if (!bar.enabled) return 0;
+    if (threadIdx.x == 0) {
+        const uint32_t e = bar.epoch[blockIdx.x] + 1u;
+        bar.epoch[blockIdx.x] = e;
+        s_val = (e << 2) | (bar.tag & 3u);
+    }
+    __syncthreads();
+    return s_val;
+}
+
 // Pairwise per-CTA barrier across ranks: CTA b of rank r tells CTA b of
 // every rank "my inputs for this phase are published" and waits for the
-// same from all of them.  Flag values are (seq << 2) | tag and only grow,
-// so no reset is needed; a peer at the same seq with another tag (payload
-// dtype or algorithm) is a call-sequence mismatch.  Spins are bounded by
-// %globaltimer (default 30 s).
-__device__ __forceinline__ void cross_rank_barrier(const Barrier &bar, int world, int slot) {
+// same from all of them.  Flag values only grow, so no reset is needed; a
+// peer at the same epoch with another tag (payload dtype or algorithm) is a
+// call-sequence mismatch.  Spins are bounded by %globaltimer (default 30 s,
+// SPEC.md:569).  Because a kernel starts only after the previous kernel on
+// its stream completed, passing the barrier also proves every peer finished
+// all its earlier collective kernels.
+__device__ __forceinline__ void cross_rank_barrier(const Barrier &bar, uint32_t value, int world,
+                                                   int slot) {
     if (!bar.enabled) return;
     __syncthreads();
     const int tid = threadIdx.x;
     if (tid < world) {
         const size_t cell = (static_cast<size_t>(slot) * kMaxBarrierBlocks + blockIdx.x) * kMaxWorld;
         __threadfence_system();
-        st_release_sys(bar.flags[tid] + cell + bar.rank, bar.value);
+        st_release_sys(bar.flags[tid] + cell + bar.rank, value);
         const uint32_t *mine = bar.flags[bar.rank] + cell + tid;
         uint64_t t0 = 0;
         for (uint32_t spin = 1;; ++spin) {
             const uint32_t v = ld_acquire_sys(mine);
-            if ((v >> 2) == (bar.value >> 2) && v != bar.value) {
+            if ((v >> 2) == (value >> 2) && v != value) {
                 *reinterpret_cast<volatile int *>(bar.err) = 2;
                 break;
             }
-            if (static_cast<int32_t>(v - bar.value) >= 0) break;
+            if (static_cast<int32_t>(v - value) >= 0) break;
             if ((spin & 1023u) == 0) {
                 const uint64_t t = global_timer_ns();
                 if (t0 == 0) {

@@ -49,11 +49,18 @@ struct GradTab {
 // Cross-rank signalling for the P2P all-reduce.  flags[r] points at rank r's
 // signal pad (IPC-mapped for peers); pad layout:
 //   uint32 [kBarrierSlots][kMaxBarrierBlocks][kMaxWorld]
+// The value CTA b signals in a call is ((epoch[b] + 1) << 2) | tag, where
+// epoch[b] is a per-CTA call counter in the rank's own device memory that
+// the kernel itself advances -- nothing call-specific is a kernel argument,
+// so a captured CUDA graph replays with fresh values.  Every rank issues the
+// same collectives with the same grids, so epoch[b] agrees across ranks.
 struct Barrier {
     uint32_t *flags[kMaxWorld];
+    uint32_t *epoch;    // kMaxBarrierBlocks per-CTA counters (own memory)
     int rank;
     int enabled;        // 0 in simulated mode: stream order replaces barriers
-    uint32_t value;     // (seq << 2) | tag expected from every peer this call
+    uint32_t tag;       // 2 bits: payload dtype | algorithm; a same-epoch
+                        // different-tag peer is a call-sequence mismatch
     uint64_t timeout_ns;
     int *err;           // host-mapped error word: 0 ok, 1 timeout, 2 mismatch
 };

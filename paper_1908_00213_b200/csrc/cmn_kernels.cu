@@ -337,7 +337,8 @@ __global__ void __launch_bounds__(kThreads) k_oneshot(const __grid_constant__ Pe
                                                       void *__restrict__ out, int64_t v0,
                                                       int64_t v1,
                                                       const __grid_constant__ Barrier bar) {
-    cross_rank_barrier(bar, N, 0);
+    const uint32_t bv = barrier_value(bar);
+    cross_rank_barrier(bar, bv, N, 0);
     for (int64_t tile = v0 + static_cast<int64_t>(blockIdx.x) * kTileVecs; tile < v1;
          tile += static_cast<int64_t>(gridDim.x) * kTileVecs) {
         uint4 x[kARVec][N];
@@ -372,8 +373,9 @@ __global__ void __launch_bounds__(kThreads) k_twoshot(const __grid_constant__ Pe
                                                       const __grid_constant__ Chunks ch,
                                                       int phases,
                                                       const __grid_constant__ Barrier bar) {
+    const uint32_t bv = barrier_value(bar);
     if (phases & 1) {
-        cross_rank_barrier(bar, N, 0);
+        cross_rank_barrier(bar, bv, N, 0);
         const int64_t s = ch.s[rank], e = ch.e[rank];
         uint4 *dst = static_cast<uint4 *>(const_cast<void *>(red.p[rank]));
         for (int64_t tile = s + static_cast<int64_t>(blockIdx.x) * kTileVecs; tile < e;
@@ -395,7 +397,7 @@ __global__ void __launch_bounds__(kThreads) k_twoshot(const __grid_constant__ Pe
         }
     }
     if (phases & 2) {
-        cross_rank_barrier(bar, N, 1);
+        cross_rank_barrier(bar, bv, N, 1);
         uint4 *dst = static_cast<uint4 *>(const_cast<void *>(red.p[rank]));
         int64_t maxlen = 0;
 #pragma unroll
@@ -483,7 +485,8 @@ __global__ void __launch_bounds__(kThreads) k_gather_params(const TensorDesc *__
                                                             const __grid_constant__ PeerBufs exch,
                                                             int world,
                                                             const __grid_constant__ Barrier bar) {
-    cross_rank_barrier(bar, world, 0);
+    const uint32_t bv = barrier_value(bar);
+    cross_rank_barrier(bar, bv, world, 0);
     for (int i = i0 + blockIdx.x; i < i1; i += gridDim.x) {
         if (i >= s0 && i < s1) continue;
         const Item it = items[i];

@@ -104,6 +104,7 @@ struct RankBufs {
     void *packed[2] = {nullptr, nullptr};
     void *reduced[2] = {nullptr, nullptr};
     uint32_t *flags = nullptr;
+    uint32_t *epoch = nullptr;   // per-CTA call counters (read by own kernels only)
     bool mapped = false;  // IPC-opened peer region
 };
 
@@ -224,10 +225,12 @@ void carve(RankBufs &b, char *base, int64_t L) {
     b.reduced[0] = base + 2 * buf;
     b.reduced[1] = base + 3 * buf;
     b.flags = reinterpret_cast<uint32_t *>(base + 4 * buf);
+    b.epoch = b.flags + static_cast<size_t>(kBarrierSlots) * kMaxBarrierBlocks * kMaxWorld;
 }
 
-size_t flags_bytes() {
-    return static_cast<size_t>(kBarrierSlots) * kMaxBarrierBlocks * kMaxWorld * sizeof(uint32_t);
+size_t flags_bytes() {   // signal pad + per-CTA epoch counters
+    return (static_cast<size_t>(kBarrierSlots) * kMaxBarrierBlocks * kMaxWorld + kMaxBarrierBlocks) *
+           sizeof(uint32_t);
 }
 
 cmn_status plan_layout_impl(int T, const int *ndims, const int64_t *dims,
@@ -362,9 +365,10 @@ GradTab make_tab(const float *const *g, int lo, int hi) {
 Barrier make_barrier(cmn_comm *c, int tag) {
     Barrier b{};
     for (int r = 0; r < c->world; ++r) b.flags[r] = c->rb[r].flags;
+    b.epoch = c->rb[c->rank].epoch;
     b.rank = c->rank;
     b.enabled = c->simulated ? 0 : 1;
-    b.value = (c->seq << 2) | static_cast<uint32_t>(tag & 3);
+    b.tag = static_cast<uint32_t>(tag & 3);
     b.timeout_ns = static_cast<uint64_t>(c->timeout_ms) * 1000000ull;
     b.err = c->d_err;
     return b;
@@ -434,8 +438,7 @@ cmn_status reduce_phase(cmn_comm *c, int ta, int tb, int dtype, uint32_t seq, cm
     }
     const int blocks = ar_blocks_for(c);
     const int tag = dtype | (algo == CMN_ALGO_TWOSHOT ? 2 : 0);
-    Barrier bar = make_barrier(c, tag);
-    bar.value = (seq << 2) | static_cast<uint32_t>(tag & 3);
+    const Barrier bar = make_barrier(c, tag);
     if (algo == CMN_ALGO_ONESHOT) {
         for (int i = 0; i < nsim; ++i) {
             const int r = c->simulated ? i : c->rank;
@@ -467,20 +470,27 @@ cmn_status reduce_phase(cmn_comm *c, int ta, int tb, int dtype, uint32_t seq, cm
 }
 
 // Validate and choose the algorithm for one collective over [ta, tb).
-// Cross-process collectives carry host-assigned sequence numbers and buffer
-// parities as kernel arguments, which a CUDA graph would freeze: replays
-// would pass barriers early.  Refuse capture loudly instead of racing.
-// (N = 1 and simulated communicators have no cross-process state and may be
-// captured.)
+// CUDA-graph policy.  Barrier values come from device-resident per-CTA
+// epochs, so replays never pass a barrier early.  What a graph does freeze is
+// the host-chosen packed-buffer parity: a single collective per step needs
+// consecutive calls to alternate buffers (a peer may still be reading the
+// previous call's packed buffer when the next pack starts), which a replayed
+// graph with one call cannot do.  Schedules whose buffer safety does not
+// depend on alternation -- the pipelined step (P >= 2 pieces: a region's
+// previous reader is >= 2 calls back) and the sharded step (every overwrite
+// is behind a start barrier) -- pass graph_safe = true and may be captured;
+// the single-call schedules refuse capture loudly instead of racing.
+// (N = 1 and simulated communicators have no cross-process state.)
 cmn_status begin_collective(cmn_comm *c, int ta, int tb, int dtype, cmn_algo &algo,
-                            cudaStream_t s) {
+                            cudaStream_t s, bool graph_safe) {
     if (cmn_status st = check_async_error(c); st != CMN_OK) return st;
-    if (!c->simulated && c->world > 1) {
+    if (!c->simulated && c->world > 1 && !graph_safe) {
         cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
         CMN_CUDA(cudaStreamIsCapturing(s, &cap));
         if (cap != cudaStreamCaptureStatusNone)
             return fail(CMN_ERR_UNSUPPORTED,
-                        "multi-process collectives cannot be captured into a CUDA graph");
+                        "this collective schedule cannot be captured into a CUDA graph "
+                        "(use cmn_step with cmn_set_pipeline >= 2, or cmn_step_sharded)");
     }
     const size_t esz = dtype == 0 ? 4 : 2;
     algo = choose_algo(c, static_cast<size_t>(c->off[tb] - c->off[ta]) * esz);
@@ -494,7 +504,7 @@ cmn_status begin_collective(cmn_comm *c, int ta, int tb, int dtype, cmn_algo &al
 cmn_status allreduce_range(cmn_comm *c, int ta, int tb, const float *const *grads, int dtype,
                            cudaStream_t s) {
     cmn_algo algo;
-    if (cmn_status st = begin_collective(c, ta, tb, dtype, algo, s); st != CMN_OK) return st;
+    if (cmn_status st = begin_collective(c, ta, tb, dtype, algo, s, false); st != CMN_OK) return st;
     const uint32_t seq = ++c->seq;
     const int par = static_cast<int>(seq & 1u);
     if (cmn_status st = pack_phase(c, ta, tb, grads, dtype, par, s); st != CMN_OK) return st;
@@ -695,7 +705,8 @@ cmn_status step_pipelined(cmn_comm *c, const float *const *grads, int dtype, flo
     if (cmn_status st = ensure_comm_stream(c, 2 * P + 1); st != CMN_OK) return st;
     std::vector<cmn_algo> algo(P);
     for (size_t p = 0; p < P; ++p)
-        if (cmn_status st = begin_collective(c, pieces[p].first, pieces[p].second, dtype, algo[p], s);
+        if (cmn_status st = begin_collective(c, pieces[p].first, pieces[p].second, dtype, algo[p], s,
+                                             P >= 2);
             st != CMN_OK)
             return st;
     cudaEvent_t entry = c->pev[2 * P];
@@ -738,7 +749,7 @@ cmn_status step_pipelined(cmn_comm *c, const float *const *grads, int dtype, flo
 cmn_status step_sharded(cmn_comm *c, const float *const *grads, int dtype, float lr, float mu,
                         cudaStream_t s) {
     cmn_algo algo;
-    if (cmn_status st = begin_collective(c, 0, c->T, dtype, algo, s); st != CMN_OK) return st;
+    if (cmn_status st = begin_collective(c, 0, c->T, dtype, algo, s, true); st != CMN_OK) return st;
     const int nsim = c->simulated ? c->world : 1;
     const uint32_t seq1 = ++c->seq;
     const int par = static_cast<int>(seq1 & 1u);
@@ -752,8 +763,7 @@ cmn_status step_sharded(cmn_comm *c, const float *const *grads, int dtype, float
     int64_t cs[kMaxWorld], ce[kMaxWorld];
     chunk_plan(0, c->L, c->world, cs, ce);
     const int blocks = ar_blocks_for(c);
-    Barrier bar = make_barrier(c, dtype | 2);
-    bar.value = (seq1 << 2) | static_cast<uint32_t>((dtype | 2) & 3);
+    const Barrier bar = make_barrier(c, dtype | 2);
     for (int i = 0; i < nsim; ++i) {
         const int r = c->simulated ? i : c->rank;
         cmn_status st = launched(c,
@@ -773,9 +783,8 @@ cmn_status step_sharded(cmn_comm *c, const float *const *grads, int dtype, float
                                  "update_chunk");
         if (st != CMN_OK) return st;
     }
-    const uint32_t seq2 = ++c->seq;
-    Barrier bar2 = make_barrier(c, 3);
-    bar2.value = (seq2 << 2) | 3u;
+    ++c->seq;
+    const Barrier bar2 = make_barrier(c, 3);
     const int total = c->sitem_begin[c->world];
     const int gblocks = total < blocks ? (total > 0 ? total : 1) : blocks;
     for (int i = 0; i < nsim; ++i) {

@@ -48,6 +48,36 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode, pieces=0):
             return
         comm.set_algo(algo)
         comm.set_pipeline(pieces)
+        if mode == "capture_unpipelined":
+            g0 = [torch.from_numpy(x).cuda() for x in synth.grads(shapes, workers=world)[rank]]
+            comm.allreduce_grads(g0, dtype)          # eager warm-up is fine
+            comm.update_momentum_sgd(0.1, 0.9)
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            try:
+                with torch.cuda.graph(graph):
+                    comm.allreduce_grads(g0, dtype)
+                q.put((rank, "ok-unexpected"))
+            except cmn.CmnError as e:
+                q.put((rank, "error", e.status_name))
+            dist.barrier()
+            return
+        if mode in ("graph", "graph_sharded"):
+            # step 0 eagerly (creates internal streams), then capture ONE step
+            # into a CUDA graph and replay it for steps 1.. with fresh grads
+            # copied into the captured buffers.
+            gs = [torch.from_numpy(x).cuda() for x in synth.grads(shapes, workers=world, step=0)[rank]]
+            fn = comm.step_sharded if mode == "graph_sharded" else comm.step
+            fn(gs, dtype, 0.1, 0.9)
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                fn(gs, dtype, 0.1, 0.9)
+            for s in range(1, steps):
+                for dst, x in zip(gs, synth.grads(shapes, workers=world, step=s)[rank]):
+                    dst.copy_(torch.from_numpy(x))
+                graph.replay()
+            steps = 0
         for s in range(steps):
             g = [torch.from_numpy(x).cuda() for x in synth.grads(shapes, workers=world, step=s)[rank]]
             if mode == "skip" and rank == 1 and s == 1:
@@ -136,6 +166,29 @@ def test_ipc_sharded_update(orc, world, dtype):
             own = (j >= starts[r[0]]) & (j < ends[r[0]])
             assert np.array_equal(got_v[pos:pos + n][own], vflat[pos:pos + n][own]), f"rank {r[0]} v[{t}]"
             pos += n
+
+
+@pytest.mark.parametrize("world,dtype,mode,pieces", [(2, "fp32", "graph", 2), (3, "fp16", "graph", 4),
+                                                    (2, "fp32", "graph_sharded", 0)])
+def test_ipc_cuda_graph_replay(orc, world, dtype, mode, pieces):
+    """A captured CUDA graph of one multi-process step, replayed for steps
+    1..3: device-resident barrier epochs advance on every replay, results
+    stay bit-exact (pipelined schedule and sharded step)."""
+    res = _run(world, dtype, "twoshot", steps=4, mode=mode, pieces=pieces)
+    assert all(r[1] == "ok" for r in res), res
+    shapes = synth.mlp_shapes()
+    w = synth.params(shapes)
+    v = [np.zeros_like(x) for x in w]
+    for s in range(4):
+        orc.step(synth.grads(shapes, workers=world, step=s), w, v, 0.1, 0.9, dtype)
+    want_w = np.concatenate(w).view(np.uint32)
+    for r in res:
+        assert np.array_equal(np.frombuffer(r[2], np.uint32), want_w), f"rank {r[0]} w"
+
+
+def test_ipc_single_call_schedule_refuses_capture():
+    res = _run(2, "fp32", "oneshot", mode="capture_unpipelined")
+    assert all(r[1] == "error" and r[2] == "CMN_ERR_UNSUPPORTED" for r in res), res
 
 
 def test_ipc_skipped_collective_times_out():
