@@ -62,10 +62,12 @@ __device__ __forceinline__ float load_r1(const void *r, int64_t j) {
 }
 
 // ------------------------------------------------------------------- a1
-// Each CTA packs kPackItems consecutive items; all of their loads are issued
-// before the first store (16 x 16 B in flight per thread), so the short
-// load->store lifetime of a CTA does not leave HBM idle.
-constexpr int kPackItems = 4;
+// Each CTA packs kPackItems consecutive items, all loads issued before the
+// first store.  The probe scripts/pack_variants.cu (profiles/r1_pack_variants.jsonl)
+// measured 1 item per CTA best (6.2 TB/s fp32, 6.6 TB/s fp16; 4 per CTA costs
+// 2-6 %: fewer resident CTAs); what made the first version slow was a
+// dependent TensorDesc load per item, now folded into Item.base/pad.
+constexpr int kPackItems = 1;
 
 template <int DT>
 __device__ __forceinline__ void pack_store(void *packed, int64_t j, const float4 &x) {

@@ -64,10 +64,13 @@ size_t env_size(const char *name, size_t dflt) {
 // ---------------------------------------------------------------- NCCL
 // The comparison backend is loaded with dlopen so the library has no hard
 // dependency on libnccl (only CMN_ALGO_NCCL needs it).
+struct NcclUniqueId {   // layout of ncclUniqueId (NCCL_UNIQUE_ID_BYTES = 128), passed BY VALUE
+    char internal[128];
+};
 struct NcclApi {
     void *h = nullptr;
-    int (*GetUniqueId)(void *) = nullptr;
-    int (*CommInitRank)(void **, int, const void *, int) = nullptr;
+    int (*GetUniqueId)(NcclUniqueId *) = nullptr;
+    int (*CommInitRank)(void **, int, NcclUniqueId, int) = nullptr;
     int (*AllReduce)(const void *, void *, size_t, int, int, void *, cudaStream_t) = nullptr;
     int (*CommDestroy)(void *) = nullptr;
     const char *(*GetErrorString)(int) = nullptr;
@@ -80,8 +83,8 @@ struct NcclApi {
             if (h) break;
         }
         if (!h) return false;
-        GetUniqueId = reinterpret_cast<int (*)(void *)>(dlsym(h, "ncclGetUniqueId"));
-        CommInitRank = reinterpret_cast<int (*)(void **, int, const void *, int)>(
+        GetUniqueId = reinterpret_cast<int (*)(NcclUniqueId *)>(dlsym(h, "ncclGetUniqueId"));
+        CommInitRank = reinterpret_cast<int (*)(void **, int, NcclUniqueId, int)>(
             dlsym(h, "ncclCommInitRank"));
         AllReduce = reinterpret_cast<int (*)(const void *, void *, size_t, int, int, void *,
                                              cudaStream_t)>(dlsym(h, "ncclAllReduce"));
@@ -91,7 +94,6 @@ struct NcclApi {
     }
 };
 NcclApi g_nccl;
-constexpr int kNcclUniqueIdBytes = 128;
 constexpr int kNcclFloat16 = 6, kNcclFloat32 = 7, kNcclSum = 0;
 constexpr int kE2EPieces = 8;   // pipeline depth of the host-buffer step
 
@@ -419,7 +421,9 @@ cmn_status reduce_phase(cmn_comm *c, int ta, int tb, int dtype, uint32_t seq, cm
     const int64_t e0 = c->off[ta], e1 = c->off[tb];
     const size_t esz = dtype == 0 ? 4 : 2;
     const int nsim = c->simulated ? c->world : 1;
-    if (c->world == 1) return CMN_OK;   // identity (fp16 rounding done by the pack)
+    // identity at N = 1 (fp16 rounding done by the pack) -- except through
+    // NCCL, whose single-rank all-reduce exercises the comparison plumbing
+    if (c->world == 1 && algo != CMN_ALGO_NCCL) return CMN_OK;
     if (algo == CMN_ALGO_NCCL) {
         void *src = static_cast<char *>(c->rb[c->rank].packed[par]) + e0 * esz;
         void *dst = static_cast<char *>(c->rb[c->rank].reduced[par]) + e0 * esz;
@@ -503,13 +507,13 @@ cmn_status begin_collective(cmn_comm *c, int ta, int tb, int dtype, cmn_algo &al
 // a1 + a2 over the tensor range [ta, tb) (whole model or one bucket).
 cmn_status allreduce_range(cmn_comm *c, int ta, int tb, const float *const *grads, int dtype,
                            cudaStream_t s) {
-    cmn_algo algo;
+    cmn_algo algo = CMN_ALGO_AUTO;
     if (cmn_status st = begin_collective(c, ta, tb, dtype, algo, s, false); st != CMN_OK) return st;
     const uint32_t seq = ++c->seq;
     const int par = static_cast<int>(seq & 1u);
     if (cmn_status st = pack_phase(c, ta, tb, grads, dtype, par, s); st != CMN_OK) return st;
     if (cmn_status st = reduce_phase(c, ta, tb, dtype, seq, algo, s); st != CMN_OK) return st;
-    c->last = ArResult{par, dtype, c->world == 1};
+    c->last = ArResult{par, dtype, c->world == 1 && algo != CMN_ALGO_NCCL};
     return CMN_OK;
 }
 
@@ -748,7 +752,7 @@ cmn_status step_pipelined(cmn_comm *c, const float *const *grads, int dtype, flo
 // momentum is sharded (valid on the owner rank only).
 cmn_status step_sharded(cmn_comm *c, const float *const *grads, int dtype, float lr, float mu,
                         cudaStream_t s) {
-    cmn_algo algo;
+    cmn_algo algo = CMN_ALGO_AUTO;
     if (cmn_status st = begin_collective(c, 0, c->T, dtype, algo, s, true); st != CMN_OK) return st;
     const int nsim = c->simulated ? c->world : 1;
     const uint32_t seq1 = ++c->seq;
@@ -1259,15 +1263,17 @@ cmn_status cmn_set_algo(cmn_comm *c, cmn_algo algo, size_t oneshot_max_bytes) {
         if (c->simulated) return fail(CMN_ERR_UNSUPPORTED, "NCCL needs one process per GPU");
         if (!g_nccl.load()) return fail(CMN_ERR_NCCL, "cannot load libnccl (set CMN_NCCL_LIB)");
         if (cmn_status st = set_device(c); st != CMN_OK) return st;
-        char id[kNcclUniqueIdBytes] = {0};
-        if (c->rank == 0 && g_nccl.GetUniqueId(id) != 0)
+        NcclUniqueId id{};
+        if (c->rank == 0 && g_nccl.GetUniqueId(&id) != 0)
             return fail(CMN_ERR_NCCL, "ncclGetUniqueId failed");
-        std::vector<char> all(static_cast<size_t>(kNcclUniqueIdBytes) * c->world);
-        if (!allgather(c, id, all.data(), kNcclUniqueIdBytes))
+        std::vector<NcclUniqueId> all(c->world);
+        if (!allgather(c, &id, all.data(), sizeof(NcclUniqueId)))
             return fail(CMN_ERR_BOOTSTRAP, "allgather callback failed");
         void *comm = nullptr;
-        const int rc = g_nccl.CommInitRank(&comm, c->world, all.data(), c->rank);
-        if (rc != 0) return fail(CMN_ERR_NCCL, "ncclCommInitRank failed");
+        const int rc = g_nccl.CommInitRank(&comm, c->world, all[0], c->rank);   // rank 0's id
+        if (rc != 0)
+            return fail(CMN_ERR_NCCL, std::string("ncclCommInitRank: ") +
+                                          (g_nccl.GetErrorString ? g_nccl.GetErrorString(rc) : "?"));
         c->nccl = comm;
     }
     c->algo = algo;

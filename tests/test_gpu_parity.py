@@ -434,6 +434,30 @@ def test_step_host_packed_simulated(cmn, orc):
         comm.finalize()
 
 
+@pytest.mark.parametrize("dtype", ["fp32", "fp16"])
+def test_nccl_comparison_plumbing_single_rank(cmn, orc, dtype):
+    """CMN_ALGO_NCCL through a real (single-rank) NCCL communicator: dlopen of
+    libnccl, ncclCommInitRank via the bootstrap path, ncclAllReduce on the
+    packed buffer; a one-rank sum is exact, so the step is bit-exact.  (NCCL
+    refuses two ranks on one GPU; its multi-rank numbers need >= 2 GPUs.)"""
+    shapes = synth.mlp_shapes()
+    g = synth.grads(shapes, workers=1)
+    params0 = synth.params(shapes)
+    ora, _, _ = run_oracle(orc, shapes, 1, dtype, [g], params0, 0.1, 0.9)
+    comm = cmn.Comm.init(0, 1, 0)
+    try:
+        w = to_dev(params0)
+        comm.register_params(w)
+        comm.set_algo("nccl")
+        comm.allreduce_grads(to_dev(g[0]), dtype)
+        comm.update_momentum_sgd(0.1, 0.9)
+        torch.cuda.synchronize()
+        for t in range(len(w)):
+            assert_bitwise(w[t].cpu().numpy().reshape(-1), ora[0]["w"][t], f"w[{t}]")
+    finally:
+        comm.finalize()
+
+
 def test_errors_are_loud(cmn):
     shapes = synth.mlp_shapes()
     comm = cmn.Comm.simulated_world(2)
