@@ -345,10 +345,31 @@ def main():
             t = torch.tensor([e_ms], dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
+        # the PCIe bound of this e2e step: bare pinned H2D and D2H of the same
+        # bytes, alone; with the call's H2D/update/D2H pipeline the floor is
+        # about max(h2d, d2h), without overlap h2d + d2h
+        dbuf = torch.empty(L, dtype=torch.float32, device=dev)
+
+        def copy_us(fn):
+            fn()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(5):
+                fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            return a.elapsed_time(b) / 5 * 1e3
+
+        h2d_us = copy_us(lambda: dbuf.copy_(hg_flat, non_blocking=True))
+        d2h_us = copy_us(lambda: hw_flat.copy_(dbuf, non_blocking=True))
+        del dbuf
         e2e = {"value": e_ms * 1e3, "unit": "us", "h2d_bytes_per_step": 4 * L,
+               "pcie_h2d_us": h2d_us, "pcie_d2h_us": d2h_us,
+               "overlap_floor_us": max(h2d_us, d2h_us), "serial_floor_us": h2d_us + d2h_us,
                "d2h_bytes_per_step": 4 * L,
                "path": "cmn_step_host_packed: pinned host grads (packed layout) -> device, "
-                       "step, params -> pinned host; pipelined over 8 tensor ranges at N=1"}
+                       "step, params -> pinned host; pipelined over 32 tensor ranges at N=1"}
 
     comm.finalize()
     if rank != 0:

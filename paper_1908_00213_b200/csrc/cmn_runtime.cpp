@@ -95,7 +95,7 @@ struct NcclApi {
 };
 NcclApi g_nccl;
 constexpr int kNcclFloat16 = 6, kNcclFloat32 = 7, kNcclSum = 0;
-constexpr int kE2EPieces = 8;   // pipeline depth of the host-buffer step
+constexpr int kE2EPieces = 32;  // pipeline depth of the host-buffer step (fill+drain ~ 1/32 of the copies)
 
 }  // namespace
 

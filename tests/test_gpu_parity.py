@@ -458,6 +458,46 @@ def test_nccl_comparison_plumbing_single_rank(cmn, orc, dtype):
         comm.finalize()
 
 
+MANY = [(i % 7 + 1, 3) if i % 3 else (i % 5,) for i in range(600)]   # 600 tensors, incl. empty ones
+TINY = [(1,), (2,), (3,)]                                               # L = 192: most chunks empty at N = 8
+
+
+@pytest.mark.parametrize("shapes_name", ["many", "tiny"])
+@pytest.mark.parametrize("N", [1, 3, 8])
+def test_edge_layouts_all_schedules(cmn, orc, shapes_name, N):
+    """600 tensors (3 launch groups of <= 256 grad pointers, zero-size tensors)
+    and a 3-tensor model whose two-shot chunks are mostly empty at N = 8:
+    unpipelined one-/two-shot, pipelined and sharded steps all bit-exact."""
+    shapes = MANY if shapes_name == "many" else TINY
+    grads = [synth.grads(shapes, workers=N, step=s, seed=11) for s in range(2)]
+    params0 = synth.params(shapes, seed=11)
+    for dtype in ("fp32", "fp16"):
+        ora, _, _ = run_oracle(orc, shapes, N, dtype, grads, params0, 0.1, 0.9)
+        for sched in ("oneshot", "twoshot", "pipelined", "sharded"):
+            comm = cmn.Comm.simulated_world(N) if N > 1 else cmn.Comm.init(0, 1, 0)
+            try:
+                w = to_dev(params0)
+                comm.register_params(w)
+                for s, g in enumerate(grads):
+                    gd = [to_dev(gw) for gw in g] if N > 1 else to_dev(g[0])
+                    if sched in ("oneshot", "twoshot"):
+                        if N > 1:
+                            comm.set_algo(sched)
+                        comm.allreduce_grads(gd, dtype)
+                        comm.update_momentum_sgd(0.1, 0.9)
+                    elif sched == "pipelined":
+                        comm.set_pipeline(3)
+                        comm.step(gd, dtype, 0.1, 0.9)
+                    else:
+                        comm.step_sharded(gd, dtype, 0.1, 0.9)
+                    torch.cuda.synchronize()
+                    for t in range(len(w)):
+                        assert_bitwise(w[t].cpu().numpy().reshape(-1), ora[s]["w"][t],
+                                       f"{sched} {dtype} w[{t}] step {s}")
+            finally:
+                comm.finalize()
+
+
 def test_errors_are_loud(cmn):
     shapes = synth.mlp_shapes()
     comm = cmn.Comm.simulated_world(2)
