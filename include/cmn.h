@@ -132,7 +132,10 @@ cmn_status cmn_init(int rank, int world_size, int cuda_device,
 cmn_status cmn_init_simulated(int world_size, int cuda_device, cmn_comm **out);
 
 /* cmn_finalize -- synchronise the device, unmap peers, free everything the
- * library owns.  NULL is a no-op. */
+ * library owns.  NULL is a no-op.  With world_size > 1 peers read this
+ * rank's exported buffers during collectives, so call it only after every
+ * rank has finished its last collective (e.g. after a host barrier);
+ * re-registration performs that barrier itself. */
 cmn_status cmn_finalize(cmn_comm *comm);
 
 /* ------------------------------------------------------------------------
@@ -223,7 +226,7 @@ cmn_status cmn_step_host(cmn_comm *comm, const float *const *host_grads,
  * rank (gradient t at offset off_t, pads ignored), host_params (NULL or L
  * floats) receives the updated parameters at the same offsets.  At N == 1
  * the call pipelines the host->device copy, the update and the
- * device->host copy over ~32 tensor ranges on two internal copy streams
+ * device->host copy over ~8 tensor ranges on two internal copy streams
  * (joined back into `stream`), so the step costs about one PCIe transfer
  * instead of two.  If the registered params are views of one allocation in
  * the packed layout, the device->host copies are contiguous. */

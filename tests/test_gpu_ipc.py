@@ -82,6 +82,8 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode, pieces=0):
             g = [torch.from_numpy(x).cuda() for x in synth.grads(shapes, workers=world, step=s)[rank]]
             if mode == "skip" and rank == 1 and s == 1:
                 continue                              # fault injection: rank 1 skips a collective
+            if mode == "reregister" and s == 1:
+                comm.register_params(w)               # collective; resets momentum (reading R7)
             if mode == "sharded":
                 comm.step_sharded(g, dtype, 0.1, 0.9)  # RS -> own-chunk update -> param all-gather
             elif pieces:
@@ -189,6 +191,23 @@ def test_ipc_cuda_graph_replay(orc, world, dtype, mode, pieces):
 def test_ipc_single_call_schedule_refuses_capture():
     res = _run(2, "fp32", "oneshot", mode="capture_unpipelined")
     assert all(r[1] == "error" and r[2] == "CMN_ERR_UNSUPPORTED" for r in res), res
+
+
+def test_ipc_reregistration(orc):
+    """Re-registration between steps (structure may change
+    per iteration) is a collective that drains peers before freeing the
+    IPC-exported buffers; momentum restarts from zero."""
+    res = _run(2, "fp32", "twoshot", mode="reregister")
+    assert all(r[1] == "ok" for r in res), res
+    shapes = synth.mlp_shapes()
+    w = synth.params(shapes)
+    v = [np.zeros_like(x) for x in w]
+    orc.step(synth.grads(shapes, workers=2, step=0), w, v, 0.1, 0.9, "fp32")
+    v = [np.zeros_like(x) for x in w]
+    orc.step(synth.grads(shapes, workers=2, step=1), w, v, 0.1, 0.9, "fp32")
+    for r in res:
+        assert np.array_equal(np.frombuffer(r[2], np.uint32), np.concatenate(w).view(np.uint32))
+        assert np.array_equal(np.frombuffer(r[3], np.uint32), np.concatenate(v).view(np.uint32))
 
 
 def test_ipc_skipped_collective_times_out():
