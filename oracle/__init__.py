@@ -8,8 +8,8 @@ imports the product package.
 Each function names the step of SURVEY.md §8(c) c.1 (restated in
 cmn_oracle.c's header and DESIGN.md §3) it implements.  All pins live in
 tests/test_oracle_*.py; every function below is pinned (none is
-"parity unpinned") except `update_adam`'s multi-step trajectory, which is
-pinned only on its step-1 closed form and the SPEC.md:463 example.
+"parity unpinned"); `update_adam` by the SPEC.md:463 example, its step-1
+closed form and the constant-gradient multi-step closed form.
 """
 from __future__ import annotations
 

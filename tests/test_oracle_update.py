@@ -163,3 +163,28 @@ def test_adam_spec_example_and_step1_closed_form(orc):
     dw = 1.0 - w[0].astype(np.float64)
     want = 1e-3 * g64 / (np.abs(g64) + 1e-8 / np.sqrt(c2))
     assert np.allclose(dw, want, rtol=2e-3, atol=1e-7)
+
+
+@pytest.mark.parametrize("steps", [1, 3, 10])
+def test_adam_constant_gradient_trajectory_closed_form(orc, steps):
+    """Multi-step pin of the Adam oracle (bias correction, step index): with a
+    constant gradient g, m_t = (1-b1^t) g and v_t = (1-b2^t) g^2 exactly in
+    real arithmetic, so each step moves w by alpha*g / (|g| + eps/sqrt(1-b2^t)).
+    The fp64 sum of those steps must match the fp32 oracle to ~1e-5 relative
+    (a wrong power, an off-by-one step index or a missing correction fails)."""
+    rng = np.random.default_rng(21)
+    g = (rng.standard_normal(400) * 10.0 ** rng.integers(-4, 0, 400)).astype(np.float32)
+    off, L = orc.layout([400])
+    w = [np.zeros(400, np.float32)]
+    m = [np.zeros(400, np.float32)]
+    v = [np.zeros(400, np.float32)]
+    a, b1, b2, eps = 1e-3, 0.9, 0.999, 1e-8
+    for t in range(1, steps + 1):
+        orc.update_adam(g, "fp32", 1, a, b1, b2, eps, t, off, w, m, v)
+    g64 = g.astype(np.float64)
+    b2f = float(np.float32(b2))
+    want = -sum(a * g64 / (np.abs(g64) + eps / np.sqrt(1.0 - b2f ** t)) for t in range(1, steps + 1))
+    assert np.allclose(w[0], want, rtol=2e-5 * steps, atol=1e-9)
+    b1f = float(np.float32(b1))
+    assert np.allclose(m[0], (1 - b1f ** steps) * g64, rtol=1e-5, atol=0)
+    assert np.allclose(v[0], (1 - b2f ** steps) * g64 * g64, rtol=1e-4, atol=0)
