@@ -289,6 +289,14 @@ cmn_status cmn_set_algo(cmn_comm *comm, cmn_algo algo, size_t oneshot_max_bytes)
  * Default 4 (env CMN_PIECES).  Every rank must use the same value. */
 cmn_status cmn_set_pipeline(cmn_comm *comm, int pieces);
 
+/* cmn_set_fused_update -- N > 1 cmn_step schedule (takes precedence over
+ * the pipeline when on): pack -> reduce-scatter -> ONE kernel that updates
+ * every parameter reading each reduced chunk directly from its owner rank
+ * over NVLink (no all-gather copy through local HBM).  Bitwise identical to
+ * the other schedules; graph-capturable.  Every rank must use the same
+ * setting.  Default off. */
+cmn_status cmn_set_fused_update(cmn_comm *comm, int on);
+
 /* cmn_set_timeout -- device spin-wait timeout in milliseconds (default
  * 30000). */
 cmn_status cmn_set_timeout(cmn_comm *comm, uint32_t timeout_ms);

@@ -48,6 +48,7 @@ SIGNATURES = [
     ("cmn_update_bucket", C.c_int, [_P, C.c_int, C.c_float, C.c_float, _P]),
     ("cmn_set_algo", C.c_int, [_P, C.c_int, C.c_size_t]),
     ("cmn_set_pipeline", C.c_int, [_P, C.c_int]),
+    ("cmn_set_fused_update", C.c_int, [_P, C.c_int]),
     ("cmn_set_timeout", C.c_int, [_P, C.c_uint32]),
     ("cmn_get_momentum", C.c_int, [_P, C.c_int, _PP]),
     ("cmn_get_adam_state", C.c_int, [_P, C.c_int, _PP, _PP]),
@@ -329,6 +330,9 @@ class Comm:
     def set_algo(self, algo, oneshot_max_bytes: int = 0):
         a = _ALGOS[algo] if isinstance(algo, str) else int(algo)
         _check(lib().cmn_set_algo(self._h, a, oneshot_max_bytes), "cmn_set_algo")
+
+    def set_fused_update(self, on: bool):
+        _check(lib().cmn_set_fused_update(self._h, int(bool(on))), "cmn_set_fused_update")
 
     def set_pipeline(self, pieces: int):
         _check(lib().cmn_set_pipeline(self._h, pieces), "cmn_set_pipeline")

@@ -72,6 +72,14 @@ __device__ __forceinline__ uint4 ld_peer_u4(const void *p) {
                  : "memory");
     return r;
 }
+__device__ __forceinline__ uint2 ld_peer_u2(const void *p) {
+    uint2 r;
+    asm volatile("ld.global.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+                 : "=r"(r.x), "=r"(r.y)
+                 : "l"(p)
+                 : "memory");
+    return r;
+}
 __device__ __forceinline__ void st_u4(void *p, const uint4 &v) {
     asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
                  "r"(v.w)

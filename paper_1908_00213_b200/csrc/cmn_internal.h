@@ -126,6 +126,12 @@ cudaError_t launch_gather_params(const TensorDesc *td, const Item *items, int i0
                                  int s1, const PeerBufs &exch, int world, const Barrier &bar,
                                  int blocks, cudaStream_t s);
 
+// Fused all-gather + update: start barrier, then momentum SGD over the
+// chunk-clipped items [i0, i1) reading r from red.p[Item.reserved].
+cudaError_t launch_update_gather(const TensorDesc *td, const Item *items, int i0, int i1,
+                                 const PeerBufs &red, int world, int dtype, float inv_n, float lr,
+                                 float mu, const Barrier &bar, int blocks, cudaStream_t s);
+
 int num_sms(int device);
 
 }  // namespace cmn

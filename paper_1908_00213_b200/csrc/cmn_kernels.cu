@@ -510,6 +510,64 @@ __global__ void __launch_bounds__(kThreads) k_gather_params(const TensorDesc *__
     }
 }
 
+// Fused all-gather + update (two-shot variant): after the reduce-scatter,
+// every rank updates ALL of its parameters reading each reduced chunk
+// straight from its owner's reduced buffer over NVLink (no local all-gather
+// copy: saves writing and re-reading (N-1)/N of the reduced buffer in HBM).
+// Start barrier: every peer has arrived, so its reduce-scatter completed.
+// Grid-stride over the chunk-clipped items (Item.reserved = owner).
+template <int DT>
+__global__ void __launch_bounds__(kThreads) k_update_gather(const TensorDesc *__restrict__ td,
+                                                            const Item *__restrict__ items, int i0,
+                                                            int i1,
+                                                            const __grid_constant__ PeerBufs red,
+                                                            int world, float inv_n, float lr,
+                                                            float mu,
+                                                            const __grid_constant__ Barrier bar) {
+    const uint32_t bv = barrier_value(bar);
+    cross_rank_barrier(bar, bv, world, 0);
+    for (int i = i0 + blockIdx.x; i < i1; i += gridDim.x) {
+        const Item it = items[i];
+        const TensorDesc d = td[it.t];
+        float *__restrict__ w = d.w + it.k0;
+        float *__restrict__ m = d.mom + it.k0;
+        const void *src = red.p[it.reserved];
+        const int nv = it.len >> 2;
+        float4 r[kVecPerThread], wv[kVecPerThread], mv[kVecPerThread];
+#pragma unroll
+        for (int u = 0; u < kVecPerThread; ++u) {
+            const int v = threadIdx.x + u * kThreads;
+            if (v < nv) {
+                if constexpr (DT == 0) {
+                    const uint4 q = ld_peer_u4(static_cast<const float *>(src) + it.base + 4 * v);
+                    r[u] = make_float4(__uint_as_float(q.x), __uint_as_float(q.y),
+                                       __uint_as_float(q.z), __uint_as_float(q.w));
+                } else {
+                    const uint2 h = ld_peer_u2(static_cast<const uint16_t *>(src) + it.base + 4 * v);
+                    r[u] = make_float4(half_lo(h.x), half_hi(h.x), half_lo(h.y), half_hi(h.y));
+                }
+                wv[u] = ld_cs_f4(w + 4 * v);
+                mv[u] = ld_cs_f4(m + 4 * v);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kVecPerThread; ++u) {
+            const int v = threadIdx.x + u * kThreads;
+            if (v < nv) {
+                sgd_vec(r[u], inv_n, lr, mu, wv[u], mv[u]);
+                st_cs_f4(w + 4 * v, wv[u]);
+                st_cs_f4(m + 4 * v, mv[u]);
+            }
+        }
+        for (int k = (nv << 2) + threadIdx.x; k < it.len; k += kThreads) {
+            float wk = w[k], mk = m[k];
+            sgd_elem(load_r1<DT>(src, it.base + k), inv_n, lr, mu, wk, mk);
+            w[k] = wk;
+            m[k] = mk;
+        }
+    }
+}
+
 inline int grid_of(int i0, int i1) { return i1 > i0 ? i1 - i0 : 0; }
 
 }  // namespace
@@ -678,6 +736,20 @@ cudaError_t launch_gather_params(const TensorDesc *td, const Item *items, int i0
     if (blocks <= 0 || blocks > kMaxBarrierBlocks) return cudaErrorInvalidValue;
     (void)cudaGetLastError();
     k_gather_params<<<blocks, kThreads, 0, s>>>(td, items, i0, i1, s0, s1, exch, world, bar);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_update_gather(const TensorDesc *td, const Item *items, int i0, int i1,
+                                 const PeerBufs &red, int world, int dtype, float inv_n, float lr,
+                                 float mu, const Barrier &bar, int blocks, cudaStream_t s) {
+    if (blocks <= 0 || blocks > kMaxBarrierBlocks) return cudaErrorInvalidValue;
+    (void)cudaGetLastError();
+    if (dtype == 0)
+        k_update_gather<0><<<blocks, kThreads, 0, s>>>(td, items, i0, i1, red, world, inv_n, lr, mu,
+                                                       bar);
+    else
+        k_update_gather<1><<<blocks, kThreads, 0, s>>>(td, items, i0, i1, red, world, inv_n, lr, mu,
+                                                       bar);
     return cudaGetLastError();
 }
 

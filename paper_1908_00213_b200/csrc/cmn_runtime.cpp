@@ -162,6 +162,7 @@ struct cmn_comm {
     // pipelined N > 1 step: pack(p+1) and update(p-1) on the caller's stream
     // overlap all-reduce(p) on a high-priority communication stream.
     int pipe_pieces = 4;
+    bool fused_update = false;    // N > 1 cmn_step: RS + fused all-gather/update
     // NEXT-4 sharded update: items clipped to every rank's two-shot chunk
     // (Item.reserved = owner), rank r's list is [sitem_begin[r], sitem_begin[r+1]).
     std::vector<int> sitem_begin;
@@ -804,6 +805,50 @@ cmn_status step_sharded(cmn_comm *c, const float *const *grads, int dtype, float
     return CMN_OK;
 }
 
+// Fused two-shot step: pack -> reduce-scatter (start barrier) -> fused
+// all-gather + update reading every reduced chunk from its owner (start
+// barrier).  Every buffer overwrite is behind a start barrier (as in the
+// sharded step), so the schedule is graph-safe.
+cmn_status step_fused(cmn_comm *c, const float *const *grads, int dtype, float lr, float mu,
+                      cudaStream_t s) {
+    cmn_algo algo = CMN_ALGO_AUTO;
+    if (cmn_status st = begin_collective(c, 0, c->T, dtype, algo, s, true); st != CMN_OK) return st;
+    const int nsim = c->simulated ? c->world : 1;
+    const uint32_t seq1 = ++c->seq;
+    const int par = static_cast<int>(seq1 & 1u);
+    if (cmn_status st = pack_phase(c, 0, c->T, grads, dtype, par, s); st != CMN_OK) return st;
+    PeerBufs in{}, red{};
+    for (int r = 0; r < c->world; ++r) {
+        in.p[r] = c->rb[r].packed[par];
+        red.p[r] = c->rb[r].reduced[0];
+    }
+    int64_t cs[kMaxWorld], ce[kMaxWorld];
+    chunk_plan(0, c->L, c->world, cs, ce);
+    const int blocks = ar_blocks_for(c);
+    const Barrier bar = make_barrier(c, dtype | 2);
+    for (int i = 0; i < nsim; ++i) {
+        const int r = c->simulated ? i : c->rank;
+        cmn_status st = launched(c,
+                                 launch_allreduce_twoshot(in, red, c->world, r, cs, ce, dtype, 1, bar,
+                                                          blocks, s),
+                                 "reduce_scatter");
+        if (st != CMN_OK) return st;
+    }
+    ++c->seq;
+    const Barrier bar2 = make_barrier(c, dtype);
+    const int total = c->sitem_begin[c->world];
+    const int gblocks = total < blocks ? (total > 0 ? total : 1) : blocks;
+    // simulated ranks share one parameter replica: one launch updates it all
+    cmn_status st = launched(c,
+                             launch_update_gather(c->d_td, c->d_sitems, 0, total, red, c->world, dtype,
+                                                  1.0f / static_cast<float>(c->world), lr, mu, bar2,
+                                                  gblocks, s),
+                             "update_gather");
+    if (st != CMN_OK) return st;
+    c->fresh = false;
+    return CMN_OK;
+}
+
 }  // namespace
 
 // =====================================================================
@@ -989,6 +1034,13 @@ cmn_status cmn_step(cmn_comm *c, const float *const *grads, cmn_dtype dtype, flo
     if (cmn_status st = require_registered(c); st != CMN_OK) return st;
     if (cmn_status st = require_dtype(dtype); st != CMN_OK) return st;
     if (c->world > 1) {
+        if (c->fused_update) {
+            std::string why;
+            if (!grads_ok(c, grads, c->T * (c->simulated ? c->world : 1), why))
+                return fail(CMN_ERR_INVALID_ARG, why);
+            if (cmn_status st = set_device(c); st != CMN_OK) return st;
+            return step_fused(c, grads, dtype, lr, mu, static_cast<cudaStream_t>(stream));
+        }
         if (c->pipe_pieces >= 2 && c->T >= 2) {
             std::string why;
             if (!grads_ok(c, grads, c->T * (c->simulated ? c->world : 1), why))
@@ -1286,6 +1338,12 @@ cmn_status cmn_set_algo(cmn_comm *c, cmn_algo algo, size_t oneshot_max_bytes) {
         c->nccl = comm;
     }
     c->algo = algo;
+    return CMN_OK;
+}
+
+cmn_status cmn_set_fused_update(cmn_comm *c, int on) {
+    if (!c) return fail(CMN_ERR_INVALID_ARG, "comm is NULL");
+    c->fused_update = on != 0;
     return CMN_OK;
 }
 

@@ -48,6 +48,7 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode, pieces=0):
             return
         comm.set_algo(algo)
         comm.set_pipeline(pieces)
+        comm.set_fused_update(mode in ("fused", "graph_fused"))
         if mode == "capture_unpipelined":
             g0 = [torch.from_numpy(x).cuda() for x in synth.grads(shapes, workers=world)[rank]]
             comm.allreduce_grads(g0, dtype)          # eager warm-up is fine
@@ -62,7 +63,7 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode, pieces=0):
                 q.put((rank, "error", e.status_name))
             dist.barrier()
             return
-        if mode in ("graph", "graph_sharded"):
+        if mode in ("graph", "graph_sharded", "graph_fused"):
             # step 0 eagerly (creates internal streams), then capture ONE step
             # into a CUDA graph and replay it for steps 1.. with fresh grads
             # copied into the captured buffers.
@@ -86,6 +87,8 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode, pieces=0):
                 comm.register_params(w)               # collective; resets momentum (reading R7)
             if mode == "sharded":
                 comm.step_sharded(g, dtype, 0.1, 0.9)  # RS -> own-chunk update -> param all-gather
+            elif mode == "fused":
+                comm.step(g, dtype, 0.1, 0.9)         # RS -> fused all-gather + update
             elif pieces:
                 comm.step(g, dtype, 0.1, 0.9)         # pipelined schedule, 2 streams
             else:
@@ -171,7 +174,8 @@ def test_ipc_sharded_update(orc, world, dtype):
 
 
 @pytest.mark.parametrize("world,dtype,mode,pieces", [(2, "fp32", "graph", 2), (3, "fp16", "graph", 4),
-                                                    (2, "fp32", "graph_sharded", 0)])
+                                                    (2, "fp32", "graph_sharded", 0),
+                                                    (3, "fp32", "graph_fused", 0)])
 def test_ipc_cuda_graph_replay(orc, world, dtype, mode, pieces):
     """A captured CUDA graph of one multi-process step, replayed for steps
     1..3: device-resident barrier epochs advance on every replay, results
@@ -191,6 +195,20 @@ def test_ipc_cuda_graph_replay(orc, world, dtype, mode, pieces):
 def test_ipc_single_call_schedule_refuses_capture():
     res = _run(2, "fp32", "oneshot", mode="capture_unpipelined")
     assert all(r[1] == "error" and r[2] == "CMN_ERR_UNSUPPORTED" for r in res), res
+
+
+@pytest.mark.parametrize("world,dtype", [(2, "fp16"), (3, "fp32")])
+def test_ipc_fused_allgather_update(orc, world, dtype):
+    res = _run(world, dtype, "twoshot", mode="fused")
+    assert all(r[1] == "ok" for r in res), res
+    shapes = synth.mlp_shapes()
+    w = synth.params(shapes)
+    v = [np.zeros_like(x) for x in w]
+    for s in range(2):
+        orc.step(synth.grads(shapes, workers=world, step=s), w, v, 0.1, 0.9, dtype)
+    for r in res:
+        assert np.array_equal(np.frombuffer(r[2], np.uint32), np.concatenate(w).view(np.uint32))
+        assert np.array_equal(np.frombuffer(r[3], np.uint32), np.concatenate(v).view(np.uint32))
 
 
 def test_ipc_reregistration(orc):

@@ -269,6 +269,29 @@ def test_pipelined_step_parity(cmn, orc, N, pieces, dtype):
         comm.finalize()
 
 
+@pytest.mark.parametrize("N,dtype", [(2, "fp32"), (3, "fp16"), (4, "fp16"), (8, "fp32")])
+def test_fused_allgather_update_parity(cmn, orc, N, dtype):
+    """Fused two-shot step (reduce-scatter, then one kernel updating every
+    parameter from the owners' reduced chunks) == oracle bitwise, 3 steps."""
+    shapes = synth.resnet50_shapes()[:30] + RAGGED
+    grads = [synth.grads(shapes, workers=N, step=s) for s in range(3)]
+    params0 = synth.params(shapes)
+    ora, _, _ = run_oracle(orc, shapes, N, dtype, grads, params0, 0.1, 0.9)
+    comm = cmn.Comm.simulated_world(N)
+    try:
+        w = to_dev(params0)
+        comm.register_params(w)
+        comm.set_fused_update(True)
+        for s, g in enumerate(grads):
+            comm.step([to_dev(gw) for gw in g], dtype, 0.1, 0.9)
+            torch.cuda.synchronize()
+            for t in range(len(w)):
+                assert_bitwise(w[t].cpu().numpy().reshape(-1), ora[s]["w"][t], f"w[{t}] step {s}")
+                assert_bitwise(comm.momentum(t).cpu().numpy().reshape(-1), ora[s]["v"][t], f"v[{t}]")
+    finally:
+        comm.finalize()
+
+
 @pytest.mark.parametrize("N,dtype", [(2, "fp32"), (3, "fp16"), (4, "fp32"), (8, "fp16"), (8, "fp32")])
 def test_sharded_update_parity(cmn, orc, N, dtype):
     """NEXT-4 (cmn_step_sharded): reduce-scatter, update of the own chunk,
@@ -473,7 +496,7 @@ def test_edge_layouts_all_schedules(cmn, orc, shapes_name, N):
     params0 = synth.params(shapes, seed=11)
     for dtype in ("fp32", "fp16"):
         ora, _, _ = run_oracle(orc, shapes, N, dtype, grads, params0, 0.1, 0.9)
-        for sched in ("oneshot", "twoshot", "pipelined", "sharded"):
+        for sched in ("oneshot", "twoshot", "pipelined", "sharded", "fused"):
             comm = cmn.Comm.simulated_world(N) if N > 1 else cmn.Comm.init(0, 1, 0)
             try:
                 w = to_dev(params0)
@@ -487,6 +510,9 @@ def test_edge_layouts_all_schedules(cmn, orc, shapes_name, N):
                         comm.update_momentum_sgd(0.1, 0.9)
                     elif sched == "pipelined":
                         comm.set_pipeline(3)
+                        comm.step(gd, dtype, 0.1, 0.9)
+                    elif sched == "fused":
+                        comm.set_fused_update(True)
                         comm.step(gd, dtype, 0.1, 0.9)
                     else:
                         comm.step_sharded(gd, dtype, 0.1, 0.9)
