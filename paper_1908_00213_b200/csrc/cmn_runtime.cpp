@@ -891,9 +891,25 @@ cmn_status cmn_finalize(cmn_comm *c) {
     return CMN_OK;
 }
 
+static cmn_status register_impl(cmn_comm *c, int T, const int *ndims, const int64_t *dims,
+                                float *const *params);
+
 cmn_status cmn_register_params(cmn_comm *c, int T, const int *ndims, const int64_t *dims,
                                float *const *params) {
     if (!c) return fail(CMN_ERR_INVALID_ARG, "comm is NULL");
+    const cmn_status st = register_impl(c, T, ndims, dims, params);
+    // A failed (re-)registration leaves the communicator unregistered (every
+    // later call returns CMN_ERR_STATE), never half-mapped.
+    if (st != CMN_OK && st != CMN_ERR_INVALID_ARG && c->T > 0) {
+        const std::string msg = g_last_error;
+        free_registration(c);
+        g_last_error = msg;
+    }
+    return st;
+}
+
+static cmn_status register_impl(cmn_comm *c, int T, const int *ndims, const int64_t *dims,
+                                float *const *params) {
     try {
         std::vector<int64_t> numel, off;
         uint64_t hash = 0;
