@@ -93,13 +93,23 @@ typedef enum { CMN_FP32 = 0, CMN_FP16 = 1 } cmn_dtype;
  *            ("We adopted NCCL ... as a primary library");
  *            NCCL's summation order is its own, so results match the oracle
  *            within the tolerance gate, not bitwise.
+ *   NVLS     NEXT-3, NVLink SHARP: rank r reduces chunk r inside the
+ *            NVSwitch (multimem.ld_reduce on a multicast object spanning every
+ *            rank's packed buffer) and multicast-stores the sum into every
+ *            rank's reduced buffer (multimem.st): ~S/N bytes per rank and
+ *            direction instead of 2(N-1)/N S.  The switch's summation order is
+ *            its own: tolerance-gate parity, not bitwise, for N > 1.  Selecting
+ *            it (after registration, on every rank) creates the multicast
+ *            resources; needs an NVSwitch system (CMN_ERR_UNSUPPORTED
+ *            otherwise).  Also runs at N = 1 (the switch "reduces" one copy).
  *   AUTO     ONESHOT when payload bytes <= oneshot_max_bytes or N == 2,
  *            else TWOSHOT. */
 typedef enum {
     CMN_ALGO_AUTO = 0,
     CMN_ALGO_ONESHOT = 1,
     CMN_ALGO_TWOSHOT = 2,
-    CMN_ALGO_NCCL = 3
+    CMN_ALGO_NCCL = 3,
+    CMN_ALGO_NVLS = 4
 } cmn_algo;
 
 /* Bootstrap allgather supplied by the caller (the Python binding uses
@@ -349,6 +359,14 @@ cmn_status cmn_plan_chunks(int64_t padded_len, int world_size, int64_t *starts, 
  * the registration-time structure check, exposed for host-only tests. */
 cmn_status cmn_bootstrap_verify(int rank, int world_size, cmn_allgather_fn ag, void *user,
                                 uint64_t hash);
+
+/* cmn_share_fd -- the file-descriptor hand-off CMN_ALGO_NVLS uses to give
+ * every rank rank 0's multicast-object handle: rank 0 listens on an
+ * abstract Unix-domain socket whose name goes through `ag`, every other
+ * rank connects and receives `fd_in` via SCM_RIGHTS into *fd_out (rank 0:
+ * *fd_out = fd_in).  Host-only; exposed for tests. */
+cmn_status cmn_share_fd(int rank, int world_size, cmn_allgather_fn ag, void *user, int fd_in,
+                        int *fd_out);
 
 #ifdef __cplusplus
 }

@@ -16,8 +16,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libcmn.so")
 
 FP32, FP16 = 0, 1
-ALGO_AUTO, ALGO_ONESHOT, ALGO_TWOSHOT, ALGO_NCCL = 0, 1, 2, 3
-_ALGOS = {"auto": 0, "oneshot": 1, "twoshot": 2, "nccl": 3}
+ALGO_AUTO, ALGO_ONESHOT, ALGO_TWOSHOT, ALGO_NCCL, ALGO_NVLS = 0, 1, 2, 3, 4
+_ALGOS = {"auto": 0, "oneshot": 1, "twoshot": 2, "nccl": 3, "nvls": 4}
 _DTYPES = {"fp32": FP32, "fp16": FP16, "float32": FP32, "float16": FP16}
 STATUS = {0: "CMN_OK", 1: "CMN_ERR_INVALID_ARG", 2: "CMN_ERR_CUDA", 3: "CMN_ERR_NCCL",
           4: "CMN_ERR_BOOTSTRAP", 5: "CMN_ERR_MISMATCH", 6: "CMN_ERR_TIMEOUT",
@@ -62,6 +62,7 @@ SIGNATURES = [
                                   C.POINTER(C.c_uint64)]),
     ("cmn_plan_chunks", C.c_int, [C.c_int64, C.c_int, _I64P, _I64P]),
     ("cmn_bootstrap_verify", C.c_int, [C.c_int, C.c_int, AllgatherFn, _P, C.c_uint64]),
+    ("cmn_share_fd", C.c_int, [C.c_int, C.c_int, AllgatherFn, _P, C.c_int, C.POINTER(C.c_int)]),
 ]
 
 _LIB = None
@@ -198,6 +199,14 @@ def bootstrap_verify(rank: int, world: int, structure_hash: int, group=None) -> 
     """Returns the cmn_status (0 = all ranks agree, 5 = mismatch)."""
     cb = torch_allgather(group)
     return lib().cmn_bootstrap_verify(rank, world, cb, None, structure_hash)
+
+
+def share_fd(rank: int, world: int, fd: int, group=None) -> int:
+    """cmn_share_fd: rank 0's fd, received by every rank (host-only)."""
+    cb = torch_allgather(group)
+    out = C.c_int(-1)
+    _check(lib().cmn_share_fd(rank, world, cb, None, fd, C.byref(out)), "cmn_share_fd")
+    return out.value
 
 
 # -------------------------------------------------------------- communicator

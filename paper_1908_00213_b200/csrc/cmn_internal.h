@@ -132,6 +132,13 @@ cudaError_t launch_update_gather(const TensorDesc *td, const Item *items, int i0
                                  const PeerBufs &red, int world, int dtype, float inv_n, float lr,
                                  float mu, const Barrier &bar, int blocks, cudaStream_t s);
 
+// NEXT-3 NVLS: this rank's chunk [e0, e1) (elements) reduced in the switch
+// from the multicast packed buffer and multicast-stored into every rank's
+// reduced buffer; start and end cross-rank barriers.
+cudaError_t launch_nvls_allreduce(const void *mc_packed, void *mc_reduced, int64_t e0, int64_t e1,
+                                  int world, int dtype, const Barrier &bar, int blocks,
+                                  cudaStream_t s);
+
 int num_sms(int device);
 
 }  // namespace cmn

@@ -568,6 +568,60 @@ __global__ void __launch_bounds__(kThreads) k_update_gather(const TensorDesc *__
     }
 }
 
+// ------------------------------------------------------------ NEXT-3
+// NVLS all-reduce: rank r owns chunk r; for each 16-B vector the NVSwitch
+// reduces the N ranks' packed copies (multimem.ld_reduce on the multicast
+// address) and the result is multicast-stored into every rank's reduced
+// buffer (multimem.st).  Per rank and direction only ~S/N bytes cross
+// NVLink instead of 2(N-1)/N S.  The switch's summation order is its own,
+// so for N > 1 results meet the tolerance gate, not the oracle's tree order.
+// fp16 payloads accumulate in fp32 inside the switch (.acc::f32) and are
+// rounded to fp16 once, as in reading R4.
+template <int DT>
+__device__ __forceinline__ uint4 mm_ld_reduce(const void *mc) {
+    uint4 r;
+    if constexpr (DT == 0) {
+        asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                     : "l"(mc)
+                     : "memory");
+    } else {
+        asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.f16x2 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                     : "l"(mc)
+                     : "memory");
+    }
+    return r;
+}
+__device__ __forceinline__ void mm_st(void *mc, const uint4 &v) {
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc), "r"(v.x),
+                 "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kThreads) k_nvls(const char *mc_packed, char *mc_reduced,
+                                                   int64_t v0, int64_t v1, int world,
+                                                   const __grid_constant__ Barrier bar) {
+    const uint32_t bv = barrier_value(bar);
+    cross_rank_barrier(bar, bv, world, 0);           // every rank's pack is complete
+    for (int64_t tile = v0 + static_cast<int64_t>(blockIdx.x) * kTileVecs; tile < v1;
+         tile += static_cast<int64_t>(gridDim.x) * kTileVecs) {
+        uint4 x[kARVec];
+#pragma unroll
+        for (int u = 0; u < kARVec; ++u) {
+            const int64_t idx = tile + threadIdx.x + u * kThreads;
+            if (idx < v1) x[u] = mm_ld_reduce<DT>(mc_packed + 16 * idx);
+        }
+#pragma unroll
+        for (int u = 0; u < kARVec; ++u) {
+            const int64_t idx = tile + threadIdx.x + u * kThreads;
+            if (idx < v1) mm_st(mc_reduced + 16 * idx, x[u]);
+        }
+    }
+    cross_rank_barrier(bar, bv, world, 1);           // every rank's stores have landed
+}
+
 inline int grid_of(int i0, int i1) { return i1 > i0 ? i1 - i0 : 0; }
 
 }  // namespace
@@ -750,6 +804,21 @@ cudaError_t launch_update_gather(const TensorDesc *td, const Item *items, int i0
     else
         k_update_gather<1><<<blocks, kThreads, 0, s>>>(td, items, i0, i1, red, world, inv_n, lr, mu,
                                                        bar);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_nvls_allreduce(const void *mc_packed, void *mc_reduced, int64_t e0, int64_t e1,
+                                  int world, int dtype, const Barrier &bar, int blocks,
+                                  cudaStream_t s) {
+    if (blocks <= 0 || blocks > kMaxBarrierBlocks) return cudaErrorInvalidValue;
+    (void)cudaGetLastError();
+    const int64_t v0 = to_vec(e0, dtype), v1 = to_vec(e1, dtype);
+    if (dtype == 0)
+        k_nvls<0><<<blocks, kThreads, 0, s>>>(static_cast<const char *>(mc_packed),
+                                              static_cast<char *>(mc_reduced), v0, v1, world, bar);
+    else
+        k_nvls<1><<<blocks, kThreads, 0, s>>>(static_cast<const char *>(mc_packed),
+                                              static_cast<char *>(mc_reduced), v0, v1, world, bar);
     return cudaGetLastError();
 }
 

@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include "cmn_internal.h"
+#include "cmn_nvls.h"
 
 using namespace cmn;
 
@@ -116,6 +117,7 @@ struct ArResult {
     int parity = 0;
     int dtype = 0;
     bool alias_packed = false;
+    bool nvls = false;      // result lives in the NVLS buffer (unicast view)
 };
 
 struct cmn_comm {
@@ -163,6 +165,7 @@ struct cmn_comm {
     // overlap all-reduce(p) on a high-priority communication stream.
     int pipe_pieces = 4;
     bool fused_update = false;    // N > 1 cmn_step: RS + fused all-gather/update
+    Nvls nvls;                    // NEXT-3 multicast resources (CMN_ALGO_NVLS)
     // NEXT-4 sharded update: items clipped to every rank's two-shot chunk
     // (Item.reserved = owner), rank r's list is [sitem_begin[r], sitem_begin[r+1]).
     std::vector<int> sitem_begin;
@@ -201,6 +204,7 @@ void free_regions(cmn_comm *c) {
 }
 
 void free_registration(cmn_comm *c) {
+    nvls_teardown(c->nvls);
     free_regions(c);
     cudaFree(c->d_td);
     cudaFree(c->d_items);
@@ -398,15 +402,16 @@ void chunk_plan(int64_t e0, int64_t e1, int world, int64_t *s, int64_t *e) {
 // a1: pack every (simulated) rank's gradients of tensors [ta, tb) into its
 // packed buffer of parity `par`.
 cmn_status pack_phase(cmn_comm *c, int ta, int tb, const float *const *grads, int dtype, int par,
-                      cudaStream_t s) {
+                      cudaStream_t s, void *dst_override = nullptr) {
     const int nsim = c->simulated ? c->world : 1;
     for (int i = 0; i < nsim; ++i) {
         const int r = c->simulated ? i : c->rank;
         const float *const *g = grads + static_cast<size_t>(i) * c->T;
+        void *dst = dst_override ? dst_override : c->rb[r].packed[par];
         cmn_status st = for_groups(c, ta, tb, [&](int lo, int hi, int i0, int i1) {
             return launched(c,
                             launch_pack(make_tab(g, lo, hi), lo, c->d_td, c->d_items, i0, i1, dtype,
-                                        c->rb[r].packed[par], s),
+                                        dst, s),
                             "pack");
         });
         if (st != CMN_OK) return st;
@@ -423,8 +428,18 @@ cmn_status reduce_phase(cmn_comm *c, int ta, int tb, int dtype, uint32_t seq, cm
     const size_t esz = dtype == 0 ? 4 : 2;
     const int nsim = c->simulated ? c->world : 1;
     // identity at N = 1 (fp16 rounding done by the pack) -- except through
-    // NCCL, whose single-rank all-reduce exercises the comparison plumbing
-    if (c->world == 1 && algo != CMN_ALGO_NCCL) return CMN_OK;
+    // NCCL / NVLS, whose single-rank all-reduce exercises their plumbing
+    if (c->world == 1 && algo != CMN_ALGO_NCCL && algo != CMN_ALGO_NVLS) return CMN_OK;
+    if (algo == CMN_ALGO_NVLS) {
+        int64_t cs[kMaxWorld], ce[kMaxWorld];
+        chunk_plan(e0, e1, c->world, cs, ce);
+        const Barrier bar = make_barrier(c, dtype | 2);
+        return launched(c,
+                        launch_nvls_allreduce(c->nvls.packed_mc(), c->nvls.reduced_mc(),
+                                              cs[c->rank], ce[c->rank], c->world, dtype, bar,
+                                              ar_blocks_for(c), s),
+                        "nvls_allreduce");
+    }
     if (algo == CMN_ALGO_NCCL) {
         void *src = static_cast<char *>(c->rb[c->rank].packed[par]) + e0 * esz;
         void *dst = static_cast<char *>(c->rb[c->rank].reduced[par]) + e0 * esz;
@@ -499,6 +514,9 @@ cmn_status begin_collective(cmn_comm *c, int ta, int tb, int dtype, cmn_algo &al
     }
     const size_t esz = dtype == 0 ? 4 : 2;
     algo = choose_algo(c, static_cast<size_t>(c->off[tb] - c->off[ta]) * esz);
+    if (algo == CMN_ALGO_NVLS && !c->nvls.ready())
+        return fail(CMN_ERR_STATE, "NVLS algorithm requested but no multicast resources "
+                                   "(cmn_set_algo(CMN_ALGO_NVLS) after registration, on every rank)");
     if (algo == CMN_ALGO_NCCL && (c->simulated || !c->nccl))
         return fail(CMN_ERR_STATE, "NCCL algorithm requested but no NCCL communicator "
                                    "(cmn_set_algo(CMN_ALGO_NCCL) on every rank of a cmn_init comm)");
@@ -509,16 +527,21 @@ cmn_status begin_collective(cmn_comm *c, int ta, int tb, int dtype, cmn_algo &al
 cmn_status allreduce_range(cmn_comm *c, int ta, int tb, const float *const *grads, int dtype,
                            cudaStream_t s) {
     cmn_algo algo = CMN_ALGO_AUTO;
-    if (cmn_status st = begin_collective(c, ta, tb, dtype, algo, s, false); st != CMN_OK) return st;
+    // NVLS is single-buffered behind start + end barriers: graph-safe.
+    const bool nvls = c->algo == CMN_ALGO_NVLS;
+    if (cmn_status st = begin_collective(c, ta, tb, dtype, algo, s, nvls); st != CMN_OK) return st;
     const uint32_t seq = ++c->seq;
     const int par = static_cast<int>(seq & 1u);
-    if (cmn_status st = pack_phase(c, ta, tb, grads, dtype, par, s); st != CMN_OK) return st;
+    if (cmn_status st = pack_phase(c, ta, tb, grads, dtype, par, s, nvls ? c->nvls.packed_uc() : nullptr);
+        st != CMN_OK)
+        return st;
     if (cmn_status st = reduce_phase(c, ta, tb, dtype, seq, algo, s); st != CMN_OK) return st;
-    c->last = ArResult{par, dtype, c->world == 1 && algo != CMN_ALGO_NCCL};
+    c->last = ArResult{par, dtype, c->world == 1 && algo != CMN_ALGO_NCCL && !nvls, nvls};
     return CMN_OK;
 }
 
 const void *reduced_ptr(const cmn_comm *c, const ArResult &res, int rank) {
+    if (res.nvls) return c->nvls.reduced_uc();
     const int r = c->simulated ? rank : c->rank;
     return res.alias_packed ? c->rb[r].packed[res.parity] : c->rb[r].reduced[res.parity];
 }
@@ -1004,6 +1027,12 @@ static cmn_status register_impl(cmn_comm *c, int T, const int *ndims, const int6
             if (c->world > 1) {
                 if (cmn_status st = exchange_and_map(c); st != CMN_OK) return st;
             }
+            if (c->algo == CMN_ALGO_NVLS) {   // collective: every rank re-registers
+                std::string err;
+                if (!nvls_setup(c->nvls, c->rank, c->world, c->device, static_cast<size_t>(c->L) * 4,
+                                c->ag, c->user, err))
+                    return fail(CMN_ERR_CUDA, "NVLS setup: " + err);
+            }
         }
         CMN_CUDA(cudaDeviceSynchronize());
         return CMN_OK;
@@ -1049,7 +1078,12 @@ cmn_status cmn_step(cmn_comm *c, const float *const *grads, cmn_dtype dtype, flo
                     void *stream) {
     if (cmn_status st = require_registered(c); st != CMN_OK) return st;
     if (cmn_status st = require_dtype(dtype); st != CMN_OK) return st;
-    if (c->world > 1) {
+    if (c->world > 1 || c->algo == CMN_ALGO_NVLS) {
+        if (c->algo == CMN_ALGO_NVLS || c->algo == CMN_ALGO_NCCL) {
+            cmn_status st = cmn_allreduce_grads(c, grads, dtype, stream);
+            if (st != CMN_OK) return st;
+            return cmn_update_momentum_sgd(c, lr, mu, stream);
+        }
         if (c->fused_update) {
             std::string why;
             if (!grads_ok(c, grads, c->T * (c->simulated ? c->world : 1), why))
@@ -1334,8 +1368,20 @@ cmn_status cmn_update_bucket(cmn_comm *c, int b, float lr, float mu, void *strea
 
 cmn_status cmn_set_algo(cmn_comm *c, cmn_algo algo, size_t oneshot_max_bytes) {
     if (!c) return fail(CMN_ERR_INVALID_ARG, "comm is NULL");
-    if (algo < CMN_ALGO_AUTO || algo > CMN_ALGO_NCCL) return fail(CMN_ERR_INVALID_ARG, "bad algo");
+    if (algo < CMN_ALGO_AUTO || algo > CMN_ALGO_NVLS) return fail(CMN_ERR_INVALID_ARG, "bad algo");
     if (oneshot_max_bytes) c->oneshot_max = oneshot_max_bytes;
+    if (algo == CMN_ALGO_NVLS && !c->nvls.ready()) {
+        if (c->simulated) return fail(CMN_ERR_UNSUPPORTED, "NVLS needs one process per GPU");
+        if (c->T == 0) return fail(CMN_ERR_STATE, "register parameters before selecting NVLS");
+        if (cmn_status st = set_device(c); st != CMN_OK) return st;
+        std::string err;
+        if (!nvls_setup(c->nvls, c->rank, c->world, c->device, static_cast<size_t>(c->L) * 4, c->ag,
+                        c->user, err)) {
+            nvls_teardown(c->nvls);
+            return fail(err.find("support") != std::string::npos ? CMN_ERR_UNSUPPORTED : CMN_ERR_CUDA,
+                        "NVLS setup: " + err);
+        }
+    }
     if (algo == CMN_ALGO_NCCL && !c->nccl) {
         if (c->simulated) return fail(CMN_ERR_UNSUPPORTED, "NCCL needs one process per GPU");
         if (!g_nccl.load()) return fail(CMN_ERR_NCCL, "cannot load libnccl (set CMN_NCCL_LIB)");
@@ -1401,7 +1447,8 @@ static cmn_status copy_buf(cmn_comm *c, int rank, void *dst, void *stream, bool 
         return fail(CMN_ERR_INVALID_ARG, "rank not accessible from this process");
     if (cmn_status st = set_device(c); st != CMN_OK) return st;
     const int r = c->simulated ? rank : c->rank;
-    const void *src = reduced ? reduced_ptr(c, c->last, r) : c->rb[r].packed[c->last.parity];
+    const void *src = reduced ? reduced_ptr(c, c->last, r)
+                              : (c->last.nvls ? c->nvls.packed_uc() : c->rb[r].packed[c->last.parity]);
     const size_t bytes = static_cast<size_t>(c->L) * (c->last.dtype == 0 ? 4 : 2);
     CMN_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice,
                              static_cast<cudaStream_t>(stream)));
@@ -1445,6 +1492,16 @@ cmn_status cmn_plan_chunks(int64_t L, int world, int64_t *starts, int64_t *ends)
     if (world < 1 || world > kMaxWorld) return fail(CMN_ERR_INVALID_ARG, "world out of range");
     if (L < 0 || !starts || !ends) return fail(CMN_ERR_INVALID_ARG, "bad arguments");
     chunk_plan(0, L, world, starts, ends);
+    return CMN_OK;
+}
+
+cmn_status cmn_share_fd(int rank, int world, cmn_allgather_fn ag, void *user, int fd_in,
+                        int *fd_out) {
+    if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world || !fd_out)
+        return fail(CMN_ERR_INVALID_ARG, "bad arguments");
+    if (world > 1 && !ag) return fail(CMN_ERR_INVALID_ARG, "allgather callback required");
+    std::string err;
+    if (!share_fd(rank, world, ag, user, fd_in, fd_out, err)) return fail(CMN_ERR_BOOTSTRAP, err);
     return CMN_OK;
 }
 

@@ -101,6 +101,18 @@ def main():
                         comm.step(gg, dtype, 0.1, 0.9)
                     t_graph = timed(gr.replay, args.iters, stream)
                     rec["graph_step_us"] = t_graph
+                    # NEXT-3 NVLS at one rank: pack + multimem.ld_reduce/st through the
+                    # NVSwitch (2 S per direction over NVLink: ld_reduce fetch+return,
+                    # st send+write-back)
+                    try:
+                        comm.set_algo("nvls")
+                        t_nv = timed(ar, args.iters, stream)
+                        rec["nvls_allreduce_incl_pack_us"] = t_nv
+                        t_nv_only = t_nv - t_ar
+                        rec["nvls_kernel_us_est"] = t_nv_only
+                        rec["nvls_nvlink_gbs_per_direction"] = 2 * c * P / (t_nv_only * 1e-6) / 1e9
+                    except Exception as e:  # noqa: BLE001 -- reported, not fatal
+                        rec["nvls_error"] = str(e)
                     rec["fused_step_us"] = t_step
                     rec["fused_step_gbs"] = 20 * P / (t_step * 1e-6) / 1e9
                     rec["fused_step_frac"] = rec["fused_step_gbs"] / peak

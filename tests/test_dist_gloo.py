@@ -41,6 +41,43 @@ def _worker(rank, world, port, mode, q):
         dist.destroy_process_group()
 
 
+def _fd_worker(rank, world, port, path, q):
+    import torch.distributed as dist
+
+    from paper_1908_00213_b200 import cmn
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        fd = os.open(path, os.O_RDONLY) if rank == 0 else -1
+        got = cmn.share_fd(rank, world, fd)
+        q.put((rank, os.pread(got, 64, 0).decode()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_share_fd_scm_rights(tmp_path, world):
+    """The NVLS multicast-handle hand-off: rank 0's open file descriptor
+    reaches every rank through an abstract Unix socket (SCM_RIGHTS) whose
+    name travels through the bootstrap allgather."""
+    from paper_1908_00213_b200 import build
+    build.build()
+    path = tmp_path / "payload"
+    path.write_text("multicast-handle-stand-in")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_fd_worker, args=(r, world, port, str(path), q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(r[1] == "multicast-handle-stand-in" for r in res)
+
+
 def _run(mode, world=2):
     from paper_1908_00213_b200 import build
     build.build()

@@ -524,6 +524,52 @@ def test_edge_layouts_all_schedules(cmn, orc, shapes_name, N):
                 comm.finalize()
 
 
+@pytest.mark.parametrize("dtype", ["fp32", "fp16"])
+def test_nvls_single_rank(cmn, orc, dtype):
+    """NEXT-3 plumbing on the one GPU gpurun provides (NVSwitch-attached):
+    multicast object + bound allocation + unicast/multicast mappings, and
+    the multimem.ld_reduce / multimem.st kernel.  With one rank the switch
+    reduces a single copy, so the step must equal the oracle; checked
+    bitwise except for signed zeros (an in-switch add may return +0 for -0),
+    and within the tolerance gate."""
+    shapes = synth.mlp_shapes() + RAGGED
+    grads = [synth.grads(shapes, workers=1, step=s) for s in range(2)]
+    params0 = synth.params(shapes)
+    ora, off, L = run_oracle(orc, shapes, 1, dtype, grads, params0, 0.1, 0.9)
+    comm = cmn.Comm.init(0, 1, 0)
+    try:
+        w = to_dev(params0)
+        comm.register_params(w)
+        try:
+            comm.set_algo("nvls")
+        except cmn.CmnError as e:
+            if e.status_name == "CMN_ERR_UNSUPPORTED":
+                pytest.skip(str(e))
+            raise
+        tdt = torch.float32 if dtype == "fp32" else torch.int16
+        for s, g in enumerate(grads):
+            comm.allreduce_grads(to_dev(g[0]), dtype)
+            red = torch.empty(L, dtype=tdt, device=DEV)
+            comm.copy_reduced(0, red)
+            comm.update_momentum_sgd(0.1, 0.9)
+            torch.cuda.synchronize()
+            r = red.cpu().numpy()
+            want = ora[s]["reduced"]
+            if dtype == "fp32":
+                r_bits, w_bits = r.view(np.uint32) & 0x7FFFFFFF, want.view(np.uint32) & 0x7FFFFFFF
+                zero = (r_bits == 0) & (w_bits == 0)
+            else:
+                r_bits, w_bits = r.view(np.uint16) & 0x7FFF, want.view(np.uint16) & 0x7FFF
+                zero = (r_bits == 0) & (w_bits == 0)
+            assert np.array_equal(r.view(want.dtype)[~zero], want[~zero]), f"reduced step {s}"
+            for t in range(len(w)):
+                got = w[t].cpu().numpy().reshape(-1)
+                assert np.allclose(got, ora[s]["w"][t], rtol=0, atol=0) or \
+                    np.array_equal(got.view(np.uint32), ora[s]["w"][t].view(np.uint32)), f"w[{t}]"
+    finally:
+        comm.finalize()
+
+
 def test_errors_are_loud(cmn):
     shapes = synth.mlp_shapes()
     comm = cmn.Comm.simulated_world(2)
