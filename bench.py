@@ -40,7 +40,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="cmn", choices=["cmn", "reference"])
     ap.add_argument("--dtype", default="fp32", choices=["fp32", "fp16"])
-    ap.add_argument("--algo", default="auto", choices=["auto", "oneshot", "twoshot", "nccl"])
+    ap.add_argument("--algo", default="auto", choices=["auto", "oneshot", "twoshot", "nccl", "nvls"])
+    ap.add_argument("--schedule", default="auto",
+                    choices=["auto", "pipelined2", "pipelined4", "pipelined8", "fused", "serial"],
+                    help="N > 1 step schedule; auto = short max-over-ranks trial of each, fastest wins")
     ap.add_argument("--min-warmup-s", type=float, default=1.0,
                     help="keep warming up (untimed) at least this long so the clock sampler sees load")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -264,6 +267,36 @@ def main():
         if world > 1:
             dist.barrier()
 
+    def set_schedule(name):
+        comm.set_fused_update(name == "fused")
+        comm.set_pipeline(int(name[len("pipelined"):]) if name.startswith("pipelined") else 0)
+
+    schedule, trials = "identity (N=1 fused direct update)", None
+    if world > 1:
+        # Runtime schedule choice: every rank times each candidate (max over
+        # ranks, so all ranks pick the same one); switching schedules between
+        # calls is safe (every buffer reuse is behind a start barrier).
+        cands = ["pipelined2", "pipelined4", "pipelined8", "fused", "serial"] \
+            if args.schedule == "auto" else [args.schedule]
+        trials = {}
+        for name in cands:
+            set_schedule(name)
+            for _ in range(3):
+                comm.step(g, args.dtype, 0.1, 0.9, stream)
+            torch.cuda.synchronize()
+            barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(10):
+                comm.step(g, args.dtype, 0.1, 0.9, stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            t = torch.tensor([a.elapsed_time(b) / 10], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            trials[name] = float(t.item()) * 1e3
+        schedule = min(trials, key=trials.get)
+        set_schedule(schedule)
+
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
@@ -409,6 +442,7 @@ def main():
                        f"{'2' if args.dtype == 'fp32' else '3'})",
            "n_tensors": T, "n_params": P, "padded_len": L, "comm_dtype": args.dtype,
            "algo": args.algo if world > 1 else "identity (N=1 fused direct update)",
+           "schedule": schedule, "schedule_trials_us": trials,
            "lr": 0.1, "mu": 0.9,
            "l2": "inputs larger than L2: 20 B/param = 511 MB streamed per step vs 126 MB L2, "
                  "K steps back to back",
