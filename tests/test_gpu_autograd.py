@@ -170,3 +170,52 @@ def test_backward_hook_overlap_bitwise(cmn):
         finally:
             comm.finalize()
     assert torch.equal(results[0].view(torch.int32), results[1].view(torch.int32))
+
+
+def test_multi_node_optimizer_adam_matches_large_batch(cmn):
+    """The paper's Fig. 4 wraps Adam: N = 2 simulated workers through
+    cmn_allreduce_grads + cmn_update_adam vs an fp64 Adam (Kingma & Ba's
+    alpha_t form, eps added to sqrt(v) -- the form the library implements;
+    torch.optim.Adam adds eps after the bias correction, a different
+    optimizer for |g| near eps) driven by the single-process bn-batch
+    gradient, 4 steps.  Adam's step is ~alpha*sign(g) where the averaged
+    gradient nearly cancels, so such elements may flip between summation
+    orders: 99.9 % must agree tightly, the rest within the 4-step bound."""
+    N = 2
+    model = mlp(seed=13)
+    ref = mlp(seed=13)
+    a, b1, b2, eps = 1e-3, 0.9, 0.999, 1e-8
+    comm = cmn.Comm.simulated_world(N)
+    try:
+        comm.register_params([p.data for p in model.parameters()])
+        w64 = [q.detach().double().clone() for q in ref.parameters()]
+        m64 = [torch.zeros_like(x) for x in w64]
+        v64 = [torch.zeros_like(x) for x in w64]
+        for it in range(4):
+            x, y = data(16 * N, seed=400 + it)
+            gw = worker_grads(model, x, y, N)
+            comm.allreduce_grads(gw, "fp32")
+            comm.update_adam(a, b1, b2, eps, it + 1)
+            with torch.no_grad():
+                for q, w_ in zip(ref.parameters(), w64):
+                    q.copy_(w_)
+            ref.zero_grad()
+            torch.nn.functional.cross_entropy(ref(x), y).backward()
+            t = it + 1
+            at = a * (1 - b2 ** t) ** 0.5 / (1 - b1 ** t)
+            for q, w_, m_, v_ in zip(ref.parameters(), w64, m64, v64):
+                g = q.grad.double()
+                m_.mul_(b1).add_((1 - b1) * g)
+                v_.mul_(b2).add_((1 - b2) * g * g)
+                w_.sub_(at * m_ / (v_.sqrt() + eps))
+        torch.cuda.synchronize()
+        total, close = 0, 0
+        for p, w_ in zip(model.parameters(), w64):
+            d = (p.double() - w_).abs()
+            ok = d <= 1e-4 * w_.abs() + 2e-6
+            total += d.numel()
+            close += int(ok.sum())
+            assert float(d.max()) <= 4 * a * 1.01
+        assert close >= 0.999 * total, (close, total)
+    finally:
+        comm.finalize()
