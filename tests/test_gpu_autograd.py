@@ -211,7 +211,7 @@ def test_multi_node_optimizer_adam_matches_large_batch(cmn):
         torch.cuda.synchronize()
         total, close = 0, 0
         for p, w_ in zip(model.parameters(), w64):
-            d = (p.double() - w_).abs()
+            d = (p.detach().double() - w_).abs()
             ok = d <= 1e-4 * w_.abs() + 2e-6
             total += d.numel()
             close += int(ok.sum())
