@@ -447,9 +447,10 @@ def main():
            "l2": "inputs larger than L2: 20 B/param = 511 MB streamed per step vs 126 MB L2, "
                  "K steps back to back",
            "step_us_after_l2_write_flush": cold_us,
+           "warmup_steps_run": n_w,
            "parallelism": f"dp{world}"}
     line = {"metric": METRIC, "value": us, "unit": "us", "n_gpus": world, "steps": args.steps,
-            "warmup": n_w, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded counter-hash, synth/)",
             "config": cfg, "bus_gbs": bus, "hbm_gbs": roof["achieved"] if world == 1 else None,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
