@@ -32,6 +32,18 @@ sys.path.insert(0, ROOT)
 METRIC = "allreduce+update step µs and bus GB/s (ResNet-50 grads) at 1/2/4/8 B200 vs roofline"
 FALLBACK_HBM_GBS = 6650.0
 
+# N > 1 step schedules: name -> (fused all-gather+update, pipeline pieces,
+# all-reduce CTAs per SM, update CTAs per SM; 0 = library default).
+SCHEDULES = {
+    "pipelined2": (False, 2, 0, 0),
+    "pipelined4": (False, 4, 0, 0),
+    "pipelined8": (False, 8, 0, 0),
+    "pipelined4_2cta": (False, 4, 2, 0),
+    "fused": (True, 0, 0, 0),
+    "fused_2cta": (True, 0, 2, 2),
+    "serial": (False, 0, 0, 0),
+}
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -42,7 +54,7 @@ def parse():
     ap.add_argument("--dtype", default="fp32", choices=["fp32", "fp16"])
     ap.add_argument("--algo", default="auto", choices=["auto", "oneshot", "twoshot", "nccl", "nvls"])
     ap.add_argument("--schedule", default="auto",
-                    choices=["auto", "pipelined2", "pipelined4", "pipelined8", "fused", "serial"],
+                    choices=["auto"] + list(SCHEDULES),
                     help="N > 1 step schedule; auto = short max-over-ranks trial of each, fastest wins")
     ap.add_argument("--min-warmup-s", type=float, default=1.0,
                     help="keep warming up (untimed) at least this long so the clock sampler sees load")
@@ -267,17 +279,20 @@ def main():
         if world > 1:
             dist.barrier()
 
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+
     def set_schedule(name):
-        comm.set_fused_update(name == "fused")
-        comm.set_pipeline(int(name[len("pipelined"):]) if name.startswith("pipelined") else 0)
+        fused, pieces, ar_x, upd_x = SCHEDULES[name]
+        comm.set_fused_update(fused)
+        comm.set_pipeline(pieces)
+        comm.set_ctas(min(1024, ar_x * nsm), min(1024, upd_x * nsm))
 
     schedule, trials = "identity (N=1 fused direct update)", None
     if world > 1:
         # Runtime schedule choice: every rank times each candidate (max over
         # ranks, so all ranks pick the same one); switching schedules between
         # calls is safe (every buffer reuse is behind a start barrier).
-        cands = ["pipelined2", "pipelined4", "pipelined8", "fused", "serial"] \
-            if args.schedule == "auto" else [args.schedule]
+        cands = list(SCHEDULES) if args.schedule == "auto" else [args.schedule]
         trials = {}
         for name in cands:
             set_schedule(name)
@@ -402,7 +417,8 @@ def main():
                "overlap_floor_us": max(h2d_us, d2h_us), "serial_floor_us": h2d_us + d2h_us,
                "d2h_bytes_per_step": 4 * L,
                "path": "cmn_step_host_packed: pinned host grads (packed layout) -> device, "
-                       "step, params -> pinned host; pipelined over 8 tensor ranges at N=1"}
+                       "step, params -> pinned host" + ("; pipelined over 8 tensor ranges at N=1"
+                                                         if world == 1 else "")}
 
     comm.finalize()
     if rank != 0:

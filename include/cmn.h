@@ -307,6 +307,17 @@ cmn_status cmn_set_pipeline(cmn_comm *comm, int pieces);
  * setting.  Default off. */
 cmn_status cmn_set_fused_update(cmn_comm *comm, int on);
 
+/* cmn_set_ctas -- grid sizes of the cross-rank kernels (takes effect on the
+ * next call; 0 restores the default).  `collective_ctas`: one-shot, two-shot
+ * and NVLS all-reduce kernels (default one CTA per SM; two per SM for a
+ * simulated communicator).  `update_ctas`: the barrier-gated, item-striding
+ * update kernels of the fused and sharded schedules (default 4 per SM).
+ * Both at most 1024 (the signal pad's per-CTA cells), else
+ * CMN_ERR_INVALID_ARG.  Results do not depend on them.  Collective: every
+ * rank must use the same values (CTA b of every rank pairs with CTA b of
+ * its peers). */
+cmn_status cmn_set_ctas(cmn_comm *comm, int collective_ctas, int update_ctas);
+
 /* cmn_set_timeout -- device spin-wait timeout in milliseconds (default
  * 30000). */
 cmn_status cmn_set_timeout(cmn_comm *comm, uint32_t timeout_ms);

@@ -49,6 +49,7 @@ SIGNATURES = [
     ("cmn_set_algo", C.c_int, [_P, C.c_int, C.c_size_t]),
     ("cmn_set_pipeline", C.c_int, [_P, C.c_int]),
     ("cmn_set_fused_update", C.c_int, [_P, C.c_int]),
+    ("cmn_set_ctas", C.c_int, [_P, C.c_int, C.c_int]),
     ("cmn_set_timeout", C.c_int, [_P, C.c_uint32]),
     ("cmn_get_momentum", C.c_int, [_P, C.c_int, _PP]),
     ("cmn_get_adam_state", C.c_int, [_P, C.c_int, _PP, _PP]),
@@ -345,6 +346,9 @@ class Comm:
 
     def set_pipeline(self, pieces: int):
         _check(lib().cmn_set_pipeline(self._h, pieces), "cmn_set_pipeline")
+
+    def set_ctas(self, collective_ctas: int = 0, update_ctas: int = 0):
+        _check(lib().cmn_set_ctas(self._h, collective_ctas, update_ctas), "cmn_set_ctas")
 
     def set_timeout(self, ms: int):
         _check(lib().cmn_set_timeout(self._h, ms), "cmn_set_timeout")

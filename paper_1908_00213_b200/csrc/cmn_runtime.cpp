@@ -151,7 +151,8 @@ struct cmn_comm {
     cmn_algo algo = CMN_ALGO_AUTO;
     size_t oneshot_max = 1u << 20;
     uint32_t timeout_ms = 30000;
-    int ar_blocks = 0;
+    int ar_blocks = 0;            // cmn_set_ctas: collective grid (0 = default)
+    int upd_blocks = 0;           // cmn_set_ctas: barrier-gated update grid (0 = default)
     int *h_err = nullptr, *d_err = nullptr;
     uint64_t launches = 0;
     std::vector<std::pair<int, int>> buckets;   // [t_begin, t_end), reverse order
@@ -328,6 +329,20 @@ int ar_blocks_for(const cmn_comm *c) {
     const size_t env = env_size("CMN_CTAS", 0);
     int b = env ? static_cast<int>(env) : (c->simulated ? 2 : 1) * c->nsm;
     if (b > kMaxBarrierBlocks) b = kMaxBarrierBlocks;
+    if (b < 1) b = 1;
+    return b;
+}
+
+// Grid of the barrier-gated HBM-bound kernels that grid-stride over work
+// items (k_update_gather, k_gather_params): they stream 20 B/param through
+// HBM, which one CTA per SM cannot saturate (scripts/update_variants.cu:
+// persistent 4 CTAs/SM reach 6.0 TB/s), so default to 4 per SM -- the
+// register-limited residency of the 256-thread item kernels -- capped by
+// the signal pad, and never more CTAs than items.
+int upd_blocks_for(const cmn_comm *c, int items) {
+    int b = c->upd_blocks > 0 ? c->upd_blocks : 4 * c->nsm;
+    if (b > kMaxBarrierBlocks) b = kMaxBarrierBlocks;
+    if (b > items) b = items;
     if (b < 1) b = 1;
     return b;
 }
@@ -814,7 +829,7 @@ cmn_status step_sharded(cmn_comm *c, const float *const *grads, int dtype, float
     ++c->seq;
     const Barrier bar2 = make_barrier(c, 3);
     const int total = c->sitem_begin[c->world];
-    const int gblocks = total < blocks ? (total > 0 ? total : 1) : blocks;
+    const int gblocks = upd_blocks_for(c, total);
     for (int i = 0; i < nsim; ++i) {
         const int r = c->simulated ? i : c->rank;
         cmn_status st = launched(c,
@@ -860,7 +875,7 @@ cmn_status step_fused(cmn_comm *c, const float *const *grads, int dtype, float l
     ++c->seq;
     const Barrier bar2 = make_barrier(c, dtype);
     const int total = c->sitem_begin[c->world];
-    const int gblocks = total < blocks ? (total > 0 ? total : 1) : blocks;
+    const int gblocks = upd_blocks_for(c, total);
     // simulated ranks share one parameter replica: one launch updates it all
     cmn_status st = launched(c,
                              launch_update_gather(c->d_td, c->d_sitems, 0, total, red, c->world, dtype,
@@ -1413,6 +1428,16 @@ cmn_status cmn_set_pipeline(cmn_comm *c, int pieces) {
     if (!c) return fail(CMN_ERR_INVALID_ARG, "comm is NULL");
     if (pieces < 0 || pieces > 64) return fail(CMN_ERR_INVALID_ARG, "pieces must be in [0, 64]");
     c->pipe_pieces = pieces;
+    return CMN_OK;
+}
+
+cmn_status cmn_set_ctas(cmn_comm *c, int collective_ctas, int update_ctas) {
+    if (!c) return fail(CMN_ERR_INVALID_ARG, "comm is NULL");
+    if (collective_ctas < 0 || collective_ctas > kMaxBarrierBlocks || update_ctas < 0 ||
+        update_ctas > kMaxBarrierBlocks)
+        return fail(CMN_ERR_INVALID_ARG, "CTA counts must be in [0, 1024] (0 = default)");
+    c->ar_blocks = collective_ctas;
+    c->upd_blocks = update_ctas;
     return CMN_OK;
 }
 

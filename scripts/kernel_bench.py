@@ -113,6 +113,18 @@ def main():
                         rec["nvls_nvlink_gbs_per_direction"] = 2 * c * P / (t_nv_only * 1e-6) / 1e9
                     except Exception as e:  # noqa: BLE001 -- reported, not fatal
                         rec["nvls_error"] = str(e)
+                    # NEXT-1: fused bias-corrected Adam from the packed buffer
+                    # (28 B/param fp32 r, 26 B/param fp16 r: read r, w, m, v;
+                    # write w, m, v)
+                    comm.set_algo("auto")
+
+                    def adam():
+                        comm.allreduce_grads(gg, dtype)
+                        comm.update_adam(1e-3, 0.9, 0.999, 1e-8, 1)
+                    t_adam = timed(adam, args.iters, stream) - t_ar
+                    rec["adam_update_us"] = t_adam
+                    rec["adam_update_gbs"] = (24 + c) * P / (t_adam * 1e-6) / 1e9
+                    rec["adam_update_frac"] = rec["adam_update_gbs"] / peak
                     rec["fused_step_us"] = t_step
                     rec["fused_step_gbs"] = 20 * P / (t_step * 1e-6) / 1e9
                     rec["fused_step_frac"] = rec["fused_step_gbs"] / peak

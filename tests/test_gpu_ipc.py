@@ -85,7 +85,20 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode, pieces=0):
                 continue                              # fault injection: rank 1 skips a collective
             if mode == "reregister" and s == 1:
                 comm.register_params(w)               # collective; resets momentum (reading R7)
-            if mode == "sharded":
+            if mode == "mixed":
+                # the schedule and the grid sizes change every step, identically
+                # on every rank: per-CTA barrier epochs must stay paired
+                fused, pcs, ctas = [(True, 0, (5, 3)), (False, 2, (9, 0)),
+                                    (False, 0, (0, 0)), (True, 0, (1, 700))][s % 4]
+                comm.set_fused_update(fused)
+                comm.set_pipeline(pcs)
+                comm.set_ctas(*ctas)
+                if fused or pcs:
+                    comm.step(g, dtype, 0.1, 0.9)
+                else:
+                    comm.allreduce_grads(g, dtype)
+                    comm.update_momentum_sgd(0.1, 0.9)
+            elif mode == "sharded":
                 comm.step_sharded(g, dtype, 0.1, 0.9)  # RS -> own-chunk update -> param all-gather
             elif mode == "fused":
                 comm.step(g, dtype, 0.1, 0.9)         # RS -> fused all-gather + update
@@ -205,6 +218,22 @@ def test_ipc_fused_allgather_update(orc, world, dtype):
     w = synth.params(shapes)
     v = [np.zeros_like(x) for x in w]
     for s in range(2):
+        orc.step(synth.grads(shapes, workers=world, step=s), w, v, 0.1, 0.9, dtype)
+    for r in res:
+        assert np.array_equal(np.frombuffer(r[2], np.uint32), np.concatenate(w).view(np.uint32))
+        assert np.array_equal(np.frombuffer(r[3], np.uint32), np.concatenate(v).view(np.uint32))
+
+
+@pytest.mark.parametrize("world,dtype", [(2, "fp32"), (3, "fp16")])
+def test_ipc_mixed_schedules_and_grids(orc, world, dtype):
+    """Schedules (fused, pipelined, serial) and CTA counts (cmn_set_ctas)
+    switched between steps: bit-exact with the oracle on every rank."""
+    res = _run(world, dtype, "twoshot", steps=4, mode="mixed")
+    assert all(r[1] == "ok" for r in res), res
+    shapes = synth.mlp_shapes()
+    w = synth.params(shapes)
+    v = [np.zeros_like(x) for x in w]
+    for s in range(4):
         orc.step(synth.grads(shapes, workers=world, step=s), w, v, 0.1, 0.9, dtype)
     for r in res:
         assert np.array_equal(np.frombuffer(r[2], np.uint32), np.concatenate(w).view(np.uint32))

@@ -269,8 +269,10 @@ def test_pipelined_step_parity(cmn, orc, N, pieces, dtype):
         comm.finalize()
 
 
-@pytest.mark.parametrize("N,dtype", [(2, "fp32"), (3, "fp16"), (4, "fp16"), (8, "fp32")])
-def test_fused_allgather_update_parity(cmn, orc, N, dtype):
+@pytest.mark.parametrize("N,dtype,ctas", [(2, "fp32", (0, 0)), (3, "fp16", (0, 0)),
+                                          (4, "fp16", (3, 1)), (8, "fp32", (0, 0)),
+                                          (8, "fp32", (1024, 1024))])
+def test_fused_allgather_update_parity(cmn, orc, N, dtype, ctas):
     """Fused two-shot step (reduce-scatter, then one kernel updating every
     parameter from the owners' reduced chunks) == oracle bitwise, 3 steps."""
     shapes = synth.resnet50_shapes()[:30] + RAGGED
@@ -282,6 +284,7 @@ def test_fused_allgather_update_parity(cmn, orc, N, dtype):
         w = to_dev(params0)
         comm.register_params(w)
         comm.set_fused_update(True)
+        comm.set_ctas(*ctas)            # grid sizes never change results
         for s, g in enumerate(grads):
             comm.step([to_dev(gw) for gw in g], dtype, 0.1, 0.9)
             torch.cuda.synchronize()
@@ -292,8 +295,9 @@ def test_fused_allgather_update_parity(cmn, orc, N, dtype):
         comm.finalize()
 
 
-@pytest.mark.parametrize("N,dtype", [(2, "fp32"), (3, "fp16"), (4, "fp32"), (8, "fp16"), (8, "fp32")])
-def test_sharded_update_parity(cmn, orc, N, dtype):
+@pytest.mark.parametrize("N,dtype,ctas", [(2, "fp32", (0, 0)), (3, "fp16", (0, 0)), (4, "fp32", (7, 2)),
+                                          (8, "fp16", (0, 0)), (8, "fp32", (0, 1024))])
+def test_sharded_update_parity(cmn, orc, N, dtype, ctas):
     """NEXT-4 (cmn_step_sharded): reduce-scatter, update of the own chunk,
     all-gather of parameters == oracle bitwise over 3 steps (w, and v, which
     the simulated ranks together update in full)."""
@@ -305,6 +309,7 @@ def test_sharded_update_parity(cmn, orc, N, dtype):
     try:
         w = to_dev(params0)
         comm.register_params(w)
+        comm.set_ctas(*ctas)
         for s, g in enumerate(grads):
             comm.step_sharded([to_dev(gw) for gw in g], dtype, 0.1, 0.9)
             torch.cuda.synchronize()
@@ -593,6 +598,10 @@ def test_errors_are_loud(cmn):
             comm.update_momentum_sgd(0.1, 0.9)         # consumed
         with pytest.raises(cmn.CmnError):
             comm.set_algo("nccl")                      # simulated: unsupported
+        for bad_ctas in ((-1, 0), (0, 1025), (2000, 0)):
+            with pytest.raises(cmn.CmnError) as e:
+                comm.set_ctas(*bad_ctas)
+            assert e.value.status_name == "CMN_ERR_INVALID_ARG"
     finally:
         comm.finalize()
 
