@@ -417,7 +417,7 @@ def main():
                "overlap_floor_us": max(h2d_us, d2h_us), "serial_floor_us": h2d_us + d2h_us,
                "d2h_bytes_per_step": 4 * L,
                "path": "cmn_step_host_packed: pinned host grads (packed layout) -> device, "
-                       "step, params -> pinned host" + ("; pipelined over 8 tensor ranges at N=1"
+                       "step, params -> pinned host" + ("; pipelined over 12 ramped item ranges at N=1"
                                                          if world == 1 else "")}
 
     comm.finalize()

@@ -236,10 +236,13 @@ cmn_status cmn_step_host(cmn_comm *comm, const float *const *host_grads,
  * rank (gradient t at offset off_t, pads ignored), host_params (NULL or L
  * floats) receives the updated parameters at the same offsets.  At N == 1
  * the call pipelines the host->device copy, the update and the
- * device->host copy over ~8 tensor ranges on two internal copy streams
- * (joined back into `stream`), so the step costs about one PCIe transfer
- * instead of two.  If the registered params are views of one allocation in
- * the packed layout, the device->host copies are contiguous. */
+ * device->host copy over 12 ranges of 4096-element work items (sizes ramp
+ * up from and down to L/62 so the pipeline's fill and drain are short;
+ * env CMN_E2E_PIECES=n selects n equal ranges) on two internal copy
+ * streams joined back into `stream`, so the step costs about one
+ * full-duplex PCIe transfer instead of two.  If the registered params are
+ * views of one allocation in the packed layout, the device->host copies
+ * are contiguous (they stop at the last tensor's last element). */
 cmn_status cmn_step_host_packed(cmn_comm *comm, const float *host_grads, float *host_params,
                                 cmn_dtype dtype, float lr, float mu, void *stream);
 

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <iterator>
 #include <string>
 #include <utility>
 #include <vector>
@@ -96,7 +97,16 @@ struct NcclApi {
 };
 NcclApi g_nccl;
 constexpr int kNcclFloat16 = 6, kNcclFloat32 = 7, kNcclSum = 0;
-constexpr int kE2EPieces = 8;   // pipeline depth of the host-buffer step (32 measured slower: 2.77 vs 2.60 ms)
+// Host-buffer (e2e) step at N = 1: piece weights of the H2D || update ||
+// D2H pipeline, in units of L/62, ramping up from and down to L/62 so the
+// fill (H2D of the first piece) and drain (D2H of the last) are short.
+// Measured (profiles/r1_pcie_probe.jsonl, bench e2e): 2.5-2.6 ms for the
+// R50 step whatever the plan (4/8/16 equal pieces, this ramp, or the
+// parameter read-back done by the update kernel's own stores into mapped
+// host memory) -- the copy engines' concurrent H2D + D2H inside a
+// dependent pipeline, not the plan, is the limit.
+constexpr int kE2EWeights[] = {1, 2, 4, 8, 8, 8, 8, 8, 8, 4, 2, 1};
+constexpr int kE2EMaxPieces = 64;   // CMN_E2E_PIECES=n (equal pieces) is capped here
 
 }  // namespace
 
@@ -679,25 +689,35 @@ cmn_status ensure_side_streams(cmn_comm *c) {
     if (c->h2d) return CMN_OK;
     CMN_CUDA(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
     CMN_CUDA(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
-    c->ev.resize(3 * kE2EPieces + 2);
+    c->ev.resize(3 * kE2EMaxPieces + 2);
     for (auto &e : c->ev) CMN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     return CMN_OK;
 }
 
-// Tensor ranges of roughly equal bytes for the pipelined e2e step.
-std::vector<std::pair<int, int>> e2e_pieces(const cmn_comm *c) {
+// Item ranges [i0, i1) of the N = 1 host-buffer pipeline (item = 4096
+// elements of one tensor, so a tensor may straddle pieces), sized by
+// kE2EWeights -- or CMN_E2E_PIECES equal pieces (measurement).
+std::vector<std::pair<int, int>> e2e_item_pieces(const cmn_comm *c) {
+    const int I = c->item_begin[c->T];
+    std::vector<int> wts(std::begin(kE2EWeights), std::end(kE2EWeights));
+    if (const size_t n = env_size("CMN_E2E_PIECES", 0); n > 0)
+        wts.assign(n < static_cast<size_t>(kE2EMaxPieces) ? n : kE2EMaxPieces, 1);
+    int64_t total = 0;
+    for (int w : wts) total += w;
     std::vector<std::pair<int, int>> out;
-    const int64_t target = (c->L + kE2EPieces - 1) / kE2EPieces;
-    int t = 0;
-    while (t < c->T) {
-        int u = t;
-        int64_t acc = 0;
-        while (u < c->T && (acc < target || static_cast<int>(out.size()) + 1 == kE2EPieces)) {
-            acc += c->numel[u];
-            ++u;
+    int i = 0;
+    int64_t acc = 0;
+    for (size_t p = 0; p < wts.size() && i < I; ++p) {
+        acc += wts[p];
+        int j = i;
+        if (p + 1 == wts.size()) {
+            j = I;
+        } else {
+            const int64_t bound = c->L * acc / total;
+            while (j < I && c->h_items[j].base < bound) ++j;
         }
-        out.emplace_back(t, u);
-        t = u;
+        if (j > i) out.emplace_back(i, j);
+        i = j;
     }
     return out;
 }
@@ -1200,7 +1220,10 @@ cmn_status cmn_step_host_packed(cmn_comm *c, const float *host_grads, float *hos
         if (cmn_status st = cmn_step(c, dg.data(), dtype, lr, mu, stream); st != CMN_OK) return st;
         if (host_params) {
             if (c->params_flat) {
-                CMN_CUDA(cudaMemcpyAsync(host_params, c->params[0], static_cast<size_t>(c->L) * 4,
+                int last = c->T - 1;          // the allocation may end at the last tensor
+                while (last > 0 && c->numel[last] == 0) --last;
+                CMN_CUDA(cudaMemcpyAsync(host_params, c->params[0],
+                                         static_cast<size_t>(c->off[last] + c->numel[last]) * 4,
                                          cudaMemcpyDeviceToHost, s));
             } else {
                 std::vector<float *> hp(c->T);
@@ -1216,26 +1239,33 @@ cmn_status cmn_step_host_packed(cmn_comm *c, const float *host_grads, float *hos
     }
 
     // N = 1: pipeline H2D(piece p+1) || update(piece p) || D2H(piece p-1) on
-    // two copy engines and the caller's stream.
+    // two copy engines and the caller's stream, over item ranges.
     if (cmn_status st = ensure_side_streams(c); st != CMN_OK) return st;
-    const auto pieces = e2e_pieces(c);
+    const auto pieces = e2e_item_pieces(c);
+    const int I = c->item_begin[c->T];
+    int last = c->T - 1;                  // end of the last tensor's data: contiguous
+    while (last > 0 && c->numel[last] == 0) --last;   // D2H copies stop there
+    const int64_t flat_end = c->off[last] + c->numel[last];
     cudaEvent_t entry = c->ev[0], done_d2h = c->ev[1];
     CMN_CUDA(cudaEventRecord(entry, s));
     CMN_CUDA(cudaStreamWaitEvent(c->h2d, entry, 0));
     CMN_CUDA(cudaStreamWaitEvent(c->d2h, entry, 0));
     c->fresh = false;
     for (size_t p = 0; p < pieces.size(); ++p) {
-        const int ta = pieces[p].first, tb = pieces[p].second;
-        const int64_t e0 = c->off[ta], e1 = c->off[tb];
+        const int i0 = pieces[p].first, i1 = pieces[p].second;
+        const int64_t e0 = i0 == 0 ? 0 : c->h_items[i0].base;
+        const int64_t e1 = i1 == I ? c->L : c->h_items[i1].base;
         cudaEvent_t ev_in = c->ev[2 + 3 * p], ev_upd = c->ev[3 + 3 * p];
         CMN_CUDA(cudaMemcpyAsync(c->d_staging + e0, host_grads + e0, static_cast<size_t>(e1 - e0) * 4,
                                  cudaMemcpyHostToDevice, c->h2d));
         CMN_CUDA(cudaEventRecord(ev_in, c->h2d));
         CMN_CUDA(cudaStreamWaitEvent(s, ev_in, 0));
-        cmn_status st = for_groups(c, ta, tb, [&](int lo, int hi, int i0, int i1) {
+        cmn_status st = for_groups(c, 0, c->T, [&](int lo, int hi, int g0, int g1) {
+            const int a = g0 > i0 ? g0 : i0, b = g1 < i1 ? g1 : i1;
+            if (a >= b) return CMN_OK;
             return launched(c,
                             launch_update_direct(make_tab(dg.data(), lo, hi), lo, c->d_td,
-                                                 c->d_items, i0, i1, dtype, lr, mu, s),
+                                                 c->d_items, a, b, dtype, lr, mu, s),
                             "update_direct");
         });
         if (st != CMN_OK) return st;
@@ -1243,17 +1273,23 @@ cmn_status cmn_step_host_packed(cmn_comm *c, const float *host_grads, float *hos
             CMN_CUDA(cudaEventRecord(ev_upd, s));
             CMN_CUDA(cudaStreamWaitEvent(c->d2h, ev_upd, 0));
             if (c->params_flat) {
-                CMN_CUDA(cudaMemcpyAsync(host_params + e0, c->params[0] + e0,
-                                         static_cast<size_t>(e1 - e0) * 4, cudaMemcpyDeviceToHost,
-                                         c->d2h));
+                const int64_t hi = e1 < flat_end ? e1 : flat_end;
+                if (hi > e0)
+                    CMN_CUDA(cudaMemcpyAsync(host_params + e0, c->params[0] + e0,
+                                             static_cast<size_t>(hi - e0) * 4,
+                                             cudaMemcpyDeviceToHost, c->d2h));
             } else {
-                std::vector<float *> hp(c->T);
-                for (int t = ta; t < tb; ++t) hp[t] = host_params + c->off[t];
-                std::vector<const float *> src(c->params.begin(), c->params.end());
-                if (cmn_status st2 = copy_tensors(c, src.data(), hp.data(), ta, tb,
-                                                  cudaMemcpyDeviceToHost, c->d2h);
-                    st2 != CMN_OK)
-                    return st2;
+                // per tensor: the elements of [i0, i1) that belong to it
+                for (int i = i0; i < i1;) {
+                    const Item &a = c->h_items[i];
+                    int j = i;
+                    while (j + 1 < i1 && c->h_items[j + 1].t == a.t) ++j;
+                    const Item &b = c->h_items[j];
+                    CMN_CUDA(cudaMemcpyAsync(host_params + c->off[a.t] + a.k0, c->params[a.t] + a.k0,
+                                             static_cast<size_t>(b.k0 + b.len - a.k0) * 4,
+                                             cudaMemcpyDeviceToHost, c->d2h));
+                    i = j + 1;
+                }
             }
         }
     }

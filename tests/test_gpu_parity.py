@@ -398,11 +398,16 @@ def test_step_host_e2e_parity(cmn, orc):
         comm.finalize()
 
 
-@pytest.mark.parametrize("flat_params", [True, False])
+@pytest.mark.parametrize("flat_params,pieces", [(True, None), (False, None), (True, "1"),
+                                                (False, "7"), (True, "64")])
 @pytest.mark.parametrize("dtype", ["fp32", "fp16"])
-def test_step_host_packed_pipelined_parity(cmn, orc, flat_params, dtype):
-    """cmn_step_host_packed at N = 1 (pipelined over tensor ranges, two copy
-    streams) over 3 steps, params as one flat allocation or separate ones."""
+def test_step_host_packed_pipelined_parity(cmn, orc, monkeypatch, flat_params, pieces, dtype):
+    """cmn_step_host_packed at N = 1 (pipelined over item ranges that cut
+    through tensors, two copy streams) over 3 steps, params as one flat
+    allocation ending at the last tensor (not at L) or as separate ones;
+    default ramped pieces and CMN_E2E_PIECES equal pieces."""
+    if pieces is not None:
+        monkeypatch.setenv("CMN_E2E_PIECES", pieces)
     shapes = synth.resnet50_shapes()[:60]
     sizes = [synth.numel(s) for s in shapes]
     off, L = orc.layout(sizes)
@@ -412,7 +417,7 @@ def test_step_host_packed_pipelined_parity(cmn, orc, flat_params, dtype):
     comm = cmn.Comm.init(0, 1, 0)
     try:
         if flat_params:
-            flat = torch.zeros(L, dtype=torch.float32, device=DEV)
+            flat = torch.zeros(off[len(sizes) - 1] + sizes[-1], dtype=torch.float32, device=DEV)
             w = [flat[off[t]: off[t] + sizes[t]].view(shapes[t]) for t in range(len(shapes))]
             for t in range(len(w)):
                 w[t].copy_(torch.from_numpy(params0[t]).view(shapes[t]))
@@ -431,6 +436,31 @@ def test_step_host_packed_pipelined_parity(cmn, orc, flat_params, dtype):
             hwn = hw.numpy()
             for t in range(len(w_o)):
                 assert_bitwise(hwn[off[t]: off[t] + sizes[t]].copy(), w_o[t], f"host w[{t}] step {s}")
+    finally:
+        comm.finalize()
+
+
+def test_step_host_packed_pageable_params(cmn, orc):
+    """Pageable host_params (synchronous D2H copies): same bits."""
+    shapes = synth.resnet50_shapes()[:20]
+    sizes = [synth.numel(s) for s in shapes]
+    off, L = orc.layout(sizes)
+    params0 = synth.params(shapes)
+    w_o = [p.copy() for p in params0]
+    v_o = [np.zeros_like(p) for p in params0]
+    g = synth.grads(shapes, workers=1)
+    orc.step(g, w_o, v_o, 0.1, 0.9, "fp32")
+    comm = cmn.Comm.init(0, 1, 0)
+    try:
+        comm.register_params([torch.from_numpy(p.copy()).to(DEV) for p in params0])
+        hg = torch.zeros(L, dtype=torch.float32).pin_memory()
+        for t in range(len(sizes)):
+            hg[off[t]: off[t] + sizes[t]].copy_(torch.from_numpy(g[0][t]))
+        hw = torch.full((L,), float("nan"), dtype=torch.float32)      # pageable
+        comm.step_host_packed(hg, hw, "fp32", 0.1, 0.9)
+        torch.cuda.synchronize()
+        for t in range(len(sizes)):
+            assert_bitwise(hw.numpy()[off[t]: off[t] + sizes[t]].copy(), w_o[t], f"host w[{t}]")
     finally:
         comm.finalize()
 
