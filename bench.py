@@ -18,6 +18,7 @@ ONE JSON line.
 from __future__ import annotations
 
 import argparse
+import contextlib
 import json
 import os
 import statistics
@@ -65,6 +66,21 @@ def parse():
 
 
 # ----------------------------------------------------------------- helpers
+
+@contextlib.contextmanager
+def stdout_to_stderr():
+    """Route fd 1 to stderr (native libraries, e.g. NCCL's version banner,
+    must not add lines to the one-JSON-line stdout)."""
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        yield
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
+
 
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -287,15 +303,13 @@ def main():
         comm.set_pipeline(pieces)
         comm.set_ctas(min(1024, ar_x * nsm), min(1024, upd_x * nsm))
 
-    schedule, trials = "identity (N=1 fused direct update)", None
+    schedule, trials, comparisons = "identity (N=1 fused direct update)", None, {}
     if world > 1:
         # Runtime schedule choice: every rank times each candidate (max over
         # ranks, so all ranks pick the same one); switching schedules between
         # calls is safe (every buffer reuse is behind a start barrier).
         cands = list(SCHEDULES) if args.schedule == "auto" else [args.schedule]
-        trials = {}
-        for name in cands:
-            set_schedule(name)
+        def trial_us():
             for _ in range(3):
                 comm.step(g, args.dtype, 0.1, 0.9, stream)
             torch.cuda.synchronize()
@@ -308,7 +322,27 @@ def main():
             torch.cuda.synchronize()
             t = torch.tensor([a.elapsed_time(b) / 10], dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            trials[name] = float(t.item()) * 1e3
+            return float(t.item()) * 1e3
+
+        trials = {}
+        for name in cands:
+            set_schedule(name)
+            trials[name] = trial_us()
+        # Comparisons, not candidates for the headline: the same step with the
+        # all-reduce done by NCCL (the north star's measured comparison) and
+        # by the NVLS in-switch kernel (tolerance-only parity).  Resource
+        # setup is collective and fails on every rank alike.
+        from paper_1908_00213_b200.cmn import CmnError
+        for alt in ("nccl", "nvls"):
+            try:
+                with stdout_to_stderr():
+                    comm.set_algo(alt)
+            except CmnError as e:
+                comparisons[alt] = {"unavailable": str(e)[:160]}
+                continue
+            set_schedule("serial")
+            comparisons[alt] = {"step_us": trial_us()}
+        comm.set_algo(args.algo)
         schedule = min(trials, key=trials.get)
         set_schedule(schedule)
 
@@ -459,6 +493,7 @@ def main():
            "n_tensors": T, "n_params": P, "padded_len": L, "comm_dtype": args.dtype,
            "algo": args.algo if world > 1 else "identity (N=1 fused direct update)",
            "schedule": schedule, "schedule_trials_us": trials,
+           "comparisons": comparisons or None,
            "lr": 0.1, "mu": 0.9,
            "l2": "inputs larger than L2: 20 B/param = 511 MB streamed per step vs 126 MB L2, "
                  "K steps back to back",

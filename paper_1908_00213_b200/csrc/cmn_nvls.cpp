@@ -11,6 +11,7 @@
 // cudaGetDriverEntryPoint, so the library never links libcuda directly.
 #include "cmn_nvls.h"
 
+#include <poll.h>
 #include <sys/socket.h>
 #include <sys/un.h>
 #include <unistd.h>
@@ -104,7 +105,8 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 bool share_fd(int rank, int world, cmn_allgather_fn ag, void *user, int fd_in, int *fd_out,
               std::string &err) {
     struct Name {
-        char path[96];
+        int ok;           // rank 0 is listening (else every rank fails together)
+        char path[92];
     };
     *fd_out = -1;
     if (world == 1) {
@@ -113,11 +115,11 @@ bool share_fd(int rank, int world, cmn_allgather_fn ag, void *user, int fd_in, i
     }
     int lsock = -1;
     Name mine{};
-    if (rank == 0) {
+    if (rank == 0) [&] {
         lsock = ::socket(AF_UNIX, SOCK_STREAM, 0);
         if (lsock < 0) {
             err = "socket() failed";
-            return false;
+            return;
         }
         std::random_device rd;
         std::snprintf(mine.path, sizeof mine.path, "cmn-nvls-%d-%08x%08x", static_cast<int>(getpid()),
@@ -129,18 +131,30 @@ bool share_fd(int rank, int world, cmn_allgather_fn ag, void *user, int fd_in, i
         const socklen_t alen = static_cast<socklen_t>(offsetof(sockaddr_un, sun_path) + 1 + std::strlen(mine.path));
         if (::bind(lsock, reinterpret_cast<sockaddr *>(&a), alen) != 0 || ::listen(lsock, world) != 0) {
             ::close(lsock);
+            lsock = -1;
             err = "bind/listen on the abstract Unix socket failed";
-            return false;
+            return;
         }
-    }
+        mine.ok = 1;
+    }();
     std::vector<Name> all(world);
     if (ag(&mine, all.data(), sizeof(Name), user) != 0) {
         if (lsock >= 0) ::close(lsock);
         err = "allgather callback failed";
         return false;
     }
+    if (!all[0].ok) {
+        if (rank != 0) err = "rank 0 could not open the fd hand-off socket";
+        return false;
+    }
     if (rank == 0) {
         for (int i = 1; i < world; ++i) {
+            pollfd pf{lsock, POLLIN, 0};
+            if (::poll(&pf, 1, 30000) != 1) {   // a peer that never connects must not hang us
+                ::close(lsock);
+                err = "timed out waiting for a peer to fetch the multicast fd";
+                return false;
+            }
             const int s = ::accept(lsock, nullptr, nullptr);
             if (s < 0) {
                 ::close(lsock);
@@ -231,33 +245,58 @@ bool nvls_supported(int device, std::string &err) {
     return true;
 }
 
+namespace {
+// Every rank learns whether every rank succeeded so far, so a local failure
+// never leaves the peers blocked in a later collective step (the fd
+// hand-off, or cuMulticastBindMem, which waits for all devices to join).
+bool agree(int world, cmn_allgather_fn ag, void *user, bool ok, std::string &err) {
+    if (world == 1) return ok;
+    // 1 = ok, 2 = multicast unsupported here, 0 = other failure; every rank
+    // reports the same class (the caller maps "support" to UNSUPPORTED)
+    std::vector<int> all(world);
+    int mine = ok ? 1 : (err.find("support") != std::string::npos ? 2 : 0);
+    if (ag(&mine, all.data(), sizeof(int), user) != 0) {
+        err = "allgather callback failed";
+        return false;
+    }
+    int worst = 1;
+    for (int v : all)
+        if (v != 1 && (worst == 1 || v == 2)) worst = v;
+    if (worst == 1) return true;
+    if (ok) err = worst == 2 ? "multicast not supported on another rank" : "NVLS setup failed on another rank";
+    return false;
+}
+}  // namespace
+
 bool nvls_setup(Nvls &n, int rank, int world, int device, size_t bytes_per_buffer,
                 cmn_allgather_fn ag, void *user, std::string &err) {
     Drv &d = drv();
-    if (!nvls_supported(device, err)) return false;
-    CUdevice dev;
-    DRV(d.DeviceGet(&dev, device), "cuDeviceGet");
+    CUdevice dev = 0;
     CUmulticastObjectProp mp{};
-    mp.numDevices = static_cast<unsigned>(world);
-    mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
-    mp.size = 2 * bytes_per_buffer;
-    size_t g_mc = 0, g_mem = 0;
-    DRV(d.MulticastGetGranularity(&g_mc, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED),
-        "cuMulticastGetGranularity");
     CUmemAllocationProp ap{};
-    ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
-    ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-    ap.location.id = device;
-    ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
-    DRV(d.MemGetAllocationGranularity(&g_mem, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED),
-        "cuMemGetAllocationGranularity");
-    const size_t gran = g_mc > g_mem ? g_mc : g_mem;
-    n.buffer_bytes = align_up(bytes_per_buffer, gran);
-    n.size = 2 * n.buffer_bytes;
-    mp.size = n.size;
-
+    size_t gran = 0;
     int fd = -1, fd_local = -1;
-    if (rank == 0) {
+    // Stage 1: capability, sizes; rank 0 creates and exports the multicast object.
+    const bool ok1 = [&]() -> bool {
+        if (!nvls_supported(device, err)) return false;
+        DRV(d.DeviceGet(&dev, device), "cuDeviceGet");
+        mp.numDevices = static_cast<unsigned>(world);
+        mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+        mp.size = 2 * bytes_per_buffer;
+        size_t g_mc = 0, g_mem = 0;
+        DRV(d.MulticastGetGranularity(&g_mc, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED),
+            "cuMulticastGetGranularity");
+        ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+        ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        ap.location.id = device;
+        ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+        DRV(d.MemGetAllocationGranularity(&g_mem, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED),
+            "cuMemGetAllocationGranularity");
+        gran = g_mc > g_mem ? g_mc : g_mem;
+        n.buffer_bytes = align_up(bytes_per_buffer, gran);
+        n.size = 2 * n.buffer_bytes;
+        mp.size = n.size;
+        if (rank != 0) return true;
         const CUresult rc = d.MulticastCreate(&n.mc, &mp);
         if (rc != CUDA_SUCCESS) {
             // Observed on single-GPU boxes whose NVSwitch fabric is not set up
@@ -271,45 +310,64 @@ bool nvls_setup(Nvls &n, int rank, int world, int device, size_t bytes_per_buffe
         if (world > 1)
             DRV(d.MemExportToShareableHandle(&fd, n.mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0),
                 "cuMemExportToShareableHandle");
-    }
-    if (world > 1) {
-        if (!share_fd(rank, world, ag, user, fd, &fd_local, err)) return false;
-        if (rank != 0) {
-            DRV(d.MemImportFromShareableHandle(&n.mc, reinterpret_cast<void *>(static_cast<intptr_t>(fd_local)),
-                                               CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR),
-                "cuMemImportFromShareableHandle");
-            n.have_mc = true;
-            ::close(fd_local);
-        } else {
-            ::close(fd);
-        }
-    }
-    DRV(d.MulticastAddDevice(n.mc, dev), "cuMulticastAddDevice");
-    DRV(d.MemCreate(&n.mem, n.size, &ap, 0), "cuMemCreate");
-    n.have_mem = true;
-    DRV(d.MulticastBindMem(n.mc, 0, n.mem, 0, n.size, 0), "cuMulticastBindMem");
-    n.bound = true;
-    n.device = device;
-    CUmemAccessDesc acc{};
-    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-    acc.location.id = device;
-    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-    CUdeviceptr uc = 0, mc = 0;
-    DRV(d.MemAddressReserve(&uc, n.size, gran, 0, 0), "cuMemAddressReserve(uc)");
-    n.uc = reinterpret_cast<char *>(uc);
-    DRV(d.MemMap(uc, n.size, 0, n.mem, 0), "cuMemMap(uc)");
-    n.uc_mapped = true;
-    DRV(d.MemSetAccess(uc, n.size, &acc, 1), "cuMemSetAccess(uc)");
-    DRV(d.MemAddressReserve(&mc, n.size, gran, 0, 0), "cuMemAddressReserve(mc)");
-    n.mcva = reinterpret_cast<char *>(mc);
-    DRV(d.MemMap(mc, n.size, 0, n.mc, 0), "cuMemMap(mc)");
-    n.mc_mapped = true;
-    DRV(d.MemSetAccess(mc, n.size, &acc, 1), "cuMemSetAccess(mc)");
-    if (cudaMemset(n.uc, 0, n.size) != cudaSuccess) {
-        err = "cudaMemset of the NVLS buffer failed";
+        return true;
+    }();
+    if (!agree(world, ag, user, ok1, err)) {
+        if (fd >= 0) ::close(fd);
         return false;
     }
-    return true;
+    // Stage 2: hand the fd to the other ranks, import, join the team.
+    bool ok2 = true;
+    if (world > 1) {
+        ok2 = share_fd(rank, world, ag, user, fd, &fd_local, err);
+        if (rank == 0 && fd >= 0) ::close(fd);
+    }
+    ok2 = ok2 && [&]() -> bool {
+        if (world > 1 && rank != 0) {
+            const CUresult rc = d.MemImportFromShareableHandle(
+                &n.mc, reinterpret_cast<void *>(static_cast<intptr_t>(fd_local)),
+                CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+            ::close(fd_local);
+            if (rc != CUDA_SUCCESS) {
+                err = "cuMemImportFromShareableHandle failed (CUresult " + std::to_string(rc) + ")";
+                return false;
+            }
+            n.have_mc = true;
+        }
+        DRV(d.MulticastAddDevice(n.mc, dev), "cuMulticastAddDevice");
+        return true;
+    }();
+    if (!agree(world, ag, user, ok2, err)) return false;
+    // Stage 3: bind this rank's memory (waits until every device joined), map
+    // unicast and multicast views, zero the buffers.
+    const bool ok3 = [&]() -> bool {
+        DRV(d.MemCreate(&n.mem, n.size, &ap, 0), "cuMemCreate");
+        n.have_mem = true;
+        DRV(d.MulticastBindMem(n.mc, 0, n.mem, 0, n.size, 0), "cuMulticastBindMem");
+        n.bound = true;
+        n.device = device;
+        CUmemAccessDesc acc{};
+        acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        acc.location.id = device;
+        acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+        CUdeviceptr uc = 0, mc = 0;
+        DRV(d.MemAddressReserve(&uc, n.size, gran, 0, 0), "cuMemAddressReserve(uc)");
+        n.uc = reinterpret_cast<char *>(uc);
+        DRV(d.MemMap(uc, n.size, 0, n.mem, 0), "cuMemMap(uc)");
+        n.uc_mapped = true;
+        DRV(d.MemSetAccess(uc, n.size, &acc, 1), "cuMemSetAccess(uc)");
+        DRV(d.MemAddressReserve(&mc, n.size, gran, 0, 0), "cuMemAddressReserve(mc)");
+        n.mcva = reinterpret_cast<char *>(mc);
+        DRV(d.MemMap(mc, n.size, 0, n.mc, 0), "cuMemMap(mc)");
+        n.mc_mapped = true;
+        DRV(d.MemSetAccess(mc, n.size, &acc, 1), "cuMemSetAccess(mc)");
+        if (cudaMemset(n.uc, 0, n.size) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+            err = "cudaMemset of the NVLS buffer failed";
+            return false;
+        }
+        return true;
+    }();
+    return agree(world, ag, user, ok3, err);
 }
 
 void nvls_teardown(Nvls &n) {

@@ -1065,8 +1065,11 @@ static cmn_status register_impl(cmn_comm *c, int T, const int *ndims, const int6
             if (c->algo == CMN_ALGO_NVLS) {   // collective: every rank re-registers
                 std::string err;
                 if (!nvls_setup(c->nvls, c->rank, c->world, c->device, static_cast<size_t>(c->L) * 4,
-                                c->ag, c->user, err))
+                                c->ag, c->user, err)) {
+                    nvls_teardown(c->nvls);
+                    c->algo = CMN_ALGO_AUTO;
                     return fail(CMN_ERR_CUDA, "NVLS setup: " + err);
+                }
             }
         }
         CMN_CUDA(cudaDeviceSynchronize());
@@ -1435,16 +1438,27 @@ cmn_status cmn_set_algo(cmn_comm *c, cmn_algo algo, size_t oneshot_max_bytes) {
     }
     if (algo == CMN_ALGO_NCCL && !c->nccl) {
         if (c->simulated) return fail(CMN_ERR_UNSUPPORTED, "NCCL needs one process per GPU");
-        if (!g_nccl.load()) return fail(CMN_ERR_NCCL, "cannot load libnccl (set CMN_NCCL_LIB)");
         if (cmn_status st = set_device(c); st != CMN_OK) return st;
-        NcclUniqueId id{};
-        if (c->rank == 0 && g_nccl.GetUniqueId(&id) != 0)
-            return fail(CMN_ERR_NCCL, "ncclGetUniqueId failed");
-        std::vector<NcclUniqueId> all(c->world);
-        if (!allgather(c, &id, all.data(), sizeof(NcclUniqueId)))
+        // Every rank joins the id exchange even after a local failure, with
+        // its status alongside, so no rank is left blocked in a collective.
+        struct IdMsg {
+            int ok;
+            NcclUniqueId id;
+        } mine{};
+        std::string why;
+        if (!g_nccl.load())
+            why = "cannot load libnccl (set CMN_NCCL_LIB)";
+        else if (c->rank == 0 && g_nccl.GetUniqueId(&mine.id) != 0)
+            why = "ncclGetUniqueId failed";
+        mine.ok = why.empty() ? 1 : 0;
+        std::vector<IdMsg> all(c->world);
+        if (!allgather(c, &mine, all.data(), sizeof(IdMsg)))
             return fail(CMN_ERR_BOOTSTRAP, "allgather callback failed");
+        for (int r = 0; r < c->world && why.empty(); ++r)
+            if (!all[r].ok) why = "NCCL setup failed on rank " + std::to_string(r);
+        if (!why.empty()) return fail(CMN_ERR_NCCL, why);
         void *comm = nullptr;
-        const int rc = g_nccl.CommInitRank(&comm, c->world, all[0], c->rank);   // rank 0's id
+        const int rc = g_nccl.CommInitRank(&comm, c->world, all[0].id, c->rank);   // rank 0's id
         if (rc != 0)
             return fail(CMN_ERR_NCCL, std::string("ncclCommInitRank: ") +
                                           (g_nccl.GetErrorString ? g_nccl.GetErrorString(rc) : "?"));

@@ -46,6 +46,17 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode, pieces=0):
         except cmn.CmnError as e:
             q.put((rank, "error", e.status_name))
             return
+        if mode == "setup_alt":
+            # NVLS / NCCL resources are created collectively: whatever the box
+            # supports, every rank must get the same outcome (never a hang)
+            try:
+                comm.set_algo(algo)
+                q.put((rank, "ok"))
+            except cmn.CmnError as e:
+                q.put((rank, "error", e.status_name))
+            dist.barrier()
+            comm.finalize()
+            return
         comm.set_algo(algo)
         comm.set_pipeline(pieces)
         comm.set_fused_update(mode in ("fused", "graph_fused"))
@@ -238,6 +249,15 @@ def test_ipc_mixed_schedules_and_grids(orc, world, dtype):
     for r in res:
         assert np.array_equal(np.frombuffer(r[2], np.uint32), np.concatenate(w).view(np.uint32))
         assert np.array_equal(np.frombuffer(r[3], np.uint32), np.concatenate(v).view(np.uint32))
+
+
+@pytest.mark.parametrize("algo", ["nvls", "nccl"])
+def test_ipc_collective_setup_outcome_agrees(algo):
+    """cmn_set_algo(NVLS | NCCL) with 2 processes: both ranks end with the
+    same status (on the one-GPU boxes: multicast refused / NCCL refusing two
+    ranks on one device), and neither blocks."""
+    res = _run(2, "fp32", algo, mode="setup_alt")
+    assert len({r[1:] for r in res}) == 1, res
 
 
 def test_ipc_reregistration(orc):

@@ -244,6 +244,47 @@ def test_r50_full_size_n8_simulated(cmn, orc, dtype, algo):
     compare(gpu, ora, N)
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("N,dtype,algo", [(2, "fp32", "oneshot"), (3, "fp16", "twoshot")])
+def test_max_size_buffer_sampled(cmn, orc, N, dtype, algo):
+    """The largest buffer of the config-5 sweep (1 GiB of fp32, one tensor of
+    2^28 + 37 elements: ragged tail, pad, uneven two-shot chunks), allreduce
+    + update at N simulated workers.  Every step of the method after the
+    layout is elementwise, so the oracle run on a sample of element indices
+    (both ends, chunk boundaries, 2^18 random) gives exactly the expected
+    values there; the rest is checked to be finite and changed."""
+    n = (1 << 28) + 37
+    grads = [[synth.grad_tensor(n, 0, worker=i)] for i in range(N)]
+    w0 = synth.param_tensor(n, 0)
+    starts, ends = cmn.plan_chunks(-(-n // 64) * 64, N)
+    rng = np.random.default_rng(5)
+    edges = np.concatenate([np.arange(0, 4096), np.arange(n - 4096, n)] +
+                           [np.arange(max(0, b - 64), min(n, b + 64)) for b in list(starts) + list(ends)])
+    idx = np.unique(np.concatenate([edges, rng.integers(0, n, 1 << 18)]))
+    comm = cmn.Comm.simulated_world(N)
+    try:
+        w = torch.from_numpy(w0).to(DEV)
+        comm.register_params([w])
+        comm.set_algo(algo)
+        gd = [[torch.from_numpy(gw[0]).to(DEV)] for gw in grads]
+        del grads[1:]
+        comm.allreduce_grads(gd, dtype)
+        comm.update_momentum_sgd(0.1, 0.9)
+        torch.cuda.synchronize()
+        del gd
+        got_w = w.cpu().numpy()
+        got_v = comm.momentum(0).cpu().numpy().reshape(-1)
+    finally:
+        comm.finalize()
+    gs = [[synth.grad_tensor(n, 0, worker=i)[idx].copy()] for i in range(N)]
+    ws, vs = [w0[idx].copy()], [np.zeros(len(idx), np.float32)]
+    orc.step(gs, ws, vs, 0.1, 0.9, dtype)
+    assert_bitwise(got_w[idx], ws[0], "w (sampled)")
+    assert_bitwise(got_v[idx], vs[0], "v (sampled)")
+    assert np.isfinite(got_w).all() and np.isfinite(got_v).all()
+    assert np.count_nonzero(got_v == 0) < n // 1000     # every element was updated
+
+
 @pytest.mark.parametrize("N,pieces,dtype", [(2, 2, "fp32"), (4, 3, "fp16"), (8, 4, "fp32"),
                                             (3, 7, "fp16"), (8, 16, "fp16")])
 def test_pipelined_step_parity(cmn, orc, N, pieces, dtype):
