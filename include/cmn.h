@@ -321,6 +321,18 @@ cmn_status cmn_set_fused_update(cmn_comm *comm, int on);
  * its peers). */
 cmn_status cmn_set_ctas(cmn_comm *comm, int collective_ctas, int update_ctas);
 
+/* cmn_set_kernel_timing -- on: bracket every launch of the step's dominant
+ * kernels (the all-reduce kernels -- one-shot / two-shot / NVLS / NCCL --,
+ * the reduce-scatter and fused all-gather+update kernels of the fused
+ * schedule, the N = 1 direct update) with CUDA events on the stream that
+ * launch runs on (internal streams included); launches being captured into
+ * a CUDA graph are not timed.  Setting it (on or off) clears the record.
+ * cmn_get_kernel_timing -- waits for the recorded launches, returns their
+ * summed device time (ms) and count, and clears the record.  Used by
+ * bench.py for the roofline of the dominant kernel. */
+cmn_status cmn_set_kernel_timing(cmn_comm *comm, int on);
+cmn_status cmn_get_kernel_timing(cmn_comm *comm, double *total_ms, int *count);
+
 /* cmn_set_timeout -- device spin-wait timeout in milliseconds (default
  * 30000). */
 cmn_status cmn_set_timeout(cmn_comm *comm, uint32_t timeout_ms);

@@ -50,6 +50,8 @@ SIGNATURES = [
     ("cmn_set_pipeline", C.c_int, [_P, C.c_int]),
     ("cmn_set_fused_update", C.c_int, [_P, C.c_int]),
     ("cmn_set_ctas", C.c_int, [_P, C.c_int, C.c_int]),
+    ("cmn_set_kernel_timing", C.c_int, [_P, C.c_int]),
+    ("cmn_get_kernel_timing", C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int)]),
     ("cmn_set_timeout", C.c_int, [_P, C.c_uint32]),
     ("cmn_get_momentum", C.c_int, [_P, C.c_int, _PP]),
     ("cmn_get_adam_state", C.c_int, [_P, C.c_int, _PP, _PP]),
@@ -349,6 +351,16 @@ class Comm:
 
     def set_ctas(self, collective_ctas: int = 0, update_ctas: int = 0):
         _check(lib().cmn_set_ctas(self._h, collective_ctas, update_ctas), "cmn_set_ctas")
+
+    def set_kernel_timing(self, on: bool):
+        _check(lib().cmn_set_kernel_timing(self._h, int(bool(on))), "cmn_set_kernel_timing")
+
+    def kernel_timing(self):
+        """(summed device ms, launch count) of the timed dominant-kernel launches
+        since the last call; clears the record."""
+        ms, n = C.c_double(), C.c_int()
+        _check(lib().cmn_get_kernel_timing(self._h, C.byref(ms), C.byref(n)), "cmn_get_kernel_timing")
+        return ms.value, n.value
 
     def set_timeout(self, ms: int):
         _check(lib().cmn_set_timeout(self._h, ms), "cmn_set_timeout")

@@ -165,6 +165,12 @@ struct cmn_comm {
     int upd_blocks = 0;           // cmn_set_ctas: barrier-gated update grid (0 = default)
     int *h_err = nullptr, *d_err = nullptr;
     uint64_t launches = 0;
+    // cmn_set_kernel_timing: CUDA events around every launch of the step's
+    // dominant kernels (all-reduce, fused all-gather+update, the N = 1
+    // direct update) on the stream each runs on; pairs [0, ktimed) in use.
+    bool ktiming = false;
+    std::vector<cudaEvent_t> kev;
+    size_t ktimed = 0;
     std::vector<std::pair<int, int>> buckets;   // [t_begin, t_end), reverse order
     std::vector<char> bucket_fresh;
     std::vector<ArResult> bucket_res;
@@ -199,6 +205,31 @@ cmn_status launched(cmn_comm *c, cudaError_t e, const char *what) {
     if (e != cudaSuccess) return cuda_fail(e, what);
     ++c->launches;
     return CMN_OK;
+}
+
+// Run `f` (kernel launches on stream s) between two timing events when
+// kernel timing is on and s is not being captured into a graph.
+template <typename F>
+cmn_status timed(cmn_comm *c, cudaStream_t s, F &&f) {
+    bool on = c->ktiming;
+    if (on) {
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        on = cudaStreamIsCapturing(s, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusNone;
+    }
+    if (on) {
+        while (c->kev.size() < 2 * (c->ktimed + 1)) {
+            cudaEvent_t e;
+            CMN_CUDA(cudaEventCreate(&e));
+            c->kev.push_back(e);
+        }
+        CMN_CUDA(cudaEventRecord(c->kev[2 * c->ktimed], s));
+    }
+    const cmn_status st = f();
+    if (on && st == CMN_OK) {
+        CMN_CUDA(cudaEventRecord(c->kev[2 * c->ktimed + 1], s));
+        ++c->ktimed;
+    }
+    return st;
 }
 
 void free_regions(cmn_comm *c) {
@@ -446,8 +477,8 @@ cmn_status pack_phase(cmn_comm *c, int ta, int tb, const float *const *grads, in
 
 // a2 over the packed range of tensors [ta, tb) for the collective call with
 // sequence number `seq` (its buffers have parity seq & 1).
-cmn_status reduce_phase(cmn_comm *c, int ta, int tb, int dtype, uint32_t seq, cmn_algo algo,
-                        cudaStream_t s) {
+cmn_status reduce_phase_launch(cmn_comm *c, int ta, int tb, int dtype, uint32_t seq, cmn_algo algo,
+                               cudaStream_t s) {
     const int par = static_cast<int>(seq & 1u);
     const int64_t e0 = c->off[ta], e1 = c->off[tb];
     const size_t esz = dtype == 0 ? 4 : 2;
@@ -512,6 +543,12 @@ cmn_status reduce_phase(cmn_comm *c, int ta, int tb, int dtype, uint32_t seq, cm
                     launch_allreduce_twoshot(in, red, c->world, c->rank, cs, ce, dtype, 3, bar,
                                              blocks, s),
                     "allreduce_twoshot");
+}
+
+cmn_status reduce_phase(cmn_comm *c, int ta, int tb, int dtype, uint32_t seq, cmn_algo algo,
+                        cudaStream_t s) {
+    if (c->world == 1 && algo != CMN_ALGO_NCCL && algo != CMN_ALGO_NVLS) return CMN_OK;
+    return timed(c, s, [&] { return reduce_phase_launch(c, ta, tb, dtype, seq, algo, s); });
 }
 
 // Validate and choose the algorithm for one collective over [ta, tb).
@@ -884,24 +921,30 @@ cmn_status step_fused(cmn_comm *c, const float *const *grads, int dtype, float l
     chunk_plan(0, c->L, c->world, cs, ce);
     const int blocks = ar_blocks_for(c);
     const Barrier bar = make_barrier(c, dtype | 2);
-    for (int i = 0; i < nsim; ++i) {
-        const int r = c->simulated ? i : c->rank;
-        cmn_status st = launched(c,
-                                 launch_allreduce_twoshot(in, red, c->world, r, cs, ce, dtype, 1, bar,
-                                                          blocks, s),
-                                 "reduce_scatter");
-        if (st != CMN_OK) return st;
-    }
+    cmn_status st = timed(c, s, [&] {
+        for (int i = 0; i < nsim; ++i) {
+            const int r = c->simulated ? i : c->rank;
+            cmn_status st2 = launched(c,
+                                      launch_allreduce_twoshot(in, red, c->world, r, cs, ce, dtype, 1,
+                                                               bar, blocks, s),
+                                      "reduce_scatter");
+            if (st2 != CMN_OK) return st2;
+        }
+        return CMN_OK;
+    });
+    if (st != CMN_OK) return st;
     ++c->seq;
     const Barrier bar2 = make_barrier(c, dtype);
     const int total = c->sitem_begin[c->world];
     const int gblocks = upd_blocks_for(c, total);
     // simulated ranks share one parameter replica: one launch updates it all
-    cmn_status st = launched(c,
-                             launch_update_gather(c->d_td, c->d_sitems, 0, total, red, c->world, dtype,
-                                                  1.0f / static_cast<float>(c->world), lr, mu, bar2,
-                                                  gblocks, s),
-                             "update_gather");
+    st = timed(c, s, [&] {
+        return launched(c,
+                        launch_update_gather(c->d_td, c->d_sitems, 0, total, red, c->world, dtype,
+                                             1.0f / static_cast<float>(c->world), lr, mu, bar2,
+                                             gblocks, s),
+                        "update_gather");
+    });
     if (st != CMN_OK) return st;
     c->fresh = false;
     return CMN_OK;
@@ -940,6 +983,7 @@ cmn_status cmn_finalize(cmn_comm *c) {
     if (c->nccl && g_nccl.CommDestroy) g_nccl.CommDestroy(c->nccl);
     for (auto e : c->ev) cudaEventDestroy(e);
     for (auto e : c->pev) cudaEventDestroy(e);
+    for (auto e : c->kev) cudaEventDestroy(e);
     if (c->sc) cudaStreamDestroy(c->sc);
     if (c->h2d) cudaStreamDestroy(c->h2d);
     if (c->d2h) cudaStreamDestroy(c->d2h);
@@ -1145,11 +1189,13 @@ cmn_status cmn_step(cmn_comm *c, const float *const *grads, cmn_dtype dtype, flo
     if (cmn_status st = set_device(c); st != CMN_OK) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     c->fresh = false;
-    return for_groups(c, 0, c->T, [&](int lo, int hi, int i0, int i1) {
-        return launched(c,
-                        launch_update_direct(make_tab(grads, lo, hi), lo, c->d_td, c->d_items, i0,
-                                             i1, dtype, lr, mu, s),
-                        "update_direct");
+    return timed(c, s, [&] {
+        return for_groups(c, 0, c->T, [&](int lo, int hi, int i0, int i1) {
+            return launched(c,
+                            launch_update_direct(make_tab(grads, lo, hi), lo, c->d_td, c->d_items,
+                                                 i0, i1, dtype, lr, mu, s),
+                            "update_direct");
+        });
     });
 }
 
@@ -1488,6 +1534,28 @@ cmn_status cmn_set_ctas(cmn_comm *c, int collective_ctas, int update_ctas) {
         return fail(CMN_ERR_INVALID_ARG, "CTA counts must be in [0, 1024] (0 = default)");
     c->ar_blocks = collective_ctas;
     c->upd_blocks = update_ctas;
+    return CMN_OK;
+}
+
+cmn_status cmn_set_kernel_timing(cmn_comm *c, int on) {
+    if (!c) return fail(CMN_ERR_INVALID_ARG, "comm is NULL");
+    c->ktiming = on != 0;
+    c->ktimed = 0;
+    return CMN_OK;
+}
+
+cmn_status cmn_get_kernel_timing(cmn_comm *c, double *total_ms, int *count) {
+    if (!c || !total_ms || !count) return fail(CMN_ERR_INVALID_ARG, "NULL argument");
+    double sum = 0.0;
+    for (size_t i = 0; i < c->ktimed; ++i) {
+        CMN_CUDA(cudaEventSynchronize(c->kev[2 * i + 1]));
+        float ms = 0.f;
+        CMN_CUDA(cudaEventElapsedTime(&ms, c->kev[2 * i], c->kev[2 * i + 1]));
+        sum += ms;
+    }
+    *total_ms = sum;
+    *count = static_cast<int>(c->ktimed);
+    c->ktimed = 0;
     return CMN_OK;
 }
 

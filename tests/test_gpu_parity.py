@@ -712,3 +712,44 @@ def test_launch_count(cmn):
         assert comm.kernel_launches - before == 1      # one fused kernel at N = 1
     finally:
         comm.finalize()
+
+
+def test_kernel_timing(cmn):
+    """cmn_set_kernel_timing brackets each dominant-kernel launch: one per
+    N = 1 step, one per piece of the pipelined schedule (internal stream),
+    two per fused step; nothing while capturing a graph; results unchanged."""
+    shapes = synth.resnet50_shapes()[:40]
+    comm = cmn.Comm.init(0, 1, 0)
+    try:
+        comm.register_params(to_dev(synth.params(shapes)))
+        g = to_dev(synth.grads(shapes, workers=1)[0])
+        comm.set_kernel_timing(True)
+        for _ in range(3):
+            comm.step(g, "fp32", 0.1, 0.9)
+        ms, n = comm.kernel_timing()
+        assert n == 3 and ms > 0
+        s2 = torch.cuda.Stream()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s2):
+            comm.step(g, "fp32", 0.1, 0.9)
+        graph.replay()
+        torch.cuda.synchronize()
+        assert comm.kernel_timing() == (0.0, 0)
+        comm.set_kernel_timing(False)
+        comm.step(g, "fp32", 0.1, 0.9)
+        assert comm.kernel_timing() == (0.0, 0)
+    finally:
+        comm.finalize()
+    comm = cmn.Comm.simulated_world(4)
+    try:
+        comm.register_params(to_dev(synth.params(shapes)))
+        gs = [to_dev(gw) for gw in synth.grads(shapes, workers=4)]
+        comm.set_pipeline(3)
+        comm.set_kernel_timing(True)
+        comm.step(gs, "fp16", 0.1, 0.9)
+        assert comm.kernel_timing()[1] == 3
+        comm.set_fused_update(True)
+        comm.step(gs, "fp16", 0.1, 0.9)
+        assert comm.kernel_timing()[1] == 2
+    finally:
+        comm.finalize()
