@@ -469,7 +469,10 @@ def main():
                "d2h_bytes_per_step": 4 * L,
                "path": "cmn_step_host_packed: pinned host grads (packed layout) -> device, "
                        "step, params -> pinned host" + ("; pipelined over 12 ramped item ranges at N=1"
-                                                         if world == 1 else "")}
+                                                         if world == 1 else
+                                                         "; H2D/D2H per piece inside the pipelined "
+                                                         "schedule" if schedule.startswith("pipelined")
+                                                         else "; copies around the step")}
 
     comm.finalize()
     if rank != 0:

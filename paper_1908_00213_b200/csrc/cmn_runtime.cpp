@@ -798,11 +798,46 @@ cmn_status ensure_comm_stream(cmn_comm *c, size_t n_events) {
 // Buffer reuse is safe for P >= 2: a piece's next pack (seq + P) is issued
 // after update(P-1), i.e. after our all-reduce at seq + P - 1 passed its
 // start barrier, so every peer finished all-reduce calls <= seq + P - 2.
+// Host buffers of the e2e step (cmn_step_host_packed): packed layout, L
+// floats per (simulated) rank for the gradients; parameters out or NULL.
+struct HostIO {
+    const float *grads = nullptr;
+    float *params = nullptr;
+};
+
+// Device->host copy of the parameters of tensors [ta, tb) into the packed
+// host layout: one copy when the params are one flat allocation (stopping
+// at the last tensor's end), else one per tensor.
+cmn_status d2h_params(cmn_comm *c, int ta, int tb, float *host_params, cudaStream_t s) {
+    if (c->params_flat) {
+        int last = c->T - 1;
+        while (last > 0 && c->numel[last] == 0) --last;
+        const int64_t flat_end = c->off[last] + c->numel[last];
+        const int64_t e0 = c->off[ta], e1 = c->off[tb] < flat_end ? c->off[tb] : flat_end;
+        if (e1 > e0)
+            CMN_CUDA(cudaMemcpyAsync(host_params + e0, c->params[0] + e0, static_cast<size_t>(e1 - e0) * 4,
+                                     cudaMemcpyDeviceToHost, s));
+        return CMN_OK;
+    }
+    std::vector<float *> hp(c->T);
+    for (int t = 0; t < c->T; ++t) hp[t] = host_params + c->off[t];
+    std::vector<const float *> src(c->params.begin(), c->params.end());
+    return copy_tensors(c, src.data(), hp.data(), ta, tb, cudaMemcpyDeviceToHost, s);
+}
+
+// With `io`, the e2e form: H2D(piece p) on a copy stream feeds pack(p), and
+// D2H(piece p) on a second copy stream follows update(p), so PCIe in both
+// directions overlaps the packs, NVLink all-reduces and updates of the
+// other pieces (gradients land in the library's staging buffer, whose
+// pointers `grads` are).
 cmn_status step_pipelined(cmn_comm *c, const float *const *grads, int dtype, float lr, float mu,
-                          cudaStream_t s) {
+                          cudaStream_t s, const HostIO *io = nullptr) {
     const auto pieces = equal_ranges(c, c->pipe_pieces);
     const size_t P = pieces.size();
     if (cmn_status st = ensure_comm_stream(c, 2 * P + 1); st != CMN_OK) return st;
+    if (io)
+        if (cmn_status st = ensure_side_streams(c); st != CMN_OK) return st;
+    const int nsim = c->simulated ? c->world : 1;
     std::vector<cmn_algo> algo(P);
     for (size_t p = 0; p < P; ++p)
         if (cmn_status st = begin_collective(c, pieces[p].first, pieces[p].second, dtype, algo[p], s,
@@ -812,11 +847,26 @@ cmn_status step_pipelined(cmn_comm *c, const float *const *grads, int dtype, flo
     cudaEvent_t entry = c->pev[2 * P];
     CMN_CUDA(cudaEventRecord(entry, s));
     CMN_CUDA(cudaStreamWaitEvent(c->sc, entry, 0));
+    if (io) {
+        CMN_CUDA(cudaStreamWaitEvent(c->h2d, entry, 0));
+        CMN_CUDA(cudaStreamWaitEvent(c->d2h, entry, 0));
+    }
     std::vector<ArResult> res(P);
     for (size_t p = 0; p < P; ++p) {
         const uint32_t seq = ++c->seq;
         const int par = static_cast<int>(seq & 1u);
         res[p] = ArResult{par, dtype, false};
+        if (io) {
+            const int64_t e0 = c->off[pieces[p].first], e1 = c->off[pieces[p].second];
+            for (int i = 0; i < nsim; ++i) {
+                const size_t base = static_cast<size_t>(i) * c->L;
+                CMN_CUDA(cudaMemcpyAsync(c->d_staging + base + e0, io->grads + base + e0,
+                                         static_cast<size_t>(e1 - e0) * 4, cudaMemcpyHostToDevice,
+                                         c->h2d));
+            }
+            CMN_CUDA(cudaEventRecord(c->ev[2 + 3 * p], c->h2d));
+            CMN_CUDA(cudaStreamWaitEvent(s, c->ev[2 + 3 * p], 0));
+        }
         if (cmn_status st = pack_phase(c, pieces[p].first, pieces[p].second, grads, dtype, par, s);
             st != CMN_OK)
             return st;
@@ -833,6 +883,17 @@ cmn_status step_pipelined(cmn_comm *c, const float *const *grads, int dtype, flo
         if (cmn_status st = update_range(c, pieces[p].first, pieces[p].second, res[p], lr, mu, s);
             st != CMN_OK)
             return st;
+        if (io && io->params) {
+            CMN_CUDA(cudaEventRecord(c->ev[3 + 3 * p], s));
+            CMN_CUDA(cudaStreamWaitEvent(c->d2h, c->ev[3 + 3 * p], 0));
+            if (cmn_status st = d2h_params(c, pieces[p].first, pieces[p].second, io->params, c->d2h);
+                st != CMN_OK)
+                return st;
+        }
+    }
+    if (io) {
+        CMN_CUDA(cudaEventRecord(c->ev[1], c->d2h));
+        CMN_CUDA(cudaStreamWaitEvent(s, c->ev[1], 0));
     }
     c->last = res[P - 1];
     c->fresh = false;
@@ -1263,28 +1324,17 @@ cmn_status cmn_step_host_packed(cmn_comm *c, const float *host_grads, float *hos
     if (!grads_ok(c, dg.data(), nsim * c->T, why)) return fail(CMN_ERR_INVALID_ARG, why);
 
     if (c->world > 1 || c->simulated) {
-        // Unpipelined: the all-reduce needs every gradient first.
+        // The pipelined schedule carries the host copies piece by piece.
+        if (c->world > 1 && c->pipe_pieces >= 2 && c->T >= 2 && !c->fused_update && c->algo != CMN_ALGO_NVLS &&
+            c->algo != CMN_ALGO_NCCL) {
+            const HostIO io{host_grads, host_params};
+            return step_pipelined(c, dg.data(), dtype, lr, mu, s, &io);
+        }
+        // Other schedules: the all-reduce needs every gradient first.
         CMN_CUDA(cudaMemcpyAsync(c->d_staging, host_grads, static_cast<size_t>(c->L) * 4 * nsim,
                                  cudaMemcpyHostToDevice, s));
         if (cmn_status st = cmn_step(c, dg.data(), dtype, lr, mu, stream); st != CMN_OK) return st;
-        if (host_params) {
-            if (c->params_flat) {
-                int last = c->T - 1;          // the allocation may end at the last tensor
-                while (last > 0 && c->numel[last] == 0) --last;
-                CMN_CUDA(cudaMemcpyAsync(host_params, c->params[0],
-                                         static_cast<size_t>(c->off[last] + c->numel[last]) * 4,
-                                         cudaMemcpyDeviceToHost, s));
-            } else {
-                std::vector<float *> hp(c->T);
-                for (int t = 0; t < c->T; ++t) hp[t] = host_params + c->off[t];
-                std::vector<const float *> src(c->params.begin(), c->params.end());
-                if (cmn_status st = copy_tensors(c, src.data(), hp.data(), 0, c->T,
-                                                 cudaMemcpyDeviceToHost, s);
-                    st != CMN_OK)
-                    return st;
-            }
-        }
-        return CMN_OK;
+        return host_params ? d2h_params(c, 0, c->T, host_params, s) : CMN_OK;
     }
 
     // N = 1: pipeline H2D(piece p+1) || update(piece p) || D2H(piece p-1) on

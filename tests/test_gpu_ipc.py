@@ -96,7 +96,21 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode, pieces=0):
                 continue                              # fault injection: rank 1 skips a collective
             if mode == "reregister" and s == 1:
                 comm.register_params(w)               # collective; resets momentum (reading R7)
-            if mode == "mixed":
+            if mode == "host":
+                # e2e form through pinned host buffers (pipelined: H2D/D2H per piece)
+                sizes = [x.numel() for x in w]
+                off, L = cmn.plan_layout(shapes)[:2]
+                hg = torch.zeros(L, dtype=torch.float32).pin_memory()
+                for t, x in enumerate(g):
+                    hg[off[t]: off[t] + sizes[t]].copy_(x.reshape(-1).cpu())
+                hw = torch.full((L,), float("nan"), dtype=torch.float32).pin_memory()
+                comm.step_host_packed(hg, hw, dtype, 0.1, 0.9)
+                torch.cuda.synchronize()
+                for t, x in enumerate(w):
+                    if not torch.equal(hw[off[t]: off[t] + sizes[t]].view(torch.int32),
+                                       x.reshape(-1).cpu().view(torch.int32)):
+                        raise RuntimeError(f"host params of tensor {t} differ from device params")
+            elif mode == "mixed":
                 # the schedule and the grid sizes change every step, identically
                 # on every rank: per-CTA barrier epochs must stay paired
                 fused, pcs, ctas = [(True, 0, (5, 3)), (False, 2, (9, 0)),
@@ -224,6 +238,23 @@ def test_ipc_single_call_schedule_refuses_capture():
 @pytest.mark.parametrize("world,dtype", [(2, "fp16"), (3, "fp32")])
 def test_ipc_fused_allgather_update(orc, world, dtype):
     res = _run(world, dtype, "twoshot", mode="fused")
+    assert all(r[1] == "ok" for r in res), res
+    shapes = synth.mlp_shapes()
+    w = synth.params(shapes)
+    v = [np.zeros_like(x) for x in w]
+    for s in range(2):
+        orc.step(synth.grads(shapes, workers=world, step=s), w, v, 0.1, 0.9, dtype)
+    for r in res:
+        assert np.array_equal(np.frombuffer(r[2], np.uint32), np.concatenate(w).view(np.uint32))
+        assert np.array_equal(np.frombuffer(r[3], np.uint32), np.concatenate(v).view(np.uint32))
+
+
+@pytest.mark.parametrize("world,dtype,pieces", [(2, "fp32", 3), (3, "fp16", 0)])
+def test_ipc_step_host_packed(orc, world, dtype, pieces):
+    """cmn_step_host_packed across processes: pinned host gradients in,
+    host parameters out (pipelined per piece, or around a serial step);
+    bit-exact with the oracle on every rank, host copy == device params."""
+    res = _run(world, dtype, "twoshot", mode="host", pieces=pieces)
     assert all(r[1] == "ok" for r in res), res
     shapes = synth.mlp_shapes()
     w = synth.params(shapes)

@@ -506,29 +506,44 @@ def test_step_host_packed_pageable_params(cmn, orc):
         comm.finalize()
 
 
-def test_step_host_packed_simulated(cmn, orc):
-    shapes = synth.mlp_shapes()
-    N = 4
+@pytest.mark.parametrize("N,sched,flat,dtype", [(4, "pipelined", False, "fp32"), (3, "pipelined", True, "fp16"),
+                                               (2, "serial", True, "fp32"), (8, "fused", False, "fp16"),
+                                               (4, "pipelined7", True, "fp32")])
+def test_step_host_packed_simulated(cmn, orc, N, sched, flat, dtype):
+    """cmn_step_host_packed at N > 1 (simulated ranks), 3 steps: with the
+    pipelined schedule the H2D of each piece feeds its pack and the D2H of
+    its parameters follows its update on two copy streams; other schedules
+    copy everything around the step.  Bit-exact with the oracle."""
+    shapes = synth.resnet50_shapes()[:24] + RAGGED
     sizes = [synth.numel(s) for s in shapes]
     off, L = orc.layout(sizes)
-    g = synth.grads(shapes, workers=N)
     params0 = synth.params(shapes)
     w_o = [p.copy() for p in params0]
     v_o = [np.zeros_like(p) for p in params0]
-    orc.step(g, w_o, v_o, 0.1, 0.9, "fp32")
     comm = cmn.Comm.simulated_world(N)
     try:
-        w = to_dev(params0)
+        if flat:
+            buf = torch.zeros(off[len(sizes) - 1] + sizes[-1], dtype=torch.float32, device=DEV)
+            w = [buf[off[t]: off[t] + sizes[t]].view(shapes[t]) for t in range(len(shapes))]
+            for t in range(len(w)):
+                w[t].copy_(torch.from_numpy(params0[t]).view(shapes[t]))
+        else:
+            w = to_dev(params0)
         comm.register_params(w)
+        comm.set_fused_update(sched == "fused")
+        comm.set_pipeline(0 if sched in ("serial", "fused") else int(sched[9:] or 4))
         hg = torch.zeros(N * L, dtype=torch.float32).pin_memory()
-        for i in range(N):
+        hw = torch.full((L,), float("nan"), dtype=torch.float32).pin_memory()
+        for step in range(3):
+            g = synth.grads(shapes, workers=N, step=step)
+            for i in range(N):
+                for t in range(len(sizes)):
+                    hg[i * L + off[t]: i * L + off[t] + sizes[t]].copy_(torch.from_numpy(g[i][t]))
+            orc.step(g, w_o, v_o, 0.1, 0.9, dtype)
+            comm.step_host_packed(hg, hw, dtype, 0.1, 0.9)
+            torch.cuda.synchronize()
             for t in range(len(sizes)):
-                hg[i * L + off[t]: i * L + off[t] + sizes[t]].copy_(torch.from_numpy(g[i][t]))
-        hw = torch.empty(L, dtype=torch.float32).pin_memory()
-        comm.step_host_packed(hg, hw, "fp32", 0.1, 0.9)
-        torch.cuda.synchronize()
-        for t in range(len(sizes)):
-            assert_bitwise(hw.numpy()[off[t]: off[t] + sizes[t]].copy(), w_o[t], f"w[{t}]")
+                assert_bitwise(hw.numpy()[off[t]: off[t] + sizes[t]].copy(), w_o[t], f"w[{t}] step {step}")
     finally:
         comm.finalize()
 
