@@ -131,6 +131,21 @@ def main():
                 else:
                     # simulated: N packs + N (oneshot) or 2N (twoshot) launches, all local HBM
                     rec["sim_note"] = "all N ranks' kernels on one GPU; local HBM stands in for NVLink"
+                    if algo == "twoshot":
+                        # whole-step schedules: in simulation every rank's pack and
+                        # all-reduce kernels run on this one GPU from local HBM, while
+                        # the simulated ranks' shared parameter replica is updated once
+                        # -- mechanics and local-memory cost, not an N-GPU time
+                        sched = {}
+                        for name, fused, pieces in (("serial", False, 0), ("pipelined4", False, 4),
+                                                    ("fused", True, 0)):
+                            comm.set_fused_update(fused)
+                            comm.set_pipeline(pieces)
+                            sched[name] = timed(lambda: comm.step(gg, dtype, 0.1, 0.9), args.iters, stream)
+                        comm.set_fused_update(False)
+                        sched["sharded"] = timed(lambda: comm.step_sharded(gg, dtype, 0.1, 0.9),
+                                                 args.iters, stream)
+                        rec["sim_step_us"] = sched
                 print(json.dumps(rec), flush=True)
                 comm.finalize()
                 del w

@@ -17,13 +17,13 @@ from paper_1908_00213_b200 import Comm  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--mode", default="n1", choices=["n1", "sim8", "adam"])
+    ap.add_argument("--mode", default="n1", choices=["n1", "sim8", "adam", "fused8", "sharded8"])
     ap.add_argument("--dtype", default="fp32")
     ap.add_argument("--algo", default="twoshot")
     ap.add_argument("--iters", type=int, default=3)
     a = ap.parse_args()
     shapes = synth.resnet50_shapes()
-    N = 8 if a.mode == "sim8" else 1
+    N = 8 if a.mode.endswith("8") else 1
     comm = Comm.init(0, 1, 0) if N == 1 else Comm.simulated_world(N)
     w = [torch.from_numpy(p).cuda() for p in synth.params(shapes)]
     comm.register_params(w)
@@ -33,7 +33,14 @@ def main():
     g = synth.grads(shapes, workers=N)
     gt = comm.prepare([[torch.from_numpy(x).cuda() for x in gw] for gw in g] if N > 1
                       else [torch.from_numpy(x).cuda() for x in g[0]])
-    for _ in range(a.iters if a.mode != "adam" else 0):
+    if a.mode == "fused8":
+        comm.set_fused_update(True)
+    for _ in range(a.iters if a.mode in ("fused8", "sharded8") else 0):
+        if a.mode == "fused8":
+            comm.step(gt, a.dtype, 0.1, 0.9)
+        else:
+            comm.step_sharded(gt, a.dtype, 0.1, 0.9)
+    for _ in range(a.iters if a.mode in ("n1", "sim8") else 0):
         comm.allreduce_grads(gt, a.dtype)
         comm.update_momentum_sgd(0.1, 0.9)
         if N == 1:
