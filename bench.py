@@ -297,12 +297,11 @@ def main():
 
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
 
-    def set_schedule(name):
-        if name == "nvls":              # in-switch all-reduce, serial step
-            comm.set_algo("nvls")
-            name = "serial"
-        elif world > 1:
-            comm.set_algo(args.algo)
+    def set_schedule(name, algo=None):
+        if name.startswith("nvls"):     # in-switch all-reduce: "nvls" (serial), "nvls_pipelined4"
+            algo, name = "nvls", name[5:] or "serial"
+        if world > 1:
+            comm.set_algo(algo or args.algo)
         fused, pieces, ar_x, upd_x = SCHEDULES[name]
         comm.set_fused_update(fused)
         comm.set_pipeline(pieces)
@@ -377,15 +376,17 @@ def main():
             except CmnError as e:
                 comparisons[alt] = {"unavailable": str(e)[:160]}
                 continue
-            set_schedule("serial")
-            comm.set_algo(alt)
-            comparisons[alt] = {"step_us": trial_us()}
+            comparisons[alt] = {}
+            for sched in ("serial", "pipelined4"):
+                set_schedule(sched, alt)
+                comparisons[alt][f"{sched}_step_us"] = trial_us()
             if alt == "nvls" and args.schedule == "auto":
                 ratio = nvls_check()
                 comparisons[alt]["tolerance_ratio_vs_tree"] = ratio
                 if ratio <= 1.0:
-                    set_schedule("nvls")
-                    trials["nvls"] = trial_us()
+                    for name in ("nvls", "nvls_pipelined4"):
+                        set_schedule(name)
+                        trials[name] = trial_us()
         schedule = min(trials, key=trials.get)
         set_schedule(schedule)
 
@@ -554,7 +555,7 @@ def main():
         bus_bytes = 2 * (world - 1) / world * S
         bus = bus_bytes / (ms * 1e-3) / 1e9
         kernel = ("k_twoshot (reduce-scatter) + k_update_gather" if schedule.startswith("fused")
-                  else "k_nvls (multimem.ld_reduce / multimem.st)" if schedule == "nvls"
+                  else "k_nvls (multimem.ld_reduce / multimem.st)" if schedule.startswith("nvls")
                   else "k_oneshot / k_twoshot all-reduce")
         roof = {"bound": "nvlink", "kernel": kernel,
                 "achieved": bus_bytes / (kernel_ms_per_step * 1e-3) / 1e9,

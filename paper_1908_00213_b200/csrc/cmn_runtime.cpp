@@ -851,11 +851,15 @@ cmn_status step_pipelined(cmn_comm *c, const float *const *grads, int dtype, flo
         CMN_CUDA(cudaStreamWaitEvent(c->h2d, entry, 0));
         CMN_CUDA(cudaStreamWaitEvent(c->d2h, entry, 0));
     }
+    // NVLS: one multicast buffer pair; a piece's region is reused only after
+    // its previous all-reduce passed its end barrier (same ordering argument
+    // as above), so no parity alternation is needed.
+    const bool nvls = c->algo == CMN_ALGO_NVLS;
     std::vector<ArResult> res(P);
     for (size_t p = 0; p < P; ++p) {
         const uint32_t seq = ++c->seq;
         const int par = static_cast<int>(seq & 1u);
-        res[p] = ArResult{par, dtype, false};
+        res[p] = ArResult{par, dtype, false, nvls};
         if (io) {
             const int64_t e0 = c->off[pieces[p].first], e1 = c->off[pieces[p].second];
             for (int i = 0; i < nsim; ++i) {
@@ -867,7 +871,8 @@ cmn_status step_pipelined(cmn_comm *c, const float *const *grads, int dtype, flo
             CMN_CUDA(cudaEventRecord(c->ev[2 + 3 * p], c->h2d));
             CMN_CUDA(cudaStreamWaitEvent(s, c->ev[2 + 3 * p], 0));
         }
-        if (cmn_status st = pack_phase(c, pieces[p].first, pieces[p].second, grads, dtype, par, s);
+        if (cmn_status st = pack_phase(c, pieces[p].first, pieces[p].second, grads, dtype, par, s,
+                                       nvls ? c->nvls.packed_uc() : nullptr);
             st != CMN_OK)
             return st;
         CMN_CUDA(cudaEventRecord(c->pev[2 * p], s));
@@ -1222,7 +1227,10 @@ cmn_status cmn_step(cmn_comm *c, const float *const *grads, cmn_dtype dtype, flo
     if (cmn_status st = require_registered(c); st != CMN_OK) return st;
     if (cmn_status st = require_dtype(dtype); st != CMN_OK) return st;
     if (c->world > 1 || c->algo == CMN_ALGO_NVLS) {
-        if (c->algo == CMN_ALGO_NVLS || c->algo == CMN_ALGO_NCCL) {
+        const bool lib_collective = c->algo == CMN_ALGO_NVLS || c->algo == CMN_ALGO_NCCL;
+        if (lib_collective && (c->world == 1 || c->fused_update || c->pipe_pieces < 2)) {
+            // single-rank plumbing, or a schedule that needs the two-shot
+            // reduce-scatter: serial step
             cmn_status st = cmn_allreduce_grads(c, grads, dtype, stream);
             if (st != CMN_OK) return st;
             return cmn_update_momentum_sgd(c, lr, mu, stream);
@@ -1325,8 +1333,7 @@ cmn_status cmn_step_host_packed(cmn_comm *c, const float *host_grads, float *hos
 
     if (c->world > 1 || c->simulated) {
         // The pipelined schedule carries the host copies piece by piece.
-        if (c->world > 1 && c->pipe_pieces >= 2 && c->T >= 2 && !c->fused_update && c->algo != CMN_ALGO_NVLS &&
-            c->algo != CMN_ALGO_NCCL) {
+        if (c->world > 1 && c->pipe_pieces >= 2 && c->T >= 2 && !c->fused_update) {
             const HostIO io{host_grads, host_params};
             return step_pipelined(c, dg.data(), dtype, lr, mu, s, &io);
         }
