@@ -43,6 +43,7 @@ SCHEDULES = {
     "fused": (True, 0, 0, 0),
     "fused_2cta": (True, 0, 2, 2),
     "serial": (False, 0, 0, 0),
+    "serial_2cta": (False, 0, 2, 0),
 }
 
 
@@ -298,7 +299,7 @@ def main():
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
 
     def set_schedule(name, algo=None):
-        if name.startswith("nvls"):     # in-switch all-reduce: "nvls" (serial), "nvls_pipelined4"
+        if name.startswith("nvls"):     # in-switch all-reduce: "nvls" (serial), "nvls_<schedule>"
             algo, name = "nvls", name[5:] or "serial"
         if world > 1:
             comm.set_algo(algo or args.algo)
@@ -384,7 +385,7 @@ def main():
                 ratio = nvls_check()
                 comparisons[alt]["tolerance_ratio_vs_tree"] = ratio
                 if ratio <= 1.0:
-                    for name in ("nvls", "nvls_pipelined4"):
+                    for name in ("nvls", "nvls_serial_2cta", "nvls_pipelined4", "nvls_pipelined4_2cta"):
                         set_schedule(name)
                         trials[name] = trial_us()
         schedule = min(trials, key=trials.get)
