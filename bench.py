@@ -33,17 +33,20 @@ sys.path.insert(0, ROOT)
 METRIC = "allreduce+update step µs and bus GB/s (ResNet-50 grads) at 1/2/4/8 B200 vs roofline"
 FALLBACK_HBM_GBS = 6650.0
 
-# N > 1 step schedules: name -> (fused all-gather+update, pipeline pieces,
-# all-reduce CTAs per SM, update CTAs per SM; 0 = library default).
+# N > 1 step schedules: name -> (fused-update mode: 0 off, 1 pull RS, 2 push
+# pack+RS; pipeline pieces; all-reduce CTAs per SM; update CTAs per SM;
+# 0 = library default).
 SCHEDULES = {
-    "pipelined2": (False, 2, 0, 0),
-    "pipelined4": (False, 4, 0, 0),
-    "pipelined8": (False, 8, 0, 0),
-    "pipelined4_2cta": (False, 4, 2, 0),
-    "fused": (True, 0, 0, 0),
-    "fused_2cta": (True, 0, 2, 2),
-    "serial": (False, 0, 0, 0),
-    "serial_2cta": (False, 0, 2, 0),
+    "pipelined2": (0, 2, 0, 0),
+    "pipelined4": (0, 4, 0, 0),
+    "pipelined8": (0, 8, 0, 0),
+    "pipelined4_2cta": (0, 4, 2, 0),
+    "fused": (1, 0, 0, 0),
+    "fused_2cta": (1, 0, 2, 2),
+    "fused_push": (2, 0, 0, 0),
+    "fused_push_2cta": (2, 0, 2, 2),
+    "serial": (0, 0, 0, 0),
+    "serial_2cta": (0, 0, 2, 0),
 }
 
 
@@ -555,7 +558,9 @@ def main():
         S = csz * P
         bus_bytes = 2 * (world - 1) / world * S
         bus = bus_bytes / (ms * 1e-3) / 1e9
-        kernel = ("k_twoshot (reduce-scatter) + k_update_gather" if schedule.startswith("fused")
+        kernel = ("k_pack_push + k_twoshot (local inbox reduce) + k_update_gather"
+                  if schedule.startswith("fused_push")
+                  else "k_twoshot (reduce-scatter) + k_update_gather" if schedule.startswith("fused")
                   else "k_nvls (multimem.ld_reduce / multimem.st)" if schedule.startswith("nvls")
                   else "k_oneshot / k_twoshot all-reduce")
         roof = {"bound": "nvlink", "kernel": kernel,

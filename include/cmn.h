@@ -303,12 +303,21 @@ cmn_status cmn_set_algo(cmn_comm *comm, cmn_algo algo, size_t oneshot_max_bytes)
 cmn_status cmn_set_pipeline(cmn_comm *comm, int pieces);
 
 /* cmn_set_fused_update -- N > 1 cmn_step schedule (takes precedence over
- * the pipeline when on): pack -> reduce-scatter -> ONE kernel that updates
- * every parameter reading each reduced chunk directly from its owner rank
- * over NVLink (no all-gather copy through local HBM).  Bitwise identical to
- * the other schedules; graph-capturable.  Every rank must use the same
- * setting.  Default off. */
-cmn_status cmn_set_fused_update(cmn_comm *comm, int on);
+ * the pipeline when on), `mode`:
+ *   0  off (default)
+ *   1  pack -> reduce-scatter (each owner pulls its chunk of every rank's
+ *      packed buffer) -> ONE kernel that updates every parameter reading
+ *      each reduced chunk directly from its owner rank over NVLink (no
+ *      all-gather copy through local HBM)
+ *   2  as 1, but pack and the reduce-scatter transfer are ONE kernel: each
+ *      rank casts its gradients and stores them straight into the chunk
+ *      owners' inboxes (NVLink stores overlapping the gradient reads; no
+ *      local packed buffer); the owner then reduces its inbox locally.
+ *      Needs n_tensors <= 256 (one kernel-parameter grad table), else
+ *      mode 1 runs.
+ * Bitwise identical to the other schedules; graph-capturable.  Every rank
+ * must use the same setting.  Other values: CMN_ERR_INVALID_ARG. */
+cmn_status cmn_set_fused_update(cmn_comm *comm, int mode);
 
 /* cmn_set_ctas -- grid sizes of the cross-rank kernels (takes effect on the
  * next call; 0 restores the default).  `collective_ctas`: one-shot, two-shot

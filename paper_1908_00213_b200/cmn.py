@@ -344,7 +344,10 @@ class Comm:
         _check(lib().cmn_set_algo(self._h, a, oneshot_max_bytes), "cmn_set_algo")
 
     def set_fused_update(self, on: bool):
-        _check(lib().cmn_set_fused_update(self._h, int(bool(on))), "cmn_set_fused_update")
+        """on: False/0 off, True/1/"pull" fused all-gather + update, 2/"push" also
+        fuses the pack with the reduce-scatter transfer."""
+        mode = {"pull": 1, "push": 2}.get(on, on) if isinstance(on, str) else int(on)
+        _check(lib().cmn_set_fused_update(self._h, mode), "cmn_set_fused_update")
 
     def set_pipeline(self, pieces: int):
         _check(lib().cmn_set_pipeline(self._h, pieces), "cmn_set_pipeline")

@@ -80,6 +80,9 @@ __device__ __forceinline__ uint2 ld_peer_u2(const void *p) {
                  : "memory");
     return r;
 }
+__device__ __forceinline__ void st_u2(void *p, const uint2 &v) {
+    asm volatile("st.global.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
+}
 __device__ __forceinline__ void st_u4(void *p, const uint4 &v) {
     asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
                  "r"(v.w)

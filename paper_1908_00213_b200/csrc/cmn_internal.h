@@ -132,6 +132,13 @@ cudaError_t launch_update_gather(const TensorDesc *td, const Item *items, int i0
                                  const PeerBufs &red, int world, int dtype, float inv_n, float lr,
                                  float mu, const Barrier &bar, int blocks, cudaStream_t s);
 
+// Fused pack + reduce-scatter transfer (push): start barrier, then cast and
+// store the elements of the chunk-clipped items [i0, i1) (Item.reserved =
+// owner; all tensors in [t_lo, t_lo + kGradCap)) to dst.p[owner] + base.
+cudaError_t launch_pack_push(const GradTab &g, int t_lo, const Item *items, int i0, int i1,
+                             const PeerBufs &dst, int world, int dtype, const Barrier &bar,
+                             int blocks, cudaStream_t s);
+
 // NEXT-3 NVLS: this rank's chunk [e0, e1) (elements) reduced in the switch
 // from the multicast packed buffer and multicast-stored into every rank's
 // reduced buffer; start and end cross-rank barriers.

@@ -8,6 +8,8 @@
 //   k_update_direct   a1'+a3 at N = 1: reads g directly (no pack), 20 B/param
 //   k_unpack_avg      writes the averaged gradient back (Chainer semantics)
 //   k_update_adam     NEXT-1: fused bias-corrected Adam
+//   k_pack_push       a1 + a2 (push): cast and store into the chunk owners' inboxes
+//   k_update_gather   a2 all-gather fused with a3 (reads owners' reduced chunks)
 //
 // Every kernel is HBM- or NVLink-bandwidth bound (0.25 flop/B); there is no
 // contraction, so no tensor cores.  Design: 16-byte vector accesses, one
@@ -568,6 +570,59 @@ __global__ void __launch_bounds__(kThreads) k_update_gather(const TensorDesc *__
     }
 }
 
+// Fused pack + reduce-scatter transfer (push form of a1 + the first half of
+// a2): after a start barrier (every owner has finished reducing its inbox
+// of the previous call), each element is cast to the payload dtype and
+// stored straight into its chunk owner's inbox slot for this rank, over
+// NVLink for the other ranks' chunks -- the gradient reads and the cast
+// overlap the transfer tile by tile and the packed buffer is never written
+// to local HBM.  Items are clipped to the chunks (Item.reserved = owner);
+// dst.p[o] is owner o's slot for this rank, offset so that packed index j
+// lands at dst.p[o] + j.  Pads after a tensor's last item are zeroed.
+template <int DT>
+__global__ void __launch_bounds__(kThreads) k_pack_push(GradTab g, int t_lo,
+                                                        const Item *__restrict__ items, int i0,
+                                                        int i1, const __grid_constant__ PeerBufs dst,
+                                                        int world,
+                                                        const __grid_constant__ Barrier bar) {
+    const uint32_t bv = barrier_value(bar);
+    cross_rank_barrier(bar, bv, world, 0);
+    for (int i = i0 + blockIdx.x; i < i1; i += gridDim.x) {
+        const Item it = items[i];
+        const float *__restrict__ src = g.p[it.t - t_lo] + it.k0;
+        const int nv = it.len >> 2;
+        float4 x[kVecPerThread];
+#pragma unroll
+        for (int u = 0; u < kVecPerThread; ++u) {
+            const int v = threadIdx.x + u * kThreads;
+            if (v < nv) x[u] = ld_cs_f4(src + 4 * v);
+        }
+        if constexpr (DT == 0) {
+            float *d = const_cast<float *>(static_cast<const float *>(dst.p[it.reserved])) + it.base;
+#pragma unroll
+            for (int u = 0; u < kVecPerThread; ++u) {
+                const int v = threadIdx.x + u * kThreads;
+                if (v < nv)
+                    st_u4(d + 4 * v, make_uint4(__float_as_uint(x[u].x), __float_as_uint(x[u].y),
+                                                __float_as_uint(x[u].z), __float_as_uint(x[u].w)));
+            }
+            for (int k = (nv << 2) + threadIdx.x; k < it.len; k += kThreads) d[k] = src[k];
+            for (int k = threadIdx.x; k < it.pad; k += kThreads) d[it.len + k] = 0.0f;
+        } else {
+            uint16_t *d = const_cast<uint16_t *>(static_cast<const uint16_t *>(dst.p[it.reserved])) + it.base;
+#pragma unroll
+            for (int u = 0; u < kVecPerThread; ++u) {
+                const int v = threadIdx.x + u * kThreads;
+                if (v < nv)
+                    st_u2(d + 4 * v, make_uint2(pack_half2(x[u].x, x[u].y), pack_half2(x[u].z, x[u].w)));
+            }
+            for (int k = (nv << 2) + threadIdx.x; k < it.len; k += kThreads)
+                d[k] = __half_as_ushort(__float2half_rn(src[k]));
+            for (int k = threadIdx.x; k < it.pad; k += kThreads) d[it.len + k] = 0;
+        }
+    }
+}
+
 // ------------------------------------------------------------ NEXT-3
 // NVLS all-reduce: rank r owns chunk r; for each 16-B vector the NVSwitch
 // reduces the N ranks' packed copies (multimem.ld_reduce on the multicast
@@ -804,6 +859,18 @@ cudaError_t launch_update_gather(const TensorDesc *td, const Item *items, int i0
     else
         k_update_gather<1><<<blocks, kThreads, 0, s>>>(td, items, i0, i1, red, world, inv_n, lr, mu,
                                                        bar);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack_push(const GradTab &g, int t_lo, const Item *items, int i0, int i1,
+                             const PeerBufs &dst, int world, int dtype, const Barrier &bar,
+                             int blocks, cudaStream_t s) {
+    if (blocks <= 0 || blocks > kMaxBarrierBlocks) return cudaErrorInvalidValue;
+    (void)cudaGetLastError();
+    if (dtype == 0)
+        k_pack_push<0><<<blocks, kThreads, 0, s>>>(g, t_lo, items, i0, i1, dst, world, bar);
+    else
+        k_pack_push<1><<<blocks, kThreads, 0, s>>>(g, t_lo, items, i0, i1, dst, world, bar);
     return cudaGetLastError();
 }
 

@@ -181,7 +181,7 @@ struct cmn_comm {
     // pipelined N > 1 step: pack(p+1) and update(p-1) on the caller's stream
     // overlap all-reduce(p) on a high-priority communication stream.
     int pipe_pieces = 4;
-    bool fused_update = false;    // N > 1 cmn_step: RS + fused all-gather/update
+    int fused_update = 0;         // N > 1 cmn_step: RS + fused all-gather/update (1 pull, 2 push)
     Nvls nvls;                    // NEXT-3 multicast resources (CMN_ALGO_NVLS)
     // NEXT-4 sharded update: items clipped to every rank's two-shot chunk
     // (Item.reserved = owner), rank r's list is [sitem_begin[r], sitem_begin[r+1]).
@@ -266,8 +266,13 @@ void free_registration(cmn_comm *c) {
     c->bucket_res.clear();
 }
 
+// Elements per region buffer: L plus slack so that a fused-push inbox of N
+// slots of max-chunk length (N * align64(ceil(L/N)) <= L + 64 N) fits one
+// buffer at any payload dtype.
+int64_t buf_elems(int64_t L) { return L + static_cast<int64_t>(kAlign) * kMaxWorld; }
+
 void carve(RankBufs &b, char *base, int64_t L) {
-    const size_t buf = static_cast<size_t>(L) * 4;
+    const size_t buf = static_cast<size_t>(buf_elems(L)) * 4;
     b.base = base;
     b.packed[0] = base;
     b.packed[1] = base + buf;
@@ -327,7 +332,7 @@ struct BootstrapMsg {
 };
 
 cmn_status alloc_regions(cmn_comm *c) {
-    c->region_bytes = static_cast<size_t>(c->L) * 4 * 4 + flags_bytes();
+    c->region_bytes = static_cast<size_t>(buf_elems(c->L)) * 4 * 4 + flags_bytes();
     const int own = c->simulated ? c->world : 1;
     for (int i = 0; i < own; ++i) {
         const int r = c->simulated ? i : c->rank;
@@ -977,19 +982,52 @@ cmn_status step_fused(cmn_comm *c, const float *const *grads, int dtype, float l
     const int nsim = c->simulated ? c->world : 1;
     const uint32_t seq1 = ++c->seq;
     const int par = static_cast<int>(seq1 & 1u);
-    if (cmn_status st = pack_phase(c, 0, c->T, grads, dtype, par, s); st != CMN_OK) return st;
-    PeerBufs in{}, red{};
-    for (int r = 0; r < c->world; ++r) {
-        in.p[r] = c->rb[r].packed[par];
-        red.p[r] = c->rb[r].reduced[0];
-    }
+    PeerBufs red{};
+    for (int r = 0; r < c->world; ++r) red.p[r] = c->rb[r].reduced[0];
     int64_t cs[kMaxWorld], ce[kMaxWorld];
     chunk_plan(0, c->L, c->world, cs, ce);
     const int blocks = ar_blocks_for(c);
+    const int total = c->sitem_begin[c->world];
     const Barrier bar = make_barrier(c, dtype | 2);
-    cmn_status st = timed(c, s, [&] {
+    // Push form (fused_update == 2, one grad table): owner o's inbox is its
+    // packed[0] buffer, slot i (rank i's contribution to chunk o) at
+    // i * cmax payload elements; view(o, i) + j addresses packed index j.
+    const bool push = c->fused_update == 2 && c->T <= kGradCap;
+    const size_t esz = dtype == 0 ? 4 : 2;
+    const int64_t cmax = align_up((c->L + c->world - 1) / c->world, kAlign);
+    auto inbox_view = [&](int owner, int slot) -> const void * {
+        const intptr_t a = reinterpret_cast<intptr_t>(c->rb[owner].packed[0]) +
+                           static_cast<intptr_t>((slot * cmax - cs[owner]) * static_cast<int64_t>(esz));
+        return reinterpret_cast<const void *>(a);
+    };
+    cmn_status st = CMN_OK;
+    if (push) {
+        const Barrier bar0 = make_barrier(c, dtype | 2);
+        st = timed(c, s, [&] {
+            for (int i = 0; i < nsim; ++i) {
+                const int r = c->simulated ? i : c->rank;
+                PeerBufs dst{};
+                for (int o = 0; o < c->world; ++o) dst.p[o] = inbox_view(o, r);
+                cmn_status st2 = launched(
+                    c,
+                    launch_pack_push(make_tab(grads + static_cast<size_t>(i) * c->T, 0, c->T), 0,
+                                     c->d_sitems, 0, total, dst, c->world, dtype, bar0,
+                                     upd_blocks_for(c, total), s),
+                    "pack_push");
+                if (st2 != CMN_OK) return st2;
+            }
+            return CMN_OK;
+        });
+    } else {
+        st = pack_phase(c, 0, c->T, grads, dtype, par, s);
+    }
+    if (st != CMN_OK) return st;
+    st = timed(c, s, [&] {
         for (int i = 0; i < nsim; ++i) {
             const int r = c->simulated ? i : c->rank;
+            PeerBufs in{};
+            for (int p = 0; p < c->world; ++p)
+                in.p[p] = push ? inbox_view(r, p) : c->rb[p].packed[par];
             cmn_status st2 = launched(c,
                                       launch_allreduce_twoshot(in, red, c->world, r, cs, ce, dtype, 1,
                                                                bar, blocks, s),
@@ -1001,7 +1039,6 @@ cmn_status step_fused(cmn_comm *c, const float *const *grads, int dtype, float l
     if (st != CMN_OK) return st;
     ++c->seq;
     const Barrier bar2 = make_barrier(c, dtype);
-    const int total = c->sitem_begin[c->world];
     const int gblocks = upd_blocks_for(c, total);
     // simulated ranks share one parameter replica: one launch updates it all
     st = timed(c, s, [&] {
@@ -1012,6 +1049,7 @@ cmn_status step_fused(cmn_comm *c, const float *const *grads, int dtype, float l
                         "update_gather");
     });
     if (st != CMN_OK) return st;
+    c->last = ArResult{0, dtype, false, false};   // rank r's chunk of reduced[0] (test hook)
     c->fresh = false;
     return CMN_OK;
 }
@@ -1158,7 +1196,12 @@ static cmn_status register_impl(cmn_comm *c, int T, const int *ndims, const int6
                     const int64_t lo = it.base > cs[r] ? it.base : cs[r];
                     const int64_t hi = it.base + it.len < ce[r] ? it.base + it.len : ce[r];
                     if (lo >= hi) continue;
-                    sit.push_back(Item{it.t, static_cast<int32_t>(hi - lo), it.k0 + (lo - it.base), lo, 0, r});
+                    // a tensor's pad never straddles a chunk boundary (boundaries
+                    // are multiples of 64, pads end at one): keep it on the piece
+                    // that ends the tensor
+                    const int32_t pad = hi == it.base + it.len ? it.pad : 0;
+                    sit.push_back(Item{it.t, static_cast<int32_t>(hi - lo), it.k0 + (lo - it.base), lo,
+                                       pad, r});
                 }
             }
             c->sitem_begin[c->world] = static_cast<int>(sit.size());
@@ -1571,9 +1614,10 @@ cmn_status cmn_set_algo(cmn_comm *c, cmn_algo algo, size_t oneshot_max_bytes) {
     return CMN_OK;
 }
 
-cmn_status cmn_set_fused_update(cmn_comm *c, int on) {
+cmn_status cmn_set_fused_update(cmn_comm *c, int mode) {
     if (!c) return fail(CMN_ERR_INVALID_ARG, "comm is NULL");
-    c->fused_update = on != 0;
+    if (mode < 0 || mode > 2) return fail(CMN_ERR_INVALID_ARG, "fused-update mode must be 0, 1 or 2");
+    c->fused_update = mode;
     return CMN_OK;
 }
 

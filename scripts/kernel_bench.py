@@ -137,12 +137,12 @@ def main():
                         # the simulated ranks' shared parameter replica is updated once
                         # -- mechanics and local-memory cost, not an N-GPU time
                         sched = {}
-                        for name, fused, pieces in (("serial", False, 0), ("pipelined4", False, 4),
-                                                    ("fused", True, 0)):
+                        for name, fused, pieces in (("serial", 0, 0), ("pipelined4", 0, 4),
+                                                    ("fused", 1, 0), ("fused_push", 2, 0)):
                             comm.set_fused_update(fused)
                             comm.set_pipeline(pieces)
                             sched[name] = timed(lambda: comm.step(gg, dtype, 0.1, 0.9), args.iters, stream)
-                        comm.set_fused_update(False)
+                        comm.set_fused_update(0)
                         sched["sharded"] = timed(lambda: comm.step_sharded(gg, dtype, 0.1, 0.9),
                                                  args.iters, stream)
                         rec["sim_step_us"] = sched

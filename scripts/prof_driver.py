@@ -17,7 +17,7 @@ from paper_1908_00213_b200 import Comm  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--mode", default="n1", choices=["n1", "sim8", "adam", "fused8", "sharded8"])
+    ap.add_argument("--mode", default="n1", choices=["n1", "sim8", "adam", "fused8", "push8", "sharded8"])
     ap.add_argument("--dtype", default="fp32")
     ap.add_argument("--algo", default="twoshot")
     ap.add_argument("--iters", type=int, default=3)
@@ -33,10 +33,10 @@ def main():
     g = synth.grads(shapes, workers=N)
     gt = comm.prepare([[torch.from_numpy(x).cuda() for x in gw] for gw in g] if N > 1
                       else [torch.from_numpy(x).cuda() for x in g[0]])
-    if a.mode == "fused8":
-        comm.set_fused_update(True)
-    for _ in range(a.iters if a.mode in ("fused8", "sharded8") else 0):
-        if a.mode == "fused8":
+    if a.mode in ("fused8", "push8"):
+        comm.set_fused_update(2 if a.mode == "push8" else 1)
+    for _ in range(a.iters if a.mode in ("fused8", "push8", "sharded8") else 0):
+        if a.mode in ("fused8", "push8"):
             comm.step(gt, a.dtype, 0.1, 0.9)
         else:
             comm.step_sharded(gt, a.dtype, 0.1, 0.9)

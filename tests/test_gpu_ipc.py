@@ -59,7 +59,7 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode, pieces=0):
             return
         comm.set_algo(algo)
         comm.set_pipeline(pieces)
-        comm.set_fused_update(mode in ("fused", "graph_fused"))
+        comm.set_fused_update(2 if mode in ("push", "graph_push") else mode in ("fused", "graph_fused"))
         if mode == "capture_unpipelined":
             g0 = [torch.from_numpy(x).cuda() for x in synth.grads(shapes, workers=world)[rank]]
             comm.allreduce_grads(g0, dtype)          # eager warm-up is fine
@@ -74,7 +74,7 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode, pieces=0):
                 q.put((rank, "error", e.status_name))
             dist.barrier()
             return
-        if mode in ("graph", "graph_sharded", "graph_fused"):
+        if mode in ("graph", "graph_sharded", "graph_fused", "graph_push"):
             # step 0 eagerly (creates internal streams), then capture ONE step
             # into a CUDA graph and replay it for steps 1.. with fresh grads
             # copied into the captured buffers.
@@ -113,8 +113,8 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode, pieces=0):
             elif mode == "mixed":
                 # the schedule and the grid sizes change every step, identically
                 # on every rank: per-CTA barrier epochs must stay paired
-                fused, pcs, ctas = [(True, 0, (5, 3)), (False, 2, (9, 0)),
-                                    (False, 0, (0, 0)), (True, 0, (1, 700))][s % 4]
+                fused, pcs, ctas = [(1, 0, (5, 3)), (0, 2, (9, 0)), (2, 0, (3, 9)),
+                                    (0, 0, (0, 0)), (1, 0, (1, 700)), (2, 0, (0, 0))][s % 6]
                 comm.set_fused_update(fused)
                 comm.set_pipeline(pcs)
                 comm.set_ctas(*ctas)
@@ -125,8 +125,8 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode, pieces=0):
                     comm.update_momentum_sgd(0.1, 0.9)
             elif mode == "sharded":
                 comm.step_sharded(g, dtype, 0.1, 0.9)  # RS -> own-chunk update -> param all-gather
-            elif mode == "fused":
-                comm.step(g, dtype, 0.1, 0.9)         # RS -> fused all-gather + update
+            elif mode in ("fused", "push"):
+                comm.step(g, dtype, 0.1, 0.9)         # RS (pulled / pushed) -> fused all-gather + update
             elif pieces:
                 comm.step(g, dtype, 0.1, 0.9)         # pipelined schedule, 2 streams
             else:
@@ -213,7 +213,8 @@ def test_ipc_sharded_update(orc, world, dtype):
 
 @pytest.mark.parametrize("world,dtype,mode,pieces", [(2, "fp32", "graph", 2), (3, "fp16", "graph", 4),
                                                     (2, "fp32", "graph_sharded", 0),
-                                                    (3, "fp32", "graph_fused", 0)])
+                                                    (3, "fp32", "graph_fused", 0),
+                                                    (2, "fp16", "graph_push", 0)])
 def test_ipc_cuda_graph_replay(orc, world, dtype, mode, pieces):
     """A captured CUDA graph of one multi-process step, replayed for steps
     1..3: device-resident barrier epochs advance on every replay, results
@@ -235,9 +236,10 @@ def test_ipc_single_call_schedule_refuses_capture():
     assert all(r[1] == "error" and r[2] == "CMN_ERR_UNSUPPORTED" for r in res), res
 
 
-@pytest.mark.parametrize("world,dtype", [(2, "fp16"), (3, "fp32")])
-def test_ipc_fused_allgather_update(orc, world, dtype):
-    res = _run(world, dtype, "twoshot", mode="fused")
+@pytest.mark.parametrize("world,dtype,mode", [(2, "fp16", "fused"), (3, "fp32", "fused"),
+                                              (2, "fp32", "push"), (3, "fp16", "push")])
+def test_ipc_fused_allgather_update(orc, world, dtype, mode):
+    res = _run(world, dtype, "twoshot", mode=mode)
     assert all(r[1] == "ok" for r in res), res
     shapes = synth.mlp_shapes()
     w = synth.params(shapes)
@@ -270,12 +272,12 @@ def test_ipc_step_host_packed(orc, world, dtype, pieces):
 def test_ipc_mixed_schedules_and_grids(orc, world, dtype):
     """Schedules (fused, pipelined, serial) and CTA counts (cmn_set_ctas)
     switched between steps: bit-exact with the oracle on every rank."""
-    res = _run(world, dtype, "twoshot", steps=4, mode="mixed")
+    res = _run(world, dtype, "twoshot", steps=7, mode="mixed")
     assert all(r[1] == "ok" for r in res), res
     shapes = synth.mlp_shapes()
     w = synth.params(shapes)
     v = [np.zeros_like(x) for x in w]
-    for s in range(4):
+    for s in range(7):
         orc.step(synth.grads(shapes, workers=world, step=s), w, v, 0.1, 0.9, dtype)
     for r in res:
         assert np.array_equal(np.frombuffer(r[2], np.uint32), np.concatenate(w).view(np.uint32))

@@ -310,12 +310,17 @@ def test_pipelined_step_parity(cmn, orc, N, pieces, dtype):
         comm.finalize()
 
 
-@pytest.mark.parametrize("N,dtype,ctas", [(2, "fp32", (0, 0)), (3, "fp16", (0, 0)),
-                                          (4, "fp16", (3, 1)), (8, "fp32", (0, 0)),
-                                          (8, "fp32", (1024, 1024))])
-def test_fused_allgather_update_parity(cmn, orc, N, dtype, ctas):
-    """Fused two-shot step (reduce-scatter, then one kernel updating every
-    parameter from the owners' reduced chunks) == oracle bitwise, 3 steps."""
+@pytest.mark.parametrize("N,dtype,ctas,mode", [(2, "fp32", (0, 0), "pull"), (3, "fp16", (0, 0), "pull"),
+                                               (4, "fp16", (3, 1), "pull"), (8, "fp32", (0, 0), "pull"),
+                                               (8, "fp32", (1024, 1024), "pull"),
+                                               (2, "fp32", (0, 0), "push"), (3, "fp16", (0, 0), "push"),
+                                               (4, "fp16", (3, 1), "push"), (8, "fp32", (0, 0), "push"),
+                                               (8, "fp16", (1024, 1024), "push"), (5, "fp32", (7, 2), "push")])
+def test_fused_allgather_update_parity(cmn, orc, N, dtype, ctas, mode):
+    """Fused two-shot step (reduce-scatter -- pulled from packed buffers, or
+    pushed by the fused pack kernel into the owners' inboxes -- then one
+    kernel updating every parameter from the owners' reduced chunks) ==
+    oracle bitwise, 3 steps; also the reduced chunks, pads included."""
     shapes = synth.resnet50_shapes()[:30] + RAGGED
     grads = [synth.grads(shapes, workers=N, step=s) for s in range(3)]
     params0 = synth.params(shapes)
@@ -324,14 +329,25 @@ def test_fused_allgather_update_parity(cmn, orc, N, dtype, ctas):
     try:
         w = to_dev(params0)
         comm.register_params(w)
-        comm.set_fused_update(True)
+        comm.set_fused_update(mode)
         comm.set_ctas(*ctas)            # grid sizes never change results
+        _, L = comm.layout()
+        starts, ends = cmn.plan_chunks(L, N)
+        tdt = torch.float32 if dtype == "fp32" else torch.int16
         for s, g in enumerate(grads):
             comm.step([to_dev(gw) for gw in g], dtype, 0.1, 0.9)
             torch.cuda.synchronize()
             for t in range(len(w)):
                 assert_bitwise(w[t].cpu().numpy().reshape(-1), ora[s]["w"][t], f"w[{t}] step {s}")
                 assert_bitwise(comm.momentum(t).cpu().numpy().reshape(-1), ora[s]["v"][t], f"v[{t}]")
+            for r in range(N):          # each owner's reduced chunk (pads included)
+                q = torch.empty(L, dtype=tdt, device=DEV)
+                comm.copy_reduced(r, q)
+                got = q.cpu().numpy()
+                if dtype == "fp16":
+                    got = got.view(np.uint16)
+                a, b = starts[r], ends[r]
+                assert_bitwise(got[a:b], ora[s]["reduced"][a:b], f"reduced chunk {r} step {s}")
     finally:
         comm.finalize()
 
@@ -587,7 +603,7 @@ def test_edge_layouts_all_schedules(cmn, orc, shapes_name, N):
     params0 = synth.params(shapes, seed=11)
     for dtype in ("fp32", "fp16"):
         ora, _, _ = run_oracle(orc, shapes, N, dtype, grads, params0, 0.1, 0.9)
-        for sched in ("oneshot", "twoshot", "pipelined", "sharded", "fused"):
+        for sched in ("oneshot", "twoshot", "pipelined", "sharded", "fused", "push"):
             comm = cmn.Comm.simulated_world(N) if N > 1 else cmn.Comm.init(0, 1, 0)
             try:
                 w = to_dev(params0)
@@ -602,8 +618,8 @@ def test_edge_layouts_all_schedules(cmn, orc, shapes_name, N):
                     elif sched == "pipelined":
                         comm.set_pipeline(3)
                         comm.step(gd, dtype, 0.1, 0.9)
-                    elif sched == "fused":
-                        comm.set_fused_update(True)
+                    elif sched in ("fused", "push"):
+                        comm.set_fused_update("pull" if sched == "fused" else "push")
                         comm.step(gd, dtype, 0.1, 0.9)
                     else:
                         comm.step_sharded(gd, dtype, 0.1, 0.9)
