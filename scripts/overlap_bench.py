@@ -98,8 +98,13 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     gemm_ms = e0.elapsed_time(e1) / 50
-    reps = [max(0, round(a.bwd_ms * STAGE_SHARE[stages[t]] / per_stage[stages[t]] / gemm_ms))
-            for t in range(T)]
+    # GEMM repetitions per layer, error-diffused so the total matches
+    # --bwd-ms (per-layer shares are often below one GEMM)
+    reps, carry = [], 0.0
+    for t in range(T):
+        want = a.bwd_ms * STAGE_SHARE[stages[t]] / per_stage[stages[t]] / gemm_ms + carry
+        reps.append(max(0, int(want)))
+        carry = want - reps[-1]
 
     comp = torch.cuda.current_stream()
     comm_stream = torch.cuda.Stream(priority=-1)
