@@ -38,12 +38,17 @@
  *   - Every rank must issue the same sequence of collective calls
  *     (cmn_register_params, cmn_allreduce_*, cmn_step*) with the same layout
  *     and dtype ("model structures are
- *     identical between workers merely in a single iteration").
+ *     identical between workers merely in a single iteration"), and a
+ *     rank's collective calls must be ordered on the GPU: issue them on one
+ *     stream, or join the streams with events between calls (their kernels
+ *     advance shared per-CTA barrier epochs; two collectives of one
+ *     communicator running concurrently on unjoined streams is undefined).
  *   - CUDA graphs: barrier values live in device-resident per-CTA epoch
  *     counters, so collectives replay correctly from a captured graph.  The
  *     schedules whose buffer reuse does not rely on host-chosen alternation
  *     -- cmn_step with cmn_set_pipeline >= 2 (the default) and
- *     cmn_step_sharded -- may be captured; the single-call schedules
+ *     cmn_step_sharded, cmn_set_fused_update on -- may be captured; the
+ *     single-call schedules
  *     (cmn_allreduce_grads, buckets, unpipelined cmn_step) return
  *     CMN_ERR_UNSUPPORTED under capture instead of racing.  N == 1 and
  *     simulated communicators may always be captured.
