@@ -231,6 +231,27 @@ def test_ipc_cuda_graph_replay(orc, world, dtype, mode, pieces):
         assert np.array_equal(np.frombuffer(r[2], np.uint32), want_w), f"rank {r[0]} w"
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("world,dtype,algo,mode,pieces", [(8, "fp32", "twoshot", "same", 0),
+                                                        (8, "fp16", "twoshot", "same", 3),
+                                                        (8, "fp16", "twoshot", "push", 0),
+                                                        (4, "fp32", "oneshot", "fused", 0),
+                                                        (5, "fp32", "twoshot", "sharded", 0)])
+def test_ipc_many_ranks(orc, world, dtype, algo, mode, pieces):
+    """4, 5 and 8 real processes (one GPU, time-sliced): every per-CTA
+    barrier cell of an 8-rank signal pad in use, the N = 8 kernel
+    instantiations across real IPC mappings; bit-exact w on every rank."""
+    res = _run(world, dtype, algo, mode=mode, pieces=pieces)
+    assert all(r[1] == "ok" for r in res), res
+    shapes = synth.mlp_shapes()
+    w = synth.params(shapes)
+    v = [np.zeros_like(x) for x in w]
+    for s in range(2):
+        orc.step(synth.grads(shapes, workers=world, step=s), w, v, 0.1, 0.9, dtype)
+    for r in res:
+        assert np.array_equal(np.frombuffer(r[2], np.uint32), np.concatenate(w).view(np.uint32)), r[0]
+
+
 def test_ipc_single_call_schedule_refuses_capture():
     res = _run(2, "fp32", "oneshot", mode="capture_unpipelined")
     assert all(r[1] == "error" and r[2] == "CMN_ERR_UNSUPPORTED" for r in res), res
