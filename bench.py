@@ -172,6 +172,12 @@ def workload():
     return shapes, [synth.numel(s) for s in shapes]
 
 
+def workload_name(P: int, dtype: str) -> str:
+    """config.workload, identical for both arms."""
+    return (f"ResNet-50 gradient set (161 tensors, {P:,} fp32 params), {dtype} payload, "
+            f"pack+allreduce+momentum-SGD step (BASELINE config {'2' if dtype == 'fp32' else '3'})")
+
+
 # ------------------------------------------------------ CPU oracle baseline
 
 def _oracle_sample(n_workers: int):
@@ -223,9 +229,8 @@ def run_reference(args):
     n = max(1, args.gpus)
     us, desc = oracle_step_time(n, args.dtype, steps=args.steps, warmup=args.warmup)
     shapes, sizes = workload()
-    cfg = {"workload": f"ResNet-50 gradient set (161 tensors, {sum(sizes):,} fp32 params), "
-                       f"{args.dtype} payload, pack+allreduce+momentum-SGD step, {n} worker(s) "
-                       f"simulated on the host"}
+    cfg = {"workload": workload_name(sum(sizes), args.dtype), "comm_dtype": args.dtype,
+           "parallelism": f"dp{n}", "workers": f"{n} worker(s) simulated on the host CPU"}
     line = {"impl": "reference", "metric": METRIC, "value": us, "unit": "us", "n_gpus": n,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": us / 1e3,
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
@@ -578,9 +583,7 @@ def main():
         cus, desc = oracle_step_time(world, args.dtype, budget_s=args.cpu_budget_s)
         cpu = {"value": cus, "unit": "us", "cores": 1, "kind": "oracle", "sample": desc}
 
-    cfg = {"workload": f"ResNet-50 gradient set (161 tensors, {P:,} fp32 params), {args.dtype} "
-                       f"payload, pack+allreduce+momentum-SGD step (BASELINE config "
-                       f"{'2' if args.dtype == 'fp32' else '3'})",
+    cfg = {"workload": workload_name(P, args.dtype),
            "n_tensors": T, "n_params": P, "padded_len": L, "comm_dtype": args.dtype,
            "algo": args.algo if world > 1 else "identity (N=1 fused direct update)",
            "schedule": schedule, "schedule_trials_us": trials,
