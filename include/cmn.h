@@ -279,6 +279,13 @@ cmn_status cmn_update_adam(cmn_comm *comm, float alpha, float beta1, float beta2
  * bucket_bytes == 0 means one bucket. */
 cmn_status cmn_plan_buckets(cmn_comm *comm, size_t bucket_bytes, int *n_buckets_out);
 
+/* cmn_plan_bucket_ranges -- the same plan, host only, from tensor sizes
+ * (numel[n_tensors]); writes the bucket count and, when non-NULL, each
+ * bucket's [t_begin[b], t_end[b]) (arrays of >= n_tensors entries, the
+ * maximum bucket count).  No communicator or GPU needed. */
+cmn_status cmn_plan_bucket_ranges(int n_tensors, const int64_t *numel, size_t bucket_bytes,
+                                  int *n_buckets_out, int *t_begin, int *t_end);
+
 /* cmn_get_bucket -- tensor range [t_begin, t_end) of bucket b. */
 cmn_status cmn_get_bucket(const cmn_comm *comm, int bucket, int *t_begin, int *t_end);
 

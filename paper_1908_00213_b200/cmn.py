@@ -64,6 +64,8 @@ SIGNATURES = [
     ("cmn_plan_layout", C.c_int, [C.c_int, C.POINTER(C.c_int), _I64P, _I64P, _I64P,
                                   C.POINTER(C.c_uint64)]),
     ("cmn_plan_chunks", C.c_int, [C.c_int64, C.c_int, _I64P, _I64P]),
+    ("cmn_plan_bucket_ranges", C.c_int, [C.c_int, _I64P, C.c_size_t, C.POINTER(C.c_int),
+                                         C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("cmn_bootstrap_verify", C.c_int, [C.c_int, C.c_int, AllgatherFn, _P, C.c_uint64]),
     ("cmn_share_fd", C.c_int, [C.c_int, C.c_int, AllgatherFn, _P, C.c_int, C.POINTER(C.c_int)]),
 ]
@@ -189,6 +191,18 @@ def plan_layout(shapes):
     h = C.c_uint64()
     _check(lib().cmn_plan_layout(T, nd, dims, off, C.byref(L), C.byref(h)), "cmn_plan_layout")
     return list(off), L.value, h.value
+
+
+def plan_bucket_ranges(sizes, bucket_bytes: int):
+    """cmn_plan_bucket_ranges: list of (t_begin, t_end), bucket 0 = last tensors."""
+    T = len(sizes)
+    numel = (C.c_int64 * T)(*[int(n) for n in sizes])
+    n = C.c_int()
+    b = (C.c_int * T)()
+    e = (C.c_int * T)()
+    _check(lib().cmn_plan_bucket_ranges(T, numel, bucket_bytes, C.byref(n), b, e),
+           "cmn_plan_bucket_ranges")
+    return [(b[i], e[i]) for i in range(n.value)]
 
 
 def plan_chunks(L: int, world: int):

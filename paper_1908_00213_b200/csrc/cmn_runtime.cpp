@@ -1501,22 +1501,49 @@ cmn_status cmn_update_adam(cmn_comm *c, float alpha, float beta1, float beta2, f
     return st;
 }
 
-cmn_status cmn_plan_buckets(cmn_comm *c, size_t bucket_bytes, int *n_out) {
-    if (cmn_status st = require_registered(c); st != CMN_OK) return st;
-    c->buckets.clear();
-    int end = c->T;
+namespace {
+// Reverse-order greedy bucket plan over tensor sizes (host only).
+std::vector<std::pair<int, int>> bucket_plan(const int64_t *numel, int T, size_t bucket_bytes) {
+    std::vector<std::pair<int, int>> out;
+    int end = T;
     while (end > 0) {
         int begin = end - 1;
-        size_t acc = static_cast<size_t>(c->numel[begin]) * 4;
+        size_t acc = static_cast<size_t>(numel[begin]) * 4;
         while (begin > 0 && bucket_bytes > 0 &&
-               acc + static_cast<size_t>(c->numel[begin - 1]) * 4 <= bucket_bytes) {
+               acc + static_cast<size_t>(numel[begin - 1]) * 4 <= bucket_bytes) {
             --begin;
-            acc += static_cast<size_t>(c->numel[begin]) * 4;
+            acc += static_cast<size_t>(numel[begin]) * 4;
         }
         if (bucket_bytes == 0) begin = 0;
-        c->buckets.emplace_back(begin, end);
+        out.emplace_back(begin, end);
         end = begin;
     }
+    return out;
+}
+}  // namespace
+
+cmn_status cmn_plan_bucket_ranges(int n_tensors, const int64_t *numel, size_t bucket_bytes,
+                                  int *n_buckets_out, int *t_begin, int *t_end) {
+    if (n_tensors <= 0 || !numel || !n_buckets_out)
+        return fail(CMN_ERR_INVALID_ARG, "n_tensors must be >= 1; numel and n_buckets_out non-NULL");
+    for (int t = 0; t < n_tensors; ++t)
+        if (numel[t] < 0) return fail(CMN_ERR_INVALID_ARG, "negative numel");
+    try {
+        const auto plan = bucket_plan(numel, n_tensors, bucket_bytes);
+        *n_buckets_out = static_cast<int>(plan.size());
+        for (size_t b = 0; b < plan.size(); ++b) {
+            if (t_begin) t_begin[b] = plan[b].first;
+            if (t_end) t_end[b] = plan[b].second;
+        }
+        return CMN_OK;
+    } catch (...) {
+        return fail(CMN_ERR_OOM, "host allocation failed");
+    }
+}
+
+cmn_status cmn_plan_buckets(cmn_comm *c, size_t bucket_bytes, int *n_out) {
+    if (cmn_status st = require_registered(c); st != CMN_OK) return st;
+    c->buckets = bucket_plan(c->numel.data(), c->T, bucket_bytes);
     c->bucket_fresh.assign(c->buckets.size(), 0);
     c->bucket_res.assign(c->buckets.size(), ArResult{});
     if (n_out) *n_out = static_cast<int>(c->buckets.size());

@@ -105,3 +105,31 @@ def test_invalid_world(lib):
     h = C.c_void_p()
     assert lib.cmn_init_simulated(9, 0, C.byref(h)) == 1
     assert lib.cmn_init_simulated(0, 0, C.byref(h)) == 1
+
+
+@pytest.mark.parametrize("bucket_mb", [0, 1, 4, 8, 16, 25, 1000])
+def test_bucket_plan(bucket_mb):
+    """cmn_plan_bucket_ranges (host only) against a plain re-statement of its
+    definition in include/cmn.h: contiguous reverse-order ranges covering
+    every tensor once, each holding at most bucket_bytes of fp32 gradients
+    unless it is a single larger tensor, and maximal (the next tensor would
+    not fit); bucket_bytes == 0 gives one bucket."""
+    import synth
+    from paper_1908_00213_b200 import cmn
+    sizes = [synth.numel(s) for s in synth.resnet50_shapes()]
+    cap = bucket_mb << 20
+    plan = cmn.plan_bucket_ranges(sizes, cap)
+    assert plan[0][1] == len(sizes) and plan[-1][0] == 0
+    for (b0, e0), (b1, e1) in zip(plan, plan[1:]):
+        assert e1 == b0                              # contiguous, reverse order
+    for b, e in plan:
+        nbytes = 4 * sum(sizes[b:e])
+        assert e > b
+        if cap == 0:
+            assert (b, e) == (0, len(sizes))
+            continue
+        assert nbytes <= cap or e - b == 1
+        if b > 0:
+            assert nbytes + 4 * sizes[b - 1] > cap    # maximal
+    if cap == 0:
+        assert len(plan) == 1
