@@ -120,8 +120,10 @@ def _shapes_args(shapes):
 
 def _stream(stream) -> int:
     if stream is None:
+        # torch's current stream of the current device, read without
+        # building a torch.cuda.Stream object (~0.3 us instead of ~3 us)
         import torch
-        return torch.cuda.current_stream().cuda_stream
+        return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
     if isinstance(stream, int):
         return stream
     return stream.cuda_stream

@@ -73,9 +73,10 @@ struct PeerBufs {
 // ---------------------------------------------------------------- launchers
 // All return cudaGetLastError() after the launch.  `dtype` 0 = fp32, 1 = fp16.
 
-// a1: pack items [i0, i1) (tensors of those items lie in [t_lo, t_lo+kGradCap)).
-cudaError_t launch_pack(const GradTab &g, int t_lo, const TensorDesc *td, const Item *items,
-                        int i0, int i1, int dtype, void *packed, cudaStream_t s);
+// a1: pack items [i0, i1) (tensors of those items lie in [t_lo, t_lo + ntab),
+// ntab <= kGradCap: the table's used entries; small tables launch smaller).
+cudaError_t launch_pack(const GradTab &g, int ntab, int t_lo, const TensorDesc *td,
+                        const Item *items, int i0, int i1, int dtype, void *packed, cudaStream_t s);
 
 // a3: update from a reduced packed buffer (payload dtype), momentum SGD.
 cudaError_t launch_update_sgd(const TensorDesc *td, const Item *items, int i0, int i1,
@@ -83,7 +84,7 @@ cudaError_t launch_update_sgd(const TensorDesc *td, const Item *items, int i0, i
                               cudaStream_t s);
 
 // a1'+a3 at N = 1: read g directly (cast through fp16 if dtype == 1).
-cudaError_t launch_update_direct(const GradTab &g, int t_lo, const TensorDesc *td,
+cudaError_t launch_update_direct(const GradTab &g, int ntab, int t_lo, const TensorDesc *td,
                                  const Item *items, int i0, int i1, int dtype, float lr, float mu,
                                  cudaStream_t s);
 

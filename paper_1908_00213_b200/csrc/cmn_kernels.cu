@@ -26,6 +26,21 @@ namespace cmn {
 namespace {
 
 constexpr int kVecPerThread = kItemElems / 4 / kThreads;  // float4s per thread per item
+
+// Grad pointer table passed by value: kernels are instantiated for a small
+// (16) and the full (kGradCap) capacity, so small models launch with a
+// 128-B instead of a 2-KB parameter block (host launch cost).
+constexpr int kSmallTab = 16;
+template <int CAP>
+struct GradTabN {
+    const float *p[CAP];
+};
+template <int CAP>
+GradTabN<CAP> shrink(const GradTab &g) {
+    GradTabN<CAP> t;
+    for (int i = 0; i < CAP; ++i) t.p[i] = g.p[i];
+    return t;
+}
 static_assert(kItemElems % (4 * kThreads) == 0, "item must be a whole number of CTA vectors");
 
 // a = r * fl(1/N); v = fma(mu, v, a); w = fma(-lr, v, w)   (readings R3, R6)
@@ -81,8 +96,8 @@ __device__ __forceinline__ void pack_store(void *packed, int64_t j, const float4
     }
 }
 
-template <int DT>
-__global__ void __launch_bounds__(kThreads) k_pack(GradTab g, int t_lo,
+template <int DT, int CAP>
+__global__ void __launch_bounds__(kThreads) k_pack(GradTabN<CAP> g, int t_lo,
                                                    const Item *__restrict__ items, int i0, int i1,
                                                    void *__restrict__ packed) {
     const int ib = i0 + blockIdx.x * kPackItems;
@@ -171,8 +186,8 @@ __global__ void __launch_bounds__(kThreads) k_update_sgd(const TensorDesc *__res
 // a1' + a3 at N = 1: the all-reduce is the identity, so r = cast(g) and the
 // pack is skipped (20 B/param instead of 28).  Bitwise equal to the
 // unfused path: a = cast(g) * 1.0f.
-template <int DT>
-__global__ void __launch_bounds__(kThreads) k_update_direct(GradTab g, int t_lo,
+template <int DT, int CAP>
+__global__ void __launch_bounds__(kThreads) k_update_direct(GradTabN<CAP> g, int t_lo,
                                                             const TensorDesc *__restrict__ td,
                                                             const Item *__restrict__ items, int i0,
                                                             float lr, float mu) {
@@ -219,8 +234,8 @@ __global__ void __launch_bounds__(kThreads) k_update_direct(GradTab g, int t_lo,
     }
 }
 
-template <int DT>
-__global__ void __launch_bounds__(kThreads) k_unpack_avg(GradTab out, int t_lo,
+template <int DT, int CAP>
+__global__ void __launch_bounds__(kThreads) k_unpack_avg(GradTabN<CAP> out, int t_lo,
                                                          const TensorDesc *__restrict__ td,
                                                          const Item *__restrict__ items, int i0,
                                                          const void *__restrict__ reduced,
@@ -579,8 +594,8 @@ __global__ void __launch_bounds__(kThreads) k_update_gather(const TensorDesc *__
 // to local HBM.  Items are clipped to the chunks (Item.reserved = owner);
 // dst.p[o] is owner o's slot for this rank, offset so that packed index j
 // lands at dst.p[o] + j.  Pads after a tensor's last item are zeroed.
-template <int DT>
-__global__ void __launch_bounds__(kThreads) k_pack_push(GradTab g, int t_lo,
+template <int DT, int CAP>
+__global__ void __launch_bounds__(kThreads) k_pack_push(GradTabN<CAP> g, int t_lo,
                                                         const Item *__restrict__ items, int i0,
                                                         int i1, const __grid_constant__ PeerBufs dst,
                                                         int world,
@@ -683,17 +698,26 @@ inline int grid_of(int i0, int i1) { return i1 > i0 ? i1 - i0 : 0; }
 
 // ----------------------------------------------------------------- launchers
 
-cudaError_t launch_pack(const GradTab &g, int t_lo, const TensorDesc *td, const Item *items,
-                        int i0, int i1, int dtype, void *packed, cudaStream_t s) {
+cudaError_t launch_pack(const GradTab &g, int ntab, int t_lo, const TensorDesc *td,
+                        const Item *items, int i0, int i1, int dtype, void *packed, cudaStream_t s) {
     const int n = grid_of(i0, i1);
     if (n == 0) return cudaSuccess;
     (void)td;
     (void)cudaGetLastError();  // report this launch's error, not a stale one
     const int grid = (n + kPackItems - 1) / kPackItems;
-    if (dtype == 0)
-        k_pack<0><<<grid, kThreads, 0, s>>>(g, t_lo, items, i0, i1, packed);
-    else
-        k_pack<1><<<grid, kThreads, 0, s>>>(g, t_lo, items, i0, i1, packed);
+    if (ntab <= kSmallTab) {
+        const auto t = shrink<kSmallTab>(g);
+        if (dtype == 0)
+            k_pack<0, kSmallTab><<<grid, kThreads, 0, s>>>(t, t_lo, items, i0, i1, packed);
+        else
+            k_pack<1, kSmallTab><<<grid, kThreads, 0, s>>>(t, t_lo, items, i0, i1, packed);
+    } else {
+        const auto t = shrink<kGradCap>(g);
+        if (dtype == 0)
+            k_pack<0, kGradCap><<<grid, kThreads, 0, s>>>(t, t_lo, items, i0, i1, packed);
+        else
+            k_pack<1, kGradCap><<<grid, kThreads, 0, s>>>(t, t_lo, items, i0, i1, packed);
+    }
     return cudaGetLastError();
 }
 
@@ -710,16 +734,25 @@ cudaError_t launch_update_sgd(const TensorDesc *td, const Item *items, int i0, i
     return cudaGetLastError();
 }
 
-cudaError_t launch_update_direct(const GradTab &g, int t_lo, const TensorDesc *td,
+cudaError_t launch_update_direct(const GradTab &g, int ntab, int t_lo, const TensorDesc *td,
                                  const Item *items, int i0, int i1, int dtype, float lr, float mu,
                                  cudaStream_t s) {
     const int grid = grid_of(i0, i1);
     if (grid == 0) return cudaSuccess;
     (void)cudaGetLastError();  // report this launch's error, not a stale one
-    if (dtype == 0)
-        k_update_direct<0><<<grid, kThreads, 0, s>>>(g, t_lo, td, items, i0, lr, mu);
-    else
-        k_update_direct<1><<<grid, kThreads, 0, s>>>(g, t_lo, td, items, i0, lr, mu);
+    if (ntab <= kSmallTab) {
+        const auto t = shrink<kSmallTab>(g);
+        if (dtype == 0)
+            k_update_direct<0, kSmallTab><<<grid, kThreads, 0, s>>>(t, t_lo, td, items, i0, lr, mu);
+        else
+            k_update_direct<1, kSmallTab><<<grid, kThreads, 0, s>>>(t, t_lo, td, items, i0, lr, mu);
+    } else {
+        const auto t = shrink<kGradCap>(g);
+        if (dtype == 0)
+            k_update_direct<0, kGradCap><<<grid, kThreads, 0, s>>>(t, t_lo, td, items, i0, lr, mu);
+        else
+            k_update_direct<1, kGradCap><<<grid, kThreads, 0, s>>>(t, t_lo, td, items, i0, lr, mu);
+    }
     return cudaGetLastError();
 }
 
@@ -729,10 +762,11 @@ cudaError_t launch_unpack_avg(const GradTab &out, int t_lo, const TensorDesc *td
     const int grid = grid_of(i0, i1);
     if (grid == 0) return cudaSuccess;
     (void)cudaGetLastError();  // report this launch's error, not a stale one
+    const auto t = shrink<kGradCap>(out);
     if (dtype == 0)
-        k_unpack_avg<0><<<grid, kThreads, 0, s>>>(out, t_lo, td, items, i0, reduced, inv_n);
+        k_unpack_avg<0, kGradCap><<<grid, kThreads, 0, s>>>(t, t_lo, td, items, i0, reduced, inv_n);
     else
-        k_unpack_avg<1><<<grid, kThreads, 0, s>>>(out, t_lo, td, items, i0, reduced, inv_n);
+        k_unpack_avg<1, kGradCap><<<grid, kThreads, 0, s>>>(t, t_lo, td, items, i0, reduced, inv_n);
     return cudaGetLastError();
 }
 
@@ -867,10 +901,11 @@ cudaError_t launch_pack_push(const GradTab &g, int t_lo, const Item *items, int 
                              int blocks, cudaStream_t s) {
     if (blocks <= 0 || blocks > kMaxBarrierBlocks) return cudaErrorInvalidValue;
     (void)cudaGetLastError();
+    const auto t = shrink<kGradCap>(g);
     if (dtype == 0)
-        k_pack_push<0><<<blocks, kThreads, 0, s>>>(g, t_lo, items, i0, i1, dst, world, bar);
+        k_pack_push<0, kGradCap><<<blocks, kThreads, 0, s>>>(t, t_lo, items, i0, i1, dst, world, bar);
     else
-        k_pack_push<1><<<blocks, kThreads, 0, s>>>(g, t_lo, items, i0, i1, dst, world, bar);
+        k_pack_push<1, kGradCap><<<blocks, kThreads, 0, s>>>(t, t_lo, items, i0, i1, dst, world, bar);
     return cudaGetLastError();
 }
 

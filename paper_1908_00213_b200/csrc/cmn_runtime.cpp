@@ -471,7 +471,7 @@ cmn_status pack_phase(cmn_comm *c, int ta, int tb, const float *const *grads, in
         void *dst = dst_override ? dst_override : c->rb[r].packed[par];
         cmn_status st = for_groups(c, ta, tb, [&](int lo, int hi, int i0, int i1) {
             return launched(c,
-                            launch_pack(make_tab(g, lo, hi), lo, c->d_td, c->d_items, i0, i1, dtype,
+                            launch_pack(make_tab(g, lo, hi), hi - lo, lo, c->d_td, c->d_items, i0, i1, dtype,
                                         dst, s),
                             "pack");
         });
@@ -636,6 +636,8 @@ cmn_status require_dtype(int dtype) {
 }
 
 cmn_status set_device(const cmn_comm *c) {
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur == c->device) return CMN_OK;
     CMN_CUDA(cudaSetDevice(c->device));
     return CMN_OK;
 }
@@ -1304,7 +1306,7 @@ cmn_status cmn_step(cmn_comm *c, const float *const *grads, cmn_dtype dtype, flo
     return timed(c, s, [&] {
         return for_groups(c, 0, c->T, [&](int lo, int hi, int i0, int i1) {
             return launched(c,
-                            launch_update_direct(make_tab(grads, lo, hi), lo, c->d_td, c->d_items,
+                            launch_update_direct(make_tab(grads, lo, hi), hi - lo, lo, c->d_td, c->d_items,
                                                  i0, i1, dtype, lr, mu, s),
                             "update_direct");
         });
@@ -1413,7 +1415,7 @@ cmn_status cmn_step_host_packed(cmn_comm *c, const float *host_grads, float *hos
             const int a = g0 > i0 ? g0 : i0, b = g1 < i1 ? g1 : i1;
             if (a >= b) return CMN_OK;
             return launched(c,
-                            launch_update_direct(make_tab(dg.data(), lo, hi), lo, c->d_td,
+                            launch_update_direct(make_tab(dg.data(), lo, hi), hi - lo, lo, c->d_td,
                                                  c->d_items, a, b, dtype, lr, mu, s),
                             "update_direct");
         });
