@@ -669,12 +669,18 @@ __device__ __forceinline__ void mm_st(void *mc, const uint4 &v) {
                  : "memory");
 }
 
+// The same physical buffers are written through unicast addresses (the
+// pack, the update's reads) and through the multicast address here, so the
+// kernel fences the alias proxy on both sides of its multicast accesses.
+__device__ __forceinline__ void fence_proxy_alias() { asm volatile("fence.proxy.alias;" ::: "memory"); }
+
 template <int DT>
 __global__ void __launch_bounds__(kThreads) k_nvls(const char *mc_packed, char *mc_reduced,
                                                    int64_t v0, int64_t v1, int world,
                                                    const __grid_constant__ Barrier bar) {
     const uint32_t bv = barrier_value(bar);
     cross_rank_barrier(bar, bv, world, 0);           // every rank's pack is complete
+    fence_proxy_alias();
     for (int64_t tile = v0 + static_cast<int64_t>(blockIdx.x) * kTileVecs; tile < v1;
          tile += static_cast<int64_t>(gridDim.x) * kTileVecs) {
         uint4 x[kARVec];
@@ -689,6 +695,7 @@ __global__ void __launch_bounds__(kThreads) k_nvls(const char *mc_packed, char *
             if (idx < v1) mm_st(mc_reduced + 16 * idx, x[u]);
         }
     }
+    fence_proxy_alias();
     cross_rank_barrier(bar, bv, world, 1);           // every rank's stores have landed
 }
 
