@@ -208,24 +208,40 @@ def test_step_n1_direct_equals_unfused(cmn, orc):
 
 
 @pytest.mark.slow
-def test_r50_full_size_n1_bench_config(cmn, orc):
-    """BASELINE config 2 at N = 1 in the launch configuration bench.py times
-    (cmn_step, fp32): all 25.6M elements of w and v vs the oracle."""
+@pytest.mark.parametrize("dtype", ["fp32", "fp16"])
+def test_r50_full_size_n1_bench_config(cmn, orc, dtype):
+    """BASELINE configs 2 / 3 at N = 1 in exactly the launch configuration
+    bench.py times: parameters and gradients as views of one flat allocation
+    each in the packed layout, a pre-marshalled pointer table, cmn_step on
+    torch's current stream, 3 steps; all 25.6M elements of w and v vs the
+    oracle after every step."""
     shapes = synth.resnet50_shapes()
-    g = synth.grads(shapes, workers=1)
+    sizes = [synth.numel(s) for s in shapes]
     params0 = synth.params(shapes)
     w_o = [p.copy() for p in params0]
     v_o = [np.zeros_like(p) for p in params0]
-    orc.step(g, w_o, v_o, 0.1, 0.9, "fp32")
+    off, L, _ = cmn.plan_layout(shapes)
     comm = cmn.Comm.init(0, 1, 0)
     try:
-        w = to_dev(params0)
-        comm.register_params(w)
-        comm.step(to_dev(g[0]), "fp32", 0.1, 0.9)
-        torch.cuda.synchronize()
+        flat_w = torch.empty(L, dtype=torch.float32, device=DEV)
+        w = [flat_w[off[t]: off[t] + sizes[t]].view(shapes[t]) for t in range(len(shapes))]
         for t in range(len(w)):
-            assert_bitwise(w[t].cpu().numpy().reshape(-1), w_o[t], f"w[{t}]")
-            assert_bitwise(comm.momentum(t).cpu().numpy().reshape(-1), v_o[t], f"v[{t}]")
+            w[t].copy_(torch.from_numpy(params0[t]).view(shapes[t]))
+        comm.register_params(w)
+        flat_g = torch.empty(L, dtype=torch.float32, device=DEV)
+        gv = [flat_g[off[t]: off[t] + sizes[t]] for t in range(len(shapes))]
+        table = comm.prepare(gv)
+        for step in range(3):
+            g = synth.grads(shapes, workers=1, step=step)
+            for t in range(len(gv)):
+                gv[t].copy_(torch.from_numpy(g[0][t]))
+            orc.step(g, w_o, v_o, 0.1, 0.9, dtype)
+            comm.step(table, dtype, 0.1, 0.9)
+            torch.cuda.synchronize()
+            got_w = flat_w.cpu().numpy()
+            for t in range(len(w)):
+                assert_bitwise(got_w[off[t]: off[t] + sizes[t]].copy(), w_o[t], f"w[{t}] step {step}")
+                assert_bitwise(comm.momentum(t).cpu().numpy().reshape(-1), v_o[t], f"v[{t}] step {step}")
     finally:
         comm.finalize()
 
