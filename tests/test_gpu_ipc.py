@@ -36,6 +36,9 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode, pieces=0):
         torch.cuda.set_device(0)
         dist.init_process_group("gloo", rank=rank, world_size=world)
         shapes = synth.mlp_shapes()
+        digest = mode.startswith("r50:")          # full ResNet-50 set: return hashes
+        if digest:
+            shapes, mode = synth.resnet50_shapes(), mode[4:]
         if mode == "mismatch" and rank == 1:
             shapes = shapes[:-1] + [(11,)]
         comm = cmn.Comm.init(rank, world, 0, dist.group.WORLD)
@@ -137,7 +140,12 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode, pieces=0):
             comm.poll_error()
             wb = np.concatenate([x.cpu().numpy().reshape(-1) for x in w])
             vb = np.concatenate([comm.momentum(t).cpu().numpy().reshape(-1) for t in range(len(w))])
-            q.put((rank, "ok", wb.tobytes(), vb.tobytes()))
+            if digest:
+                import hashlib
+                q.put((rank, "ok", hashlib.sha256(wb.tobytes()).hexdigest(),
+                       hashlib.sha256(vb.tobytes()).hexdigest()))
+            else:
+                q.put((rank, "ok", wb.tobytes(), vb.tobytes()))
         except cmn.CmnError as e:
             q.put((rank, "error", e.status_name))
         dist.barrier()            # no rank frees its IPC-exported buffers while a peer may read them
@@ -250,6 +258,27 @@ def test_ipc_many_ranks(orc, world, dtype, algo, mode, pieces):
         orc.step(synth.grads(shapes, workers=world, step=s), w, v, 0.1, 0.9, dtype)
     for r in res:
         assert np.array_equal(np.frombuffer(r[2], np.uint32), np.concatenate(w).view(np.uint32)), r[0]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("dtype,mode,pieces", [("fp32", "r50:same", 4), ("fp16", "r50:push", 0)])
+def test_ipc_r50_full_size(orc, dtype, mode, pieces):
+    """The bench's workload at N = 2 across two real processes: the full
+    ResNet-50 gradient set, pipelined (4 pieces, the default) and push-fused
+    schedules, 2 steps; every rank's w and v bit-exact with the oracle
+    (compared by SHA-256 of all 25.6M elements)."""
+    import hashlib
+    res = _run(2, dtype, "twoshot", mode=mode, pieces=pieces)
+    assert all(r[1] == "ok" for r in res), res
+    shapes = synth.resnet50_shapes()
+    w = synth.params(shapes)
+    v = [np.zeros_like(x) for x in w]
+    for s in range(2):
+        orc.step(synth.grads(shapes, workers=2, step=s), w, v, 0.1, 0.9, dtype)
+    hw = hashlib.sha256(np.concatenate(w).tobytes()).hexdigest()
+    hv = hashlib.sha256(np.concatenate(v).tobytes()).hexdigest()
+    for r in res:
+        assert r[2] == hw and r[3] == hv, f"rank {r[0]}"
 
 
 def test_ipc_single_call_schedule_refuses_capture():
