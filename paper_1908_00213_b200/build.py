@@ -48,7 +48,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     for src in SOURCES:
         obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
-        cmd = [nvcc(), *ARCH, *NVFLAGS, "-I", os.path.join(ROOT, "include"), "-c",
+        extra = os.environ.get("CMN_EXTRA_NVFLAGS", "").split()   # measurement builds only
+        cmd = [nvcc(), *ARCH, *NVFLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-c",
                os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"] if verbose else []

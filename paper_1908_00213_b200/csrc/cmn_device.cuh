@@ -48,6 +48,9 @@ struct Tree<I, I> {
 
 // ------------------------------------------------------------- memory ops
 // Streaming (evict-first) 16-byte accesses for data touched exactly once.
+// Built with -DCMN_NO_STREAMING_HINTS they become plain accesses (a
+// measurement switch for scripts/gpu_hints_ab.sh).
+#ifndef CMN_NO_STREAMING_HINTS
 __device__ __forceinline__ float4 ld_cs_f4(const float *p) {
     return __ldcs(reinterpret_cast<const float4 *>(p));
 }
@@ -60,6 +63,20 @@ __device__ __forceinline__ uint2 ld_cs_u2(const void *p) {
 __device__ __forceinline__ void st_cs_u2(void *p, const uint2 &v) {
     __stcs(reinterpret_cast<uint2 *>(p), v);
 }
+#else
+__device__ __forceinline__ float4 ld_cs_f4(const float *p) {
+    return *reinterpret_cast<const float4 *>(p);
+}
+__device__ __forceinline__ void st_cs_f4(float *p, const float4 &v) {
+    *reinterpret_cast<float4 *>(p) = v;
+}
+__device__ __forceinline__ uint2 ld_cs_u2(const void *p) {
+    return *reinterpret_cast<const uint2 *>(p);
+}
+__device__ __forceinline__ void st_cs_u2(void *p, const uint2 &v) {
+    *reinterpret_cast<uint2 *>(p) = v;
+}
+#endif
 
 // 16-byte load that may target a peer GPU's memory (UVA / IPC mapping) and
 // data published by a peer during this kernel: weak load, no L1 allocation

@@ -84,9 +84,11 @@ cudaError_t launch_update_sgd(const TensorDesc *td, const Item *items, int i0, i
                               cudaStream_t s);
 
 // a1'+a3 at N = 1: read g directly (cast through fp16 if dtype == 1).
-cudaError_t launch_update_direct(const GradTab &g, int ntab, int t_lo, const TensorDesc *td,
-                                 const Item *items, int i0, int i1, int dtype, float lr, float mu,
-                                 cudaStream_t s);
+// wt: the parameter pointers of the same tensors; mom: momentum base (tensor
+// t at off_t, so element (t, k) at mom + off_t + k).
+cudaError_t launch_update_direct(const GradTab &g, const GradTab &wt, int ntab, int t_lo,
+                                 float *mom, const Item *items, int i0, int i1, int dtype, float lr,
+                                 float mu, cudaStream_t s);
 
 // write a = r * inv_n into out tensors (test hook / Chainer semantics).
 cudaError_t launch_unpack_avg(const GradTab &out, int t_lo, const TensorDesc *td,

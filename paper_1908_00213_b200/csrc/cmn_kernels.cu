@@ -186,26 +186,34 @@ __global__ void __launch_bounds__(kThreads) k_update_sgd(const TensorDesc *__res
 // a1' + a3 at N = 1: the all-reduce is the identity, so r = cast(g) and the
 // pack is skipped (20 B/param instead of 28).  Bitwise equal to the
 // unfused path: a = cast(g) * 1.0f.
+//
+// Addresses come from kernel-parameter tables (w) and the packed index
+// (momentum at d_mom + base): no dependent descriptor load before the first
+// data load.  Default cache operators: the streaming (.cs, evict-first)
+// hints measured 1.6 % slower here (bench 79.3 vs 78.0 us; probe
+// scripts/update_variants.cu B vs A), so this kernel -- the whole N = 1
+// step -- uses plain LDG/STG.128.
 template <int DT, int CAP>
-__global__ void __launch_bounds__(kThreads) k_update_direct(GradTabN<CAP> g, int t_lo,
-                                                            const TensorDesc *__restrict__ td,
+__global__ void __launch_bounds__(kThreads) k_update_direct(GradTabN<CAP> g, GradTabN<CAP> wt,
+                                                            int t_lo, float *__restrict__ mom,
                                                             const Item *__restrict__ items, int i0,
                                                             float lr, float mu) {
     const Item it = items[i0 + blockIdx.x];
-    const TensorDesc d = td[it.t];
     const float *__restrict__ gp = g.p[it.t - t_lo] + it.k0;
-    float *__restrict__ w = d.w + it.k0;
-    float *__restrict__ m = d.mom + it.k0;
+    float *__restrict__ w = const_cast<float *>(wt.p[it.t - t_lo]) + it.k0;
+    float *__restrict__ m = mom + it.base;
     const int nv = it.len >> 2;
+    auto ld = [](const float *p) { return *reinterpret_cast<const float4 *>(p); };
+    auto st = [](float *p, const float4 &x) { *reinterpret_cast<float4 *>(p) = x; };
 
     float4 r[kVecPerThread], wv[kVecPerThread], mv[kVecPerThread];
 #pragma unroll
     for (int u = 0; u < kVecPerThread; ++u) {
         const int v = threadIdx.x + u * kThreads;
         if (v < nv) {
-            r[u] = ld_cs_f4(gp + 4 * v);
-            wv[u] = ld_cs_f4(w + 4 * v);
-            mv[u] = ld_cs_f4(m + 4 * v);
+            r[u] = ld(gp + 4 * v);
+            wv[u] = ld(w + 4 * v);
+            mv[u] = ld(m + 4 * v);
         }
     }
 #pragma unroll
@@ -220,8 +228,8 @@ __global__ void __launch_bounds__(kThreads) k_update_direct(GradTabN<CAP> g, int
                 a.w = round_through_half(a.w);
             }
             sgd_vec(a, 1.0f, lr, mu, wv[u], mv[u]);
-            st_cs_f4(w + 4 * v, wv[u]);
-            st_cs_f4(m + 4 * v, mv[u]);
+            st(w + 4 * v, wv[u]);
+            st(m + 4 * v, mv[u]);
         }
     }
     for (int k = (nv << 2) + threadIdx.x; k < it.len; k += kThreads) {
@@ -741,25 +749,28 @@ cudaError_t launch_update_sgd(const TensorDesc *td, const Item *items, int i0, i
     return cudaGetLastError();
 }
 
-cudaError_t launch_update_direct(const GradTab &g, int ntab, int t_lo, const TensorDesc *td,
-                                 const Item *items, int i0, int i1, int dtype, float lr, float mu,
-                                 cudaStream_t s) {
+template <int CAP>
+void update_direct_cap(const GradTab &g, const GradTab &wt, int t_lo, float *mom,
+                       const Item *items, int i0, int grid, int dtype, float lr, float mu,
+                       cudaStream_t s) {
+    const auto tg = shrink<CAP>(g);
+    const auto tw = shrink<CAP>(wt);
+    if (dtype == 0)
+        k_update_direct<0, CAP><<<grid, kThreads, 0, s>>>(tg, tw, t_lo, mom, items, i0, lr, mu);
+    else
+        k_update_direct<1, CAP><<<grid, kThreads, 0, s>>>(tg, tw, t_lo, mom, items, i0, lr, mu);
+}
+
+cudaError_t launch_update_direct(const GradTab &g, const GradTab &wt, int ntab, int t_lo,
+                                 float *mom, const Item *items, int i0, int i1, int dtype, float lr,
+                                 float mu, cudaStream_t s) {
     const int grid = grid_of(i0, i1);
     if (grid == 0) return cudaSuccess;
     (void)cudaGetLastError();  // report this launch's error, not a stale one
-    if (ntab <= kSmallTab) {
-        const auto t = shrink<kSmallTab>(g);
-        if (dtype == 0)
-            k_update_direct<0, kSmallTab><<<grid, kThreads, 0, s>>>(t, t_lo, td, items, i0, lr, mu);
-        else
-            k_update_direct<1, kSmallTab><<<grid, kThreads, 0, s>>>(t, t_lo, td, items, i0, lr, mu);
-    } else {
-        const auto t = shrink<kGradCap>(g);
-        if (dtype == 0)
-            k_update_direct<0, kGradCap><<<grid, kThreads, 0, s>>>(t, t_lo, td, items, i0, lr, mu);
-        else
-            k_update_direct<1, kGradCap><<<grid, kThreads, 0, s>>>(t, t_lo, td, items, i0, lr, mu);
-    }
+    if (ntab <= kSmallTab)
+        update_direct_cap<kSmallTab>(g, wt, t_lo, mom, items, i0, grid, dtype, lr, mu, s);
+    else
+        update_direct_cap<kGradCap>(g, wt, t_lo, mom, items, i0, grid, dtype, lr, mu, s);
     return cudaGetLastError();
 }
 

@@ -1306,8 +1306,9 @@ cmn_status cmn_step(cmn_comm *c, const float *const *grads, cmn_dtype dtype, flo
     return timed(c, s, [&] {
         return for_groups(c, 0, c->T, [&](int lo, int hi, int i0, int i1) {
             return launched(c,
-                            launch_update_direct(make_tab(grads, lo, hi), hi - lo, lo, c->d_td, c->d_items,
-                                                 i0, i1, dtype, lr, mu, s),
+                            launch_update_direct(make_tab(grads, lo, hi), make_tab(c->params.data(), lo, hi),
+                                                 hi - lo, lo, c->d_mom, c->d_items, i0, i1, dtype, lr,
+                                                 mu, s),
                             "update_direct");
         });
     });
@@ -1415,8 +1416,9 @@ cmn_status cmn_step_host_packed(cmn_comm *c, const float *host_grads, float *hos
             const int a = g0 > i0 ? g0 : i0, b = g1 < i1 ? g1 : i1;
             if (a >= b) return CMN_OK;
             return launched(c,
-                            launch_update_direct(make_tab(dg.data(), lo, hi), hi - lo, lo, c->d_td,
-                                                 c->d_items, a, b, dtype, lr, mu, s),
+                            launch_update_direct(make_tab(dg.data(), lo, hi),
+                                                 make_tab(c->params.data(), lo, hi), hi - lo, lo,
+                                                 c->d_mom, c->d_items, a, b, dtype, lr, mu, s),
                             "update_direct");
         });
         if (st != CMN_OK) return st;

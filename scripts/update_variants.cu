@@ -16,6 +16,9 @@
 //   F  TMA bulk copies: 3 x 16 KB cp.async.bulk loads into smem (mbarrier),
 //      compute in smem, 2 bulk stores; one item per CTA
 //   G  as F, persistent, 2-stage smem ring (loads of item i+1 under item i)
+//   H  as A with the L2::256B prefetch-size hint on the loads
+//   I  as H without .cs
+//   J  8192-element items, 256 threads (8 float4 per thread per array in flight)
 #include <cstdio>
 #include <cstdint>
 #include <vector>
@@ -60,6 +63,41 @@ __global__ void __launch_bounds__(THR) k_item(const float *__restrict__ g, float
             if (CS) { __stcs(w4 + q, b[u]); __stcs(v4 + q, c[u]); }
             else { w4[q] = b[u]; v4[q] = c[u]; }
         }
+    }
+}
+
+// H / I: variant A with an L2 prefetch-size hint on the loads (256-B
+// sectors fetched per miss), with (.cs) or without the streaming operator.
+template <bool CS>
+__device__ __forceinline__ float4 ld_hint(const float4 *p) {
+    float4 r;
+    if (CS)
+        asm volatile("ld.global.cs.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+    else
+        asm volatile("ld.global.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+    return r;
+}
+template <bool CS>
+__global__ void __launch_bounds__(256) k_hint(const float *__restrict__ g, float *__restrict__ w,
+                                              float *__restrict__ v, float lr, float mu) {
+    constexpr int U = 4;
+    const int64_t base = (int64_t)blockIdx.x * 4096;
+    const float4 *g4 = reinterpret_cast<const float4 *>(g + base);
+    float4 *w4 = reinterpret_cast<float4 *>(w + base);
+    float4 *v4 = reinterpret_cast<float4 *>(v + base);
+    const int nv = (int)(int64_t)((4096) < (N - base) ? (4096) : (N - base)) / 4;
+    float4 a[U], b[U], c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int q = threadIdx.x + u * 256;
+        if (q < nv) { a[u] = ld_hint<CS>(g4 + q); b[u] = ld_hint<CS>(w4 + q); c[u] = ld_hint<CS>(v4 + q); }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int q = threadIdx.x + u * 256;
+        if (q < nv) { upd4(a[u], lr, mu, b[u], c[u]); __stcs(w4 + q, b[u]); __stcs(v4 + q, c[u]); }
     }
 }
 
@@ -244,12 +282,16 @@ int main() {
             case 4: k_persist<<<nsm * 4, 256>>>(g, w, v, 0.1f, 0.9f, items4k); break;
             case 5: k_tma<<<items4k, 256, 3 * TB>>>(g, w, v, 0.1f, 0.9f); break;
             case 6: k_tma2<<<nsm * 2, 256, 6 * TB>>>(g, w, v, 0.1f, 0.9f, items4k); break;
+            case 7: k_hint<true><<<items4k, 256>>>(g, w, v, 0.1f, 0.9f); break;
+            case 8: k_hint<false><<<items4k, 256>>>(g, w, v, 0.1f, 0.9f); break;
+            case 9: k_item<8192, 256, true><<<(int)((N + 8191) / 8192), 256>>>(g, w, v, 0.1f, 0.9f); break;
         }
     };
     const char *names[] = {"A item4096 .cs", "B item4096 default-cache", "C item2048 .cs",
                            "D item8192 512thr", "E persistent 4/SM", "F TMA bulk 1 item/CTA",
-                           "G TMA bulk persistent 2-stage"};
-    for (int which = 0; which < 7; ++which) {
+                           "G TMA bulk persistent 2-stage", "H item4096 .cs + L2::256B prefetch",
+                           "I item4096 L2::256B prefetch", "J item8192 256thr (8 float4/thread/array)"};
+    for (int which = 0; which < 10; ++which) {
         // correctness: one step from the saved state must equal variant A's
         CK(cudaMemcpy(w, w0, N * 4, cudaMemcpyDeviceToDevice));
         CK(cudaMemcpy(v, v0, N * 4, cudaMemcpyDeviceToDevice));
