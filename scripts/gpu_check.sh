@@ -13,4 +13,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
     python bench.py --steps 5 --warmup 3 --min-warmup-s 0 --no-cpu-baseline --no-e2e > $O/bench_ncu.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_update_direct -s 3 -c 1 \
     -o $O/prof_update_direct -f python bench.py --steps 3 --warmup 3 --min-warmup-s 0 --no-cpu-baseline --no-e2e > $O/prof.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_update_direct -s 3 -c 1 \
+    -o $O/prof_update_direct_fp16 -f python bench.py --dtype fp16 --steps 3 --warmup 3 --min-warmup-s 0 --no-cpu-baseline --no-e2e > $O/prof16.log 2>&1
 echo ALL DONE
