@@ -59,11 +59,23 @@ __device__ __forceinline__ void sgd_vec(const float4 &r, float inv_n, float lr, 
     sgd_elem(r.w, inv_n, lr, mu, w.w, v.w);
 }
 
+// 16-byte accesses with (CS) or without the streaming hint.
+template <bool CS>
+__device__ __forceinline__ float4 ld_f4(const float *p) {
+    if constexpr (CS) return ld_cs_f4(p);
+    else return *reinterpret_cast<const float4 *>(p);
+}
+template <bool CS>
+__device__ __forceinline__ void st_f4(float *p, const float4 &v) {
+    if constexpr (CS) st_cs_f4(p, v);
+    else *reinterpret_cast<float4 *>(p) = v;
+}
+
 // Reduced-buffer element loads in the payload dtype, widened to fp32.
-template <int DT>
+template <int DT, bool CS = true>
 __device__ __forceinline__ float4 load_r4(const void *r, int64_t j) {
     if constexpr (DT == 0) {
-        return ld_cs_f4(static_cast<const float *>(r) + j);
+        return ld_f4<CS>(static_cast<const float *>(r) + j);
     } else {
         const uint2 h = ld_cs_u2(static_cast<const uint16_t *>(r) + j);
         return make_float4(half_lo(h.x), half_hi(h.x), half_lo(h.y), half_hi(h.y));
@@ -144,11 +156,15 @@ __global__ void __launch_bounds__(kThreads) k_pack(GradTabN<CAP> g, int t_lo,
 }
 
 // ------------------------------------------------------------------- a3
+// Streaming hints only for the fp16 payload: the .cs A/B
+// (profiles/r1_hints_ab.jsonl) measured plain accesses 1-4 % faster for the
+// fp32 payload and .cs ~4 % faster for fp16.
 template <int DT>
 __global__ void __launch_bounds__(kThreads) k_update_sgd(const TensorDesc *__restrict__ td,
                                                          const Item *__restrict__ items, int i0,
                                                          const void *__restrict__ reduced,
                                                          float inv_n, float lr, float mu) {
+    constexpr bool CS = DT == 1;
     const Item it = items[i0 + blockIdx.x];
     const TensorDesc d = td[it.t];
     float *__restrict__ w = d.w + it.k0;
@@ -161,9 +177,9 @@ __global__ void __launch_bounds__(kThreads) k_update_sgd(const TensorDesc *__res
     for (int u = 0; u < kVecPerThread; ++u) {
         const int v = threadIdx.x + u * kThreads;
         if (v < nv) {
-            r[u] = load_r4<DT>(reduced, base + 4 * v);
-            wv[u] = ld_cs_f4(w + 4 * v);
-            mv[u] = ld_cs_f4(m + 4 * v);
+            r[u] = load_r4<DT, CS>(reduced, base + 4 * v);
+            wv[u] = ld_f4<CS>(w + 4 * v);
+            mv[u] = ld_f4<CS>(m + 4 * v);
         }
     }
 #pragma unroll
@@ -171,8 +187,8 @@ __global__ void __launch_bounds__(kThreads) k_update_sgd(const TensorDesc *__res
         const int v = threadIdx.x + u * kThreads;
         if (v < nv) {
             sgd_vec(r[u], inv_n, lr, mu, wv[u], mv[u]);
-            st_cs_f4(w + 4 * v, wv[u]);
-            st_cs_f4(m + 4 * v, mv[u]);
+            st_f4<CS>(w + 4 * v, wv[u]);
+            st_f4<CS>(m + 4 * v, mv[u]);
         }
     }
     for (int k = (nv << 2) + threadIdx.x; k < it.len; k += kThreads) {
