@@ -800,3 +800,24 @@ def test_kernel_timing(cmn):
         assert comm.kernel_timing()[1] == 2
     finally:
         comm.finalize()
+
+
+@pytest.mark.parametrize("algo", ["oneshot", "twoshot"])
+def test_fp16_rounded_once_on_gpu(cmn, algo):
+    """The oracle pin test_fp16_payload_rounded_once on the CUDA path: the
+    fp16 sum is accumulated in fp32 and rounded once (1 + 2^-11 + 2^-11 ->
+    0x3c01; 65504 + 16 + 16 -> +inf), in both all-reduce kernels."""
+    for vals, want in (([1.0, 2.0 ** -11, 2.0 ** -11], 0x3C01), ([65504.0, 16.0, 16.0], 0x7C00)):
+        comm = cmn.Comm.simulated_world(3)
+        try:
+            comm.register_params([torch.zeros(1, device=DEV)])
+            comm.set_algo(algo)
+            comm.allreduce_grads([[torch.tensor([v], dtype=torch.float32, device=DEV)] for v in vals],
+                                 "fp16")
+            _, L = comm.layout()
+            for r in range(3):
+                q = torch.empty(L, dtype=torch.int16, device=DEV)
+                comm.copy_reduced(r, q)
+                assert int(q.cpu().numpy().view(np.uint16)[0]) == want, (vals, r)
+        finally:
+            comm.finalize()

@@ -112,3 +112,21 @@ def test_exact_avg_closed_form(orc):
     avg, mag = orc.exact_avg(x)
     assert list(avg) == [2.0, 0.0, 0.125]
     assert list(mag) == [2.0, 2.0, 0.375]
+
+
+def test_fp16_payload_rounded_once(orc):
+    """Reading R4: fp16 payloads are accumulated in fp32 and the reduced sum
+    is rounded to fp16 exactly once.  Hand-derived case where rounding per
+    addition (an fp16 accumulator, or re-rounding per hop) gives another
+    answer: 1 + 2^-11 + 2^-11 with fp16 ulp(1) = 2^-10.
+      once:     fl16(1 + 2^-11 + 2^-11) = fl16(1 + 2^-10) = 0x3c01
+      per add:  fl16(1 + 2^-11) = 1 (tie to even), then again 1 = 0x3c00
+    Also 65504 + 16 + 16 (fp16 max, half an ulp = 16): once -> 65536 -> +inf
+    (0x7c00); per add: 65504 + 16 ties to even 65504, then 65504 (0x7bff)."""
+    cases = [([1.0, 2.0 ** -11, 2.0 ** -11], 0x3C01),
+             ([65504.0, 16.0, 16.0], 0x7C00)]
+    for vals, want in cases:
+        bufs = [np.array([v], dtype=np.float32) for v in vals]
+        packed = [orc.pack([b], np.array([0, 64]), 64, "fp16") for b in bufs]
+        r = orc.reduce_tree(packed, "fp16")
+        assert int(r.view(np.uint16)[0]) == want, (vals, hex(int(r.view(np.uint16)[0])))
