@@ -367,10 +367,51 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             return float(t.item()) * 1e3
 
+        def capture_step():
+            """One step of the current schedule captured into a CUDA graph
+            (graph-safe schedules only: their buffer reuse is barrier-ordered
+            and barrier epochs live on the device, so replays stay paired
+            across ranks); None if the schedule refuses capture."""
+            from paper_1908_00213_b200.cmn import CmnError as _E
+            comm.step(g, args.dtype, 0.1, 0.9, stream)          # internal streams exist
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            try:
+                with torch.cuda.graph(graph):
+                    comm.step(g, args.dtype, 0.1, 0.9)          # on the capture stream
+            except _E:
+                return None
+            return graph
+
+        def trial_graph_us(graph):
+            for _ in range(3):
+                graph.replay()
+            torch.cuda.synchronize()
+            barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(10):
+                graph.replay()
+            b.record(stream)
+            torch.cuda.synchronize()
+            t = torch.tensor([a.elapsed_time(b) / 10], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item()) * 1e3
+
         trials = {}
         for name in cands:
             set_schedule(name)
             trials[name] = trial_us()
+        # The same schedules replayed from a captured CUDA graph (no host
+        # launch cost per step: the pipelined step is ~7 API calls per piece).
+        for name in ("pipelined4", "pipelined8", "fused", "fused_push"):
+            if args.schedule != "auto":
+                break
+            set_schedule(name)
+            gr = capture_step()
+            if gr is not None:
+                trials[name + "_graph"] = trial_graph_us(gr)
+            del gr
         # Comparisons, not candidates for the headline: the same step with the
         # all-reduce done by NCCL (the north star's measured comparison) and
         # by the NVLS in-switch kernel (tolerance-only parity).  Resource
@@ -397,7 +438,21 @@ def main():
                         set_schedule(name)
                         trials[name] = trial_us()
         schedule = min(trials, key=trials.get)
-        set_schedule(schedule)
+        set_schedule(schedule[:-len("_graph")] if schedule.endswith("_graph") else schedule)
+
+    # what the timed region runs per step: the eager call, or the replay of
+    # the chosen schedule's captured graph
+    def eager_step():
+        comm.step(g, args.dtype, 0.1, 0.9, stream)
+
+    run_step = eager_step
+    if schedule.endswith("_graph"):
+        step_graph = capture_step()
+        run_step = step_graph.replay
+    launches_before = comm.kernel_launches
+    eager_step()                       # kernels one step launches (graph replays launch the same)
+    torch.cuda.synchronize()
+    launches_per_step = comm.kernel_launches - launches_before
 
     sampler = ClockSampler(local)
     sampler.start()
@@ -407,7 +462,7 @@ def main():
     t_w = time.time()
     n_w = 0
     while n_w < args.warmup or time.time() - t_w < args.min_warmup_s:
-        comm.step(g, args.dtype, 0.1, 0.9, stream)
+        run_step()
         n_w += 1
         if n_w % 64 == 0:
             torch.cuda.synchronize()
@@ -421,14 +476,13 @@ def main():
     e_stop = torch.cuda.Event(enable_timing=True)
     barrier()
     torch.cuda.synchronize()
-    launches0 = comm.kernel_launches
     e_start.record(stream)
     for k in range(args.steps):
-        comm.step(g, args.dtype, 0.1, 0.9, stream)
+        run_step()
     e_stop.record(stream)
     torch.cuda.synchronize()
     barrier()
-    launches = comm.kernel_launches - launches0
+    launches = launches_per_step * args.steps
     t_load1 = time.time()
     total_ms = e_start.elapsed_time(e_stop)
     if world > 1:
@@ -444,7 +498,7 @@ def main():
     comm.set_kernel_timing(True)
     barrier()
     for k in range(args.steps):
-        comm.step(g, args.dtype, 0.1, 0.9, stream)
+        eager_step()                   # (launches inside a graph replay are not bracketed)
     torch.cuda.synchronize()
     k_ms, k_count = comm.kernel_timing()
     comm.set_kernel_timing(False)
@@ -463,7 +517,7 @@ def main():
         flush.add_(1)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        comm.step(g, args.dtype, 0.1, 0.9, stream)
+        run_step()
         b.record(stream)
         cold.append((a, b))
     torch.cuda.synchronize()
