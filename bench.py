@@ -509,6 +509,24 @@ def main():
     kernel_ms_per_step = k_ms / args.steps
     kernel_launches_per_step = k_count / args.steps
 
+    # Per-step distribution (median / mean / std over the
+    # timed steps, max over ranks): a third pass with events between steps.
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    barrier()
+    evs[0].record(stream)
+    for k in range(args.steps):
+        run_step()
+        evs[k + 1].record(stream)
+    torch.cuda.synchronize()
+    per = [evs[k].elapsed_time(evs[k + 1]) * 1e3 for k in range(args.steps)]
+    dstats = torch.tensor([statistics.median(per), statistics.fmean(per),
+                           statistics.pstdev(per), min(per), max(per)], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(dstats, op=dist.ReduceOp.MAX)
+    per_step = dict(zip(["median_us", "mean_us", "std_us", "min_us", "max_us"],
+                        [float(x) for x in dstats]))
+    per_step["n"] = args.steps
+
     # Transparency: the same step with a 256 MiB L2 write-flush before each
     # (untimed) -- the flush leaves up to 126 MB of dirty lines that the
     # step must write back, so this is a pessimistic "cold" figure.
@@ -646,6 +664,7 @@ def main():
            "l2": "inputs larger than L2: 20 B/param = 511 MB streamed per step vs 126 MB L2, "
                  "K steps back to back",
            "step_us_after_l2_write_flush": cold_us,
+           "per_step_us": per_step,
            "warmup_steps_run": n_w,
            "parallelism": f"dp{world}"}
     line = {"metric": METRIC, "value": us, "unit": "us", "n_gpus": world, "steps": args.steps,
