@@ -20,6 +20,16 @@ import oracle
 import synth
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or platform.machine()
+
+
 def main():
     ap = argparse.ArgumentParser(prog="python -m oracle")
     ap.add_argument("--config", default="mlp", choices=sorted(synth.WORKLOADS))
@@ -44,7 +54,7 @@ def main():
         res = oracle.step(g, w, v, a.lr, a.mu, a.dtype)
         times.append(time.perf_counter() - t0)
     out = {"config": a.config, "workers": a.workers, "dtype": a.dtype, "steps": a.steps, "set": a.set,
-           "params": int(sum(x.size for x in w)), "threads": 1, "cpu": platform.processor() or platform.machine(),
+           "params": int(sum(x.size for x in w)), "threads": 1, "cpu": cpu_model(), "nproc": os.cpu_count(),
            "w_checksum": float(np.sum([np.sum(x, dtype=np.float64) for x in w])),
            "v_checksum": float(np.sum([np.sum(x, dtype=np.float64) for x in v]))}
     if a.time:
