@@ -3,10 +3,11 @@
 // out over PCIe, by copy engines vs by SM loads/stores on mapped pinned host
 // memory (zero-copy), alone and concurrently?  Prints one JSON line per case.
 //
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/pcie_probe scripts/pcie_probe.cu
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o /tmp/pcie_probe scripts/pcie_probe.cu -lcuda
 #include <cstdio>
 #include <cstdint>
 #include <vector>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
@@ -57,6 +58,36 @@ __global__ void k_zc_update(const float4 *__restrict__ hg, float4 *__restrict__ 
                 b[u].w = __fmaf_rn(mu, b[u].w, g[u].w); a[u].w = __fmaf_rn(-lr, b[u].w, a[u].w);
                 w[i] = a[u]; v[i] = b[u]; hw[i] = a[u];
             }
+        }
+    }
+}
+
+// Flag-driven pipeline: the copy engine's H2D of piece p is followed on its
+// stream by cuStreamWriteValue32(in_flag[p] = seq); one persistent kernel
+// waits on in_flag[p], processes piece p, and the last CTA to finish it
+// publishes out_flag[p] = seq, which cuStreamWaitValue32 on the D2H stream
+// waits for before copying piece p back.  No event round trips per piece.
+__global__ void k_flag_pipe(const uint4 *__restrict__ src, uint4 *__restrict__ dst, int64_t nv,
+                            int pieces, const unsigned *in_flag, unsigned *out_flag,
+                            unsigned *counters, unsigned seq) {
+    for (int p = 0; p < pieces; ++p) {
+        const int64_t v0 = nv * p / pieces, v1 = nv * (p + 1) / pieces;
+        if (threadIdx.x == 0) {
+            unsigned f;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(in_flag + p) : "memory");
+            } while ((int)(f - seq) < 0);
+        }
+        __syncthreads();
+        for (int64_t i = v0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < v1;
+             i += (int64_t)gridDim.x * blockDim.x)
+            dst[i] = src[i];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            const unsigned old = atomicAdd(counters + p, 1u);
+            if (old + 1 == seq * gridDim.x)
+                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(out_flag + p), "r"(seq) : "memory");
         }
     }
 }
@@ -193,6 +224,47 @@ int main() {
         std::printf("{\"case\": \"pipeline\", \"weights\": [");
         for (int p = 0; p < np; ++p) std::printf("%s%d", p ? ", " : "", wts[p]);
         std::printf("], \"ms\": %.4f}\n", ms);
+    }
+    // flag-driven pipeline (stream memory operations), P pieces
+    {
+        unsigned *flags;
+        const int maxp = 128;
+        CK(cudaMalloc(&flags, 3 * maxp * sizeof(unsigned)));
+        CK(cudaMemset(flags, 0, 3 * maxp * sizeof(unsigned)));
+        unsigned *in_flag = flags, *out_flag = flags + maxp, *counters = flags + 2 * maxp;
+        unsigned seq = 0;
+        for (int P : {8, 16, 32, 64, 128}) {
+            CK(cudaMemset(flags, 0, 3 * maxp * sizeof(unsigned)));
+            seq = 0;
+            auto step = [&]() {
+                ++seq;
+                cudaEventRecord(fork, s0);
+                cudaStreamWaitEvent(s1, fork, 0);
+                cudaStreamWaitEvent(s2, fork, 0);
+                k_flag_pipe<<<2 * nsm, 256, 0, s0>>>(reinterpret_cast<const uint4 *>(dg), reinterpret_cast<uint4 *>(dw),
+                                                     nv, P, in_flag, out_flag, counters, seq);
+                for (int p = 0; p < P; ++p) {
+                    const int64_t v0 = nv * p / P, v1 = nv * (p + 1) / P;
+                    cudaMemcpyAsync(dg + 4 * v0, hg + 4 * v0, (v1 - v0) * 16, cudaMemcpyHostToDevice, s1);
+                    cuStreamWriteValue32(s1, reinterpret_cast<CUdeviceptr>(in_flag + p), seq, 0);
+                    cuStreamWaitValue32(s2, reinterpret_cast<CUdeviceptr>(out_flag + p), seq, CU_STREAM_WAIT_VALUE_GEQ);
+                    cudaMemcpyAsync(hw + 4 * v0, dw + 4 * v0, (v1 - v0) * 16, cudaMemcpyDeviceToHost, s2);
+                }
+                cudaEvent_t j1, j2;
+                cudaEventCreateWithFlags(&j1, cudaEventDisableTiming);
+                cudaEventCreateWithFlags(&j2, cudaEventDisableTiming);
+                cudaEventRecord(j1, s1); cudaEventRecord(j2, s2);
+                cudaStreamWaitEvent(s0, j1, 0); cudaStreamWaitEvent(s0, j2, 0);
+                cudaEventDestroy(j1); cudaEventDestroy(j2);
+            };
+            step();
+            CK(cudaDeviceSynchronize());
+            t.start(s0);
+            for (int r = 0; r < reps; ++r) step();
+            const float ms = t.stop(s0) / reps;
+            CK(cudaGetLastError());
+            std::printf("{\"case\": \"flag_pipeline\", \"pieces\": %d, \"ms\": %.4f}\n", P, ms);
+        }
     }
     CK(cudaDeviceSynchronize());
     return 0;
