@@ -543,6 +543,18 @@ def main():
     clocks = sampler.summary(t_load0, t_load1)
     sampler.stop()
 
+    # Replica consistency: after the timed steps
+    # every rank's parameters must be bitwise identical.
+    replicas_equal = None
+    if world > 1:
+        bits = flat_w.view(torch.int32).to(torch.int64)
+        wgt = torch.arange(bits.numel(), device=dev, dtype=torch.int64) % 1009 + 1
+        digest = torch.stack([bits.sum(), (bits * wgt).sum()]).cpu()
+        all_d = [torch.zeros_like(digest) for _ in range(world)]
+        dist.all_gather(all_d, digest)
+        replicas_equal = all(torch.equal(d, all_d[0]) for d in all_d)
+        del bits, wgt
+
     # ---- e2e: host buffers through cmn_step_host_packed (pinned H2D grads
     # in, updated params D2H out; pipelined over tensor ranges at N = 1)
     e2e = None
@@ -665,6 +677,7 @@ def main():
                  "K steps back to back",
            "step_us_after_l2_write_flush": cold_us,
            "per_step_us": per_step,
+           "replicas_bitwise_equal": replicas_equal,
            "warmup_steps_run": n_w,
            "parallelism": f"dp{world}"}
     line = {"metric": METRIC, "value": us, "unit": "us", "n_gpus": world, "steps": args.steps,
