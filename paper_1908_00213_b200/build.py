@@ -17,8 +17,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcmn.so")
-SOURCES = ["cmn_kernels.cu", "cmn_runtime.cpp", "cmn_nvls.cpp"]
-HEADERS = ["cmn_internal.h", "cmn_device.cuh", "cmn_nvls.h", os.path.join("..", "..", "include", "cmn.h")]
+SOURCES = ["cmn_kernels.cu", "cmn_core.cpp", "cmn_schedules.cpp", "cmn_api.cpp", "cmn_nvls.cpp"]
+HEADERS = ["cmn_internal.h", "cmn_device.cuh", "cmn_nvls.h", "cmn_comm.h", os.path.join("..", "..", "include", "cmn.h")]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",

@@ -1,4 +1,4 @@
-// cmn_internal.h -- types shared by the host runtime (cmn_runtime.cpp) and
+// cmn_internal.h -- types shared by the host runtime (cmn_comm.h and its .cpp files) and
 // the sm_100a kernels (cmn_kernels.cu).  Not part of the public ABI.
 #pragma once
 
