@@ -663,7 +663,7 @@ def main():
         roof["frac"] = roof["achieved"] / 770.0
 
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:      # the contract: rank 0 at N = 1 only
         cus, desc = oracle_step_time(world, args.dtype, budget_s=args.cpu_budget_s)
         cpu = {"value": cus, "unit": "us", "cores": 1, "kind": "oracle", "sample": desc}
 
