@@ -821,3 +821,39 @@ def test_fp16_rounded_once_on_gpu(cmn, algo):
                 assert int(q.cpu().numpy().view(np.uint16)[0]) == want, (vals, r)
         finally:
             comm.finalize()
+
+
+@pytest.mark.parametrize("value_set", ["identical", "integer", "edge"])
+@pytest.mark.parametrize("dtype", ["fp32", "fp16"])
+def test_value_sets_every_schedule(cmn, orc, value_set, dtype):
+    """The special value sets (identical workers, exact integer/dyadic set,
+    planted inf / NaN / fp16-overflow / subnormal / tie values) through every
+    N > 1 step schedule -- pipelined, fused pull, fused push, sharded --
+    3 steps, bit-exact with the oracle (NaNs by position)."""
+    shapes = synth.mlp_shapes()
+    N = 4
+    lr, mu = (2.0 ** -4, 2.0 ** -1) if value_set == "integer" else (0.1, 0.9)
+    grads = [synth.grads(shapes, workers=N, step=s, value_set=value_set) for s in range(3)]
+    params0 = synth.params(shapes, value_set="integer" if value_set == "integer" else "random")
+    ora, _, _ = run_oracle(orc, shapes, N, dtype, grads, params0, lr, mu)
+    for sched in ("pipelined", "pull", "push", "sharded"):
+        comm = cmn.Comm.simulated_world(N)
+        try:
+            w = to_dev(params0)
+            comm.register_params(w)
+            comm.set_pipeline(3 if sched == "pipelined" else 0)
+            comm.set_fused_update(sched if sched in ("pull", "push") else 0)
+            for s, g in enumerate(grads):
+                gd = [to_dev(gw) for gw in g]
+                if sched == "sharded":
+                    comm.step_sharded(gd, dtype, lr, mu)
+                else:
+                    comm.step(gd, dtype, lr, mu)
+                torch.cuda.synchronize()
+                for t in range(len(w)):
+                    assert_bitwise(w[t].cpu().numpy().reshape(-1), ora[s]["w"][t],
+                                   f"{sched} {value_set} {dtype} w[{t}] step {s}")
+                    assert_bitwise(comm.momentum(t).cpu().numpy().reshape(-1), ora[s]["v"][t],
+                                   f"{sched} {value_set} {dtype} v[{t}] step {s}")
+        finally:
+            comm.finalize()
