@@ -15,7 +15,9 @@
 // contraction, so no tensor cores.  Design: 16-byte vector accesses, one
 // 4096-element work item per CTA for the tensor-indexed kernels (balanced
 // block -> (tensor, chunk) map precomputed at registration), grid-stride
-// 8 KB tiles for the packed-index kernels, streaming cache hints.
+// 8 KB tiles for the packed-index kernels, streaming (.cs) cache hints where
+// they measured faster (profiles/r1_hints_ab.jsonl: not in the N = 1 direct
+// update, nor in the fp32 update-from-packed).
 #include <cstdint>
 
 #include "cmn_device.cuh"
