@@ -98,7 +98,10 @@ __device__ __forceinline__ float load_r1(const void *r, int64_t j) {
 // measured 1 item per CTA best (6.2 TB/s fp32, 6.6 TB/s fp16; 4 per CTA costs
 // 2-6 %: fewer resident CTAs); what made the first version slow was a
 // dependent TensorDesc load per item, now folded into Item.base/pad.
-constexpr int kPackItems = 1;
+#ifndef CMN_PACK_ITEMS
+#define CMN_PACK_ITEMS 1
+#endif
+constexpr int kPackItems = CMN_PACK_ITEMS;
 
 template <int DT>
 __device__ __forceinline__ void pack_store(void *packed, int64_t j, const float4 &x) {
@@ -111,7 +114,7 @@ __device__ __forceinline__ void pack_store(void *packed, int64_t j, const float4
 }
 
 template <int DT, int CAP>
-__global__ void __launch_bounds__(kThreads) k_pack(GradTabN<CAP> g, int t_lo,
+__global__ void __launch_bounds__(kThreads) k_pack(const __grid_constant__ GradTabN<CAP> g, int t_lo,
                                                    const Item *__restrict__ items, int i0, int i1,
                                                    void *__restrict__ packed) {
     const int ib = i0 + blockIdx.x * kPackItems;
@@ -212,7 +215,8 @@ __global__ void __launch_bounds__(kThreads) k_update_sgd(const TensorDesc *__res
 // scripts/update_variants.cu B vs A), so this kernel -- the whole N = 1
 // step -- uses plain LDG/STG.128.
 template <int DT, int CAP>
-__global__ void __launch_bounds__(kThreads) k_update_direct(GradTabN<CAP> g, GradTabN<CAP> wt,
+__global__ void __launch_bounds__(kThreads) k_update_direct(const __grid_constant__ GradTabN<CAP> g,
+                                                            const __grid_constant__ GradTabN<CAP> wt,
                                                             int t_lo, float *__restrict__ mom,
                                                             const Item *__restrict__ items, int i0,
                                                             float lr, float mu) {
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__(kThreads) k_update_direct(GradTabN<CAP> g, Gra
 }
 
 template <int DT, int CAP>
-__global__ void __launch_bounds__(kThreads) k_unpack_avg(GradTabN<CAP> out, int t_lo,
+__global__ void __launch_bounds__(kThreads) k_unpack_avg(const __grid_constant__ GradTabN<CAP> out, int t_lo,
                                                          const TensorDesc *__restrict__ td,
                                                          const Item *__restrict__ items, int i0,
                                                          const void *__restrict__ reduced,
@@ -621,7 +625,7 @@ __global__ void __launch_bounds__(kThreads) k_update_gather(const TensorDesc *__
 // dst.p[o] is owner o's slot for this rank, offset so that packed index j
 // lands at dst.p[o] + j.  Pads after a tensor's last item are zeroed.
 template <int DT, int CAP>
-__global__ void __launch_bounds__(kThreads) k_pack_push(GradTabN<CAP> g, int t_lo,
+__global__ void __launch_bounds__(kThreads) k_pack_push(const __grid_constant__ GradTabN<CAP> g, int t_lo,
                                                         const Item *__restrict__ items, int i0,
                                                         int i1, const __grid_constant__ PeerBufs dst,
                                                         int world,
