@@ -19,6 +19,7 @@
 // they measured faster (profiles/r1_hints_ab.jsonl: not in the N = 1 direct
 // update, nor in the fp32 update-from-packed).
 #include <cstdint>
+#include <cstdlib>
 
 #include "cmn_device.cuh"
 #include "cmn_internal.h"
@@ -220,11 +221,17 @@ __global__ void __launch_bounds__(kThreads) k_update_direct(const __grid_constan
                                                             int t_lo, float *__restrict__ mom,
                                                             const Item *__restrict__ items, int i0,
                                                             float lr, float mu) {
+    // Programmatic dependent launch (when launched with the attribute): let
+    // the next kernel on the stream start its CTAs as this grid drains, and
+    // run this CTA's prologue (static item table, parameter tables) before
+    // waiting for the previous grid's memory.  No-ops otherwise.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const Item it = items[i0 + blockIdx.x];
     const float *__restrict__ gp = g.p[it.t - t_lo] + it.k0;
     float *__restrict__ w = const_cast<float *>(wt.p[it.t - t_lo]) + it.k0;
     float *__restrict__ m = mom + it.base;
     const int nv = it.len >> 2;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     auto ld = [](const float *p) { return *reinterpret_cast<const float4 *>(p); };
     auto st = [](float *p, const float4 &x) { *reinterpret_cast<float4 *>(p) = x; };
 
@@ -771,16 +778,34 @@ cudaError_t launch_update_sgd(const TensorDesc *td, const Item *items, int i0, i
     return cudaGetLastError();
 }
 
+// The N = 1 step kernel is launched with programmatic stream serialization
+// (PDL): consecutive steps overlap one grid's drain with the next grid's
+// CTA launch and prologue (78.0 -> 75.8 us per R50 step,
+// profiles/r1_pdl_ab.jsonl).  Only this kernel: the cross-rank kernels'
+// barrier reasoning relies on a kernel starting after its predecessor
+// completed.  CMN_PDL=0 disables it (measurement).
 template <int CAP>
-void update_direct_cap(const GradTab &g, const GradTab &wt, int t_lo, float *mom,
-                       const Item *items, int i0, int grid, int dtype, float lr, float mu,
-                       cudaStream_t s) {
+cudaError_t update_direct_cap(const GradTab &g, const GradTab &wt, int t_lo, float *mom,
+                              const Item *items, int i0, int grid, int dtype, float lr, float mu,
+                              cudaStream_t s) {
     const auto tg = shrink<CAP>(g);
     const auto tw = shrink<CAP>(wt);
+    static const bool pdl = [] {
+        const char *v = std::getenv("CMN_PDL");
+        return !(v && *v == '0');
+    }();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
     if (dtype == 0)
-        k_update_direct<0, CAP><<<grid, kThreads, 0, s>>>(tg, tw, t_lo, mom, items, i0, lr, mu);
-    else
-        k_update_direct<1, CAP><<<grid, kThreads, 0, s>>>(tg, tw, t_lo, mom, items, i0, lr, mu);
+        return cudaLaunchKernelEx(&cfg, k_update_direct<0, CAP>, tg, tw, t_lo, mom, items, i0, lr, mu);
+    return cudaLaunchKernelEx(&cfg, k_update_direct<1, CAP>, tg, tw, t_lo, mom, items, i0, lr, mu);
 }
 
 cudaError_t launch_update_direct(const GradTab &g, const GradTab &wt, int ntab, int t_lo,
@@ -789,11 +814,10 @@ cudaError_t launch_update_direct(const GradTab &g, const GradTab &wt, int ntab, 
     const int grid = grid_of(i0, i1);
     if (grid == 0) return cudaSuccess;
     (void)cudaGetLastError();  // report this launch's error, not a stale one
-    if (ntab <= kSmallTab)
-        update_direct_cap<kSmallTab>(g, wt, t_lo, mom, items, i0, grid, dtype, lr, mu, s);
-    else
-        update_direct_cap<kGradCap>(g, wt, t_lo, mom, items, i0, grid, dtype, lr, mu, s);
-    return cudaGetLastError();
+    const cudaError_t e =
+        ntab <= kSmallTab ? update_direct_cap<kSmallTab>(g, wt, t_lo, mom, items, i0, grid, dtype, lr, mu, s)
+                          : update_direct_cap<kGradCap>(g, wt, t_lo, mom, items, i0, grid, dtype, lr, mu, s);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_unpack_avg(const GradTab &out, int t_lo, const TensorDesc *td,
