@@ -43,6 +43,7 @@ class MultiNodeOptimizer:
         self._hooks = []
         self._stream = None
         self._launched = set()
+        self._table, self._table_key = None, None
         self._setup(list(params))
 
     # -------------------------------------------------------------- structure
@@ -94,8 +95,19 @@ class MultiNodeOptimizer:
 
     def _grad_table(self) -> PtrTable:
         # Only the bucket's own grads are read; others may be missing yet, so
-        # absent grads point at the parameter (never dereferenced).
-        return PtrTable([p.grad if p.grad is not None else p for p in self.params])
+        # absent grads point at the parameter (never dereferenced).  The
+        # marshalled table is reused while the gradient storage stays put
+        # (persistent .grad buffers, the usual case between zero_grad()s
+        # that keep them).
+        ts = [p.grad if p.grad is not None else p for p in self.params]
+        key = tuple(t.data_ptr() for t in ts)
+        if key != self._table_key:
+            self._table, self._table_key = PtrTable(ts), key
+            # the pointed-to storage is kept alive by the parameters' .grad
+            # (the key matched it); holding the tensors here would pin old
+            # gradients across zero_grad(set_to_none)
+            self._table.tensors = []
+        return self._table
 
     # -------------------------------------------------------------------- step
     def step(self, params=None):
