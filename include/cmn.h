@@ -101,8 +101,10 @@ typedef enum { CMN_FP32 = 0, CMN_FP16 = 1 } cmn_dtype;
  *   NVLS     NEXT-3, NVLink SHARP: rank r reduces chunk r inside the
  *            NVSwitch (multimem.ld_reduce on a multicast object spanning every
  *            rank's packed buffer) and multicast-stores the sum into every
- *            rank's reduced buffer (multimem.st): ~S/N bytes per rank and
- *            direction instead of 2(N-1)/N S.  The switch's summation order is
+ *            rank's reduced buffer (multimem.st): (N+1)/N S bytes per rank and
+ *            direction (the switch reads each rank's copy of every chunk once
+ *            and fans each sum out once) instead of 2(N-1)/N S; the NVLink
+ *            time falls by ~1.6x at N = 8.  The switch's summation order is
  *            its own: tolerance-gate parity, not bitwise, for N > 1.  Selecting
  *            it (after registration, on every rank) creates the multicast
  *            resources; needs an NVSwitch system (CMN_ERR_UNSUPPORTED

@@ -679,8 +679,9 @@ __global__ void __launch_bounds__(kThreads) k_pack_push(const __grid_constant__ 
 // NVLS all-reduce: rank r owns chunk r; for each 16-B vector the NVSwitch
 // reduces the N ranks' packed copies (multimem.ld_reduce on the multicast
 // address) and the result is multicast-stored into every rank's reduced
-// buffer (multimem.st).  Per rank and direction only ~S/N bytes cross
-// NVLink instead of 2(N-1)/N S.  The switch's summation order is its own,
+// buffer (multimem.st).  Per rank and direction (N+1)/N S bytes cross
+// NVLink (every rank's copy of each chunk is read once by the switch, each
+// sum fanned out once) instead of 2(N-1)/N S.  The switch's summation order is its own,
 // so for N > 1 results meet the tolerance gate, not the oracle's tree order.
 // fp16 payloads accumulate in fp32 inside the switch (.acc::f32) and are
 // rounded to fp16 once, as in reading R4.
