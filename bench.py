@@ -661,6 +661,13 @@ def main():
                 "launches_per_step": kernel_launches_per_step, "timing": timing_note,
                 "step_achieved": bus, "traffic": None}
         roof["frac"] = roof["achieved"] / 770.0
+        if schedule.startswith("nvls"):
+            # bus bytes follow the all-reduce convention (2(N-1)/N S); the
+            # bytes the in-switch reduction actually moves per rank and
+            # direction are (N+1)/N S, reported beside it
+            link = (world + 1) / world * S
+            roof["nvls_link_bytes_per_rank_direction"] = link
+            roof["nvls_link_frac"] = link / (kernel_ms_per_step * 1e-3) / 1e9 / 770.0
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:      # the contract: rank 0 at N = 1 only
