@@ -269,6 +269,17 @@ cmn_status cmn_unpack_avg_grads(cmn_comm *comm, float *const *out, void *stream)
 cmn_status cmn_update_adam(cmn_comm *comm, float alpha, float beta1, float beta2,
                            float eps, int step, void *stream);
 
+/* cmn_step_adam -- the whole step (a1-a3) with the Adam update of
+ * cmn_update_adam, same arguments as cmn_allreduce_grads for grads/dtype.
+ * N == 1: one kernel straight from the gradients (no pack; 28 B/param).
+ * N > 1: the pipelined schedule of cmn_step (cmn_set_pipeline >= 2, the
+ * default; per-piece Adam updates overlap the all-reduces), else all-reduce
+ * then update.  Bitwise identical to cmn_allreduce_grads + cmn_update_adam.
+ * Errors as cmn_allreduce_grads; INVALID_ARG for step < 1. */
+cmn_status cmn_step_adam(cmn_comm *comm, const float *const *grads, cmn_dtype dtype,
+                         float alpha, float beta1, float beta2, float eps, int step,
+                         void *stream);
+
 /* ------------------------------------------------------------------------
  * Overlap with backward (a4): contiguous buckets of the layout
  * ------------------------------------------------------------------------ */

@@ -42,6 +42,8 @@ SIGNATURES = [
     ("cmn_step_host_packed", C.c_int, [_P, _P, _P, C.c_int, C.c_float, C.c_float, _P]),
     ("cmn_unpack_avg_grads", C.c_int, [_P, _PP, _P]),
     ("cmn_update_adam", C.c_int, [_P, C.c_float, C.c_float, C.c_float, C.c_float, C.c_int, _P]),
+    ("cmn_step_adam", C.c_int, [_P, _PP, C.c_int, C.c_float, C.c_float, C.c_float, C.c_float, C.c_int,
+                                _P]),
     ("cmn_plan_buckets", C.c_int, [_P, C.c_size_t, C.POINTER(C.c_int)]),
     ("cmn_get_bucket", C.c_int, [_P, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("cmn_allreduce_bucket", C.c_int, [_P, C.c_int, _PP, C.c_int, _P]),
@@ -331,6 +333,11 @@ class Comm:
     def unpack_avg_grads(self, out, stream=None):
         _check(lib().cmn_unpack_avg_grads(self._h, _ptr_array(_data_ptrs(out)), _stream(stream)),
                "cmn_unpack_avg_grads")
+
+    def step_adam(self, grads, dtype="fp32", alpha=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, step=1,
+                  stream=None):
+        _check(lib().cmn_step_adam(self._h, self._grad_table(grads), _dt(dtype), alpha, beta1, beta2,
+                                   eps, step, _stream(stream)), "cmn_step_adam")
 
     def update_adam(self, alpha, beta1, beta2, eps, step, stream=None):
         _check(lib().cmn_update_adam(self._h, alpha, beta1, beta2, eps, step, _stream(stream)),

@@ -425,31 +425,44 @@ cmn_status cmn_update_adam(cmn_comm *c, float alpha, float beta1, float beta2, f
     if (!c->fresh) return fail(CMN_ERR_STATE, "no fresh all-reduce result to consume");
     if (step < 1) return fail(CMN_ERR_INVALID_ARG, "step must be >= 1");
     if (cmn_status st = set_device(c); st != CMN_OK) return st;
-    if (!c->d_adam) {
-        const size_t b = static_cast<size_t>(c->L > 0 ? c->L : 1) * 4 * 2;
-        if (cudaMalloc(&c->d_adam, b) != cudaSuccess) return fail(CMN_ERR_OOM, "adam state alloc");
-        CMN_CUDA(cudaMemset(c->d_adam, 0, b));
-        for (int t = 0; t < c->T; ++t) {
-            c->h_td[t].adam_m = c->d_adam + c->off[t];
-            c->h_td[t].adam_v = c->d_adam + c->L + c->off[t];
-        }
-        CMN_CUDA(cudaMemcpy(c->d_td, c->h_td.data(), sizeof(TensorDesc) * c->T,
-                            cudaMemcpyHostToDevice));
-    }
-    // alpha_t = alpha * sqrt(1 - beta2^t) / (1 - beta1^t), evaluated in double.
-    const double b1t = std::pow(static_cast<double>(beta1), static_cast<double>(step));
-    const double b2t = std::pow(static_cast<double>(beta2), static_cast<double>(step));
-    const float alpha_t = static_cast<float>(static_cast<double>(alpha) * std::sqrt(1.0 - b2t) / (1.0 - b1t));
-    const float c1 = 1.0f - beta1, c2 = 1.0f - beta2;
-    const float inv_n = 1.0f / static_cast<float>(c->world);
+    if (cmn_status st = ensure_adam(c); st != CMN_OK) return st;
+    cmn_status st = update_range_adam(c, 0, c->T, c->last, adam_args(alpha, beta1, beta2, eps, step),
+                                      static_cast<cudaStream_t>(stream));
+    if (st == CMN_OK) c->fresh = false;
+    return st;
+}
+
+cmn_status cmn_step_adam(cmn_comm *c, const float *const *grads, cmn_dtype dtype, float alpha,
+                         float beta1, float beta2, float eps, int step, void *stream) {
+    if (cmn_status st = require_registered(c); st != CMN_OK) return st;
+    if (cmn_status st = require_dtype(dtype); st != CMN_OK) return st;
+    if (step < 1) return fail(CMN_ERR_INVALID_ARG, "step must be >= 1");
+    std::string why;
+    if (!grads_ok(c, grads, c->T * (c->simulated ? c->world : 1), why))
+        return fail(CMN_ERR_INVALID_ARG, why);
+    if (cmn_status st = set_device(c); st != CMN_OK) return st;
+    if (cmn_status st = ensure_adam(c); st != CMN_OK) return st;
+    const AdamArgs a = adam_args(alpha, beta1, beta2, eps, step);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    cmn_status st = for_groups(c, 0, c->T, [&](int, int, int i0, int i1) {
-        return launched(c,
-                        launch_update_adam(c->d_td, c->d_items, i0, i1,
-                                           reduced_ptr(c, c->last, 0), c->last.dtype, inv_n,
-                                           alpha_t, beta1, beta2, c1, c2, eps, s),
-                        "update_adam");
-    });
+    if (c->world == 1 && c->algo != CMN_ALGO_NVLS && c->algo != CMN_ALGO_NCCL) {
+        // N = 1: the all-reduce is the identity; Adam straight from g.
+        c->fresh = false;
+        return timed(c, s, [&] {
+            return for_groups(c, 0, c->T, [&](int lo, int hi, int i0, int i1) {
+                return launched(c,
+                                launch_adam_direct(make_tab(grads, lo, hi),
+                                                   make_tab(c->params.data(), lo, hi), hi - lo, lo,
+                                                   c->d_adam, c->d_adam + c->L, c->d_items, i0, i1,
+                                                   dtype, a.alpha_t, a.beta1, a.beta2, a.c1, a.c2,
+                                                   a.eps, s),
+                                "adam_direct");
+            });
+        });
+    }
+    if (c->world > 1 && c->pipe_pieces >= 2 && c->T >= 2)
+        return step_pipelined(c, grads, dtype, 0.0f, 0.0f, s, nullptr, &a);
+    if (cmn_status st = cmn_allreduce_grads(c, grads, dtype, stream); st != CMN_OK) return st;
+    cmn_status st = update_range_adam(c, 0, c->T, c->last, a, s);
     if (st == CMN_OK) c->fresh = false;
     return st;
 }

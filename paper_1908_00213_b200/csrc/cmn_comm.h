@@ -151,6 +151,12 @@ struct cmn_comm {
 
 namespace cmn::rt {
 
+// Bias-corrected Adam constants of one step (NEXT-1): alpha_t evaluated in
+// double on the host (reading R17), c1 = 1 - beta1, c2 = 1 - beta2.
+struct AdamArgs {
+    float alpha_t, beta1, beta2, c1, c2, eps;
+};
+
 // Host buffers of the e2e step (cmn_step_host_packed): packed layout, L
 // floats per (simulated) rank for the gradients; parameters out or NULL.
 struct HostIO {
@@ -217,7 +223,12 @@ std::vector<std::pair<int, int>> equal_ranges(const cmn_comm *c, int n);
 cmn_status ensure_comm_stream(cmn_comm *c, size_t n_events);
 cmn_status d2h_params(cmn_comm *c, int ta, int tb, float *host_params, cudaStream_t s);
 cmn_status step_pipelined(cmn_comm *c, const float *const *grads, int dtype, float lr, float mu,
-                          cudaStream_t s, const HostIO *io = nullptr);
+                          cudaStream_t s, const HostIO *io = nullptr,
+                          const AdamArgs *adam = nullptr);
+cmn_status ensure_adam(cmn_comm *c);
+AdamArgs adam_args(float alpha, float beta1, float beta2, float eps, int step);
+cmn_status update_range_adam(cmn_comm *c, int ta, int tb, const ArResult &res, const AdamArgs &a,
+                             cudaStream_t s);
 cmn_status step_sharded(cmn_comm *c, const float *const *grads, int dtype, float lr, float mu,
                         cudaStream_t s);
 cmn_status step_fused(cmn_comm *c, const float *const *grads, int dtype, float lr, float mu,

@@ -101,6 +101,13 @@ cudaError_t launch_update_adam(const TensorDesc *td, const Item *items, int i0, 
                                float beta1, float beta2, float c1, float c2, float eps,
                                cudaStream_t s);
 
+// NEXT-1 at N = 1: Adam straight from the gradients (no pack); m, v at
+// adam_m / adam_v + packed index; programmatic dependent launch.
+cudaError_t launch_adam_direct(const GradTab &g, const GradTab &wt, int ntab, int t_lo,
+                               float *adam_m, float *adam_v, const Item *items, int i0, int i1,
+                               int dtype, float alpha_t, float beta1, float beta2, float c1,
+                               float c2, float eps, cudaStream_t s);
+
 // a2 one-shot: out[j] = tree_i(in_i[j]) for j in [e0, e1) (elements; e0, e1
 // multiples of kAlign).  Barrier slot 0 at entry when enabled.
 cudaError_t launch_allreduce_oneshot(const PeerBufs &in, int world, void *out, int64_t e0,

@@ -348,6 +348,74 @@ __global__ void __launch_bounds__(kThreads) k_update_adam(const TensorDesc *__re
     }
 }
 
+// NEXT-1 at N = 1: Adam straight from the gradients (the all-reduce is the
+// identity, so a = cast(g) and the pack is skipped: 28 instead of 36
+// B/param), addresses from kernel-parameter tables and the packed index
+// (m at adam_m + base, v at adam_v + base), launched with programmatic
+// dependent launch like k_update_direct.  Same arithmetic as k_update_adam
+// with inv_n = 1, so bitwise equal to the unfused path.
+template <int DT, int CAP>
+__global__ void __launch_bounds__(kThreads) k_adam_direct(const __grid_constant__ GradTabN<CAP> g,
+                                                          const __grid_constant__ GradTabN<CAP> wt,
+                                                          int t_lo, float *__restrict__ adam_m,
+                                                          float *__restrict__ adam_v,
+                                                          const Item *__restrict__ items, int i0,
+                                                          float alpha_t, float beta1, float beta2,
+                                                          float c1, float c2, float eps) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const Item it = items[i0 + blockIdx.x];
+    const float *__restrict__ gp = g.p[it.t - t_lo] + it.k0;
+    float *__restrict__ w = const_cast<float *>(wt.p[it.t - t_lo]) + it.k0;
+    float *__restrict__ m = adam_m + it.base;
+    float *__restrict__ v = adam_v + it.base;
+    const int nv = it.len >> 2;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    constexpr int U = kVecPerThread / 2;   // two passes keep 4 arrays x 2 float4 in registers
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+        float4 r[U], wv[U], mv[U], vv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int q = threadIdx.x + (pass * U + u) * kThreads;
+            if (q < nv) {
+                r[u] = ld_cs_f4(gp + 4 * q);
+                wv[u] = ld_cs_f4(w + 4 * q);
+                mv[u] = ld_cs_f4(m + 4 * q);
+                vv[u] = ld_cs_f4(v + 4 * q);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int q = threadIdx.x + (pass * U + u) * kThreads;
+            if (q < nv) {
+                float4 a = r[u];
+                if constexpr (DT == 1) {
+                    a.x = round_through_half(a.x);
+                    a.y = round_through_half(a.y);
+                    a.z = round_through_half(a.z);
+                    a.w = round_through_half(a.w);
+                }
+                adam_elem(a.x, 1.0f, alpha_t, beta1, beta2, c1, c2, eps, wv[u].x, mv[u].x, vv[u].x);
+                adam_elem(a.y, 1.0f, alpha_t, beta1, beta2, c1, c2, eps, wv[u].y, mv[u].y, vv[u].y);
+                adam_elem(a.z, 1.0f, alpha_t, beta1, beta2, c1, c2, eps, wv[u].z, mv[u].z, vv[u].z);
+                adam_elem(a.w, 1.0f, alpha_t, beta1, beta2, c1, c2, eps, wv[u].w, mv[u].w, vv[u].w);
+                st_cs_f4(w + 4 * q, wv[u]);
+                st_cs_f4(m + 4 * q, mv[u]);
+                st_cs_f4(v + 4 * q, vv[u]);
+            }
+        }
+    }
+    for (int k = (nv << 2) + threadIdx.x; k < it.len; k += kThreads) {
+        float a = gp[k];
+        if constexpr (DT == 1) a = round_through_half(a);
+        float wk = w[k], mk = m[k], vk = v[k];
+        adam_elem(a, 1.0f, alpha_t, beta1, beta2, c1, c2, eps, wk, mk, vk);
+        w[k] = wk;
+        m[k] = mk;
+        v[k] = vk;
+    }
+}
+
 // ------------------------------------------------------------------- a2
 // 16-byte lanes: fp32 -> 4 values, fp16 -> 8 values.  Word W of each of the
 // N inputs is reduced independently (compile-time indices keep everything
@@ -779,6 +847,14 @@ cudaError_t launch_update_sgd(const TensorDesc *td, const Item *items, int i0, i
     return cudaGetLastError();
 }
 
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *v = std::getenv("CMN_PDL");
+        return !(v && *v == '0');
+    }();
+    return on;
+}
+
 // The N = 1 step kernel is launched with programmatic stream serialization
 // (PDL): consecutive steps overlap one grid's drain with the next grid's
 // CTA launch and prologue (78.0 -> 75.8 us per R50 step,
@@ -791,10 +867,6 @@ cudaError_t update_direct_cap(const GradTab &g, const GradTab &wt, int t_lo, flo
                               cudaStream_t s) {
     const auto tg = shrink<CAP>(g);
     const auto tw = shrink<CAP>(wt);
-    static const bool pdl = [] {
-        const char *v = std::getenv("CMN_PDL");
-        return !(v && *v == '0');
-    }();
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(grid));
     cfg.blockDim = dim3(kThreads);
@@ -803,7 +875,7 @@ cudaError_t update_direct_cap(const GradTab &g, const GradTab &wt, int t_lo, flo
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
     if (dtype == 0)
         return cudaLaunchKernelEx(&cfg, k_update_direct<0, CAP>, tg, tw, t_lo, mom, items, i0, lr, mu);
     return cudaLaunchKernelEx(&cfg, k_update_direct<1, CAP>, tg, tw, t_lo, mom, items, i0, lr, mu);
@@ -849,6 +921,45 @@ cudaError_t launch_update_adam(const TensorDesc *td, const Item *items, int i0, 
         k_update_adam<1><<<grid, kThreads, 0, s>>>(td, items, i0, reduced, inv_n, alpha_t, beta1,
                                                    beta2, c1, c2, eps);
     return cudaGetLastError();
+}
+
+template <int CAP>
+cudaError_t adam_direct_cap(const GradTab &g, const GradTab &wt, int t_lo, float *adam_m,
+                            float *adam_v, const Item *items, int i0, int grid, int dtype,
+                            float alpha_t, float beta1, float beta2, float c1, float c2, float eps,
+                            cudaStream_t s) {
+    const auto tg = shrink<CAP>(g);
+    const auto tw = shrink<CAP>(wt);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    if (dtype == 0)
+        return cudaLaunchKernelEx(&cfg, k_adam_direct<0, CAP>, tg, tw, t_lo, adam_m, adam_v, items, i0,
+                                  alpha_t, beta1, beta2, c1, c2, eps);
+    return cudaLaunchKernelEx(&cfg, k_adam_direct<1, CAP>, tg, tw, t_lo, adam_m, adam_v, items, i0,
+                              alpha_t, beta1, beta2, c1, c2, eps);
+}
+
+cudaError_t launch_adam_direct(const GradTab &g, const GradTab &wt, int ntab, int t_lo,
+                               float *adam_m, float *adam_v, const Item *items, int i0, int i1,
+                               int dtype, float alpha_t, float beta1, float beta2, float c1,
+                               float c2, float eps, cudaStream_t s) {
+    const int grid = grid_of(i0, i1);
+    if (grid == 0) return cudaSuccess;
+    (void)cudaGetLastError();
+    const cudaError_t e =
+        ntab <= kSmallTab
+            ? adam_direct_cap<kSmallTab>(g, wt, t_lo, adam_m, adam_v, items, i0, grid, dtype, alpha_t,
+                                         beta1, beta2, c1, c2, eps, s)
+            : adam_direct_cap<kGradCap>(g, wt, t_lo, adam_m, adam_v, items, i0, grid, dtype, alpha_t,
+                                        beta1, beta2, c1, c2, eps, s);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 namespace {

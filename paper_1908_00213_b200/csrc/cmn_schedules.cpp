@@ -5,6 +5,7 @@
 // sharded update (NEXT-4) and the host-buffer pipeline of the e2e step.
 #include "cmn_comm.h"
 
+#include <cmath>
 #include <iterator>
 
 namespace cmn::rt {
@@ -173,6 +174,42 @@ cmn_status update_range(cmn_comm *c, int ta, int tb, const ArResult &res, float 
     });
 }
 
+// NEXT-1 state: m and v, L floats each in the packed layout, zeroed on
+// first use after a registration.
+cmn_status ensure_adam(cmn_comm *c) {
+    if (c->d_adam) return CMN_OK;
+    const size_t b = static_cast<size_t>(c->L > 0 ? c->L : 1) * 4 * 2;
+    if (cudaMalloc(&c->d_adam, b) != cudaSuccess) return fail(CMN_ERR_OOM, "adam state alloc");
+    CMN_CUDA(cudaMemset(c->d_adam, 0, b));
+    for (int t = 0; t < c->T; ++t) {
+        c->h_td[t].adam_m = c->d_adam + c->off[t];
+        c->h_td[t].adam_v = c->d_adam + c->L + c->off[t];
+    }
+    CMN_CUDA(cudaMemcpy(c->d_td, c->h_td.data(), sizeof(TensorDesc) * c->T, cudaMemcpyHostToDevice));
+    return CMN_OK;
+}
+
+// alpha_t = alpha * sqrt(1 - beta2^t) / (1 - beta1^t), evaluated in double.
+AdamArgs adam_args(float alpha, float beta1, float beta2, float eps, int step) {
+    const double b1t = std::pow(static_cast<double>(beta1), static_cast<double>(step));
+    const double b2t = std::pow(static_cast<double>(beta2), static_cast<double>(step));
+    const float alpha_t =
+        static_cast<float>(static_cast<double>(alpha) * std::sqrt(1.0 - b2t) / (1.0 - b1t));
+    return AdamArgs{alpha_t, beta1, beta2, 1.0f - beta1, 1.0f - beta2, eps};
+}
+
+cmn_status update_range_adam(cmn_comm *c, int ta, int tb, const ArResult &res, const AdamArgs &a,
+                             cudaStream_t s) {
+    const float inv_n = 1.0f / static_cast<float>(c->world);
+    return for_groups(c, ta, tb, [&](int, int, int i0, int i1) {
+        return launched(c,
+                        launch_update_adam(c->d_td, c->d_items, i0, i1, reduced_ptr(c, res, 0),
+                                           res.dtype, inv_n, a.alpha_t, a.beta1, a.beta2, a.c1,
+                                           a.c2, a.eps, s),
+                        "update_adam");
+    });
+}
+
 // Item ranges [i0, i1) of the N = 1 host-buffer pipeline (item = 4096
 // elements of one tensor, so a tensor may straddle pieces), sized by
 // kE2EWeights -- or CMN_E2E_PIECES equal pieces (measurement).
@@ -266,7 +303,7 @@ cmn_status d2h_params(cmn_comm *c, int ta, int tb, float *host_params, cudaStrea
 // other pieces (gradients land in the library's staging buffer, whose
 // pointers `grads` are).
 cmn_status step_pipelined(cmn_comm *c, const float *const *grads, int dtype, float lr, float mu,
-                          cudaStream_t s, const HostIO *io) {
+                          cudaStream_t s, const HostIO *io, const AdamArgs *adam) {
     const auto pieces = equal_ranges(c, c->pipe_pieces);
     const size_t P = pieces.size();
     if (cmn_status st = ensure_comm_stream(c, 2 * P + 1); st != CMN_OK) return st;
@@ -320,7 +357,9 @@ cmn_status step_pipelined(cmn_comm *c, const float *const *grads, int dtype, flo
     }
     for (size_t p = 0; p < P; ++p) {
         CMN_CUDA(cudaStreamWaitEvent(s, c->pev[2 * p + 1], 0));
-        if (cmn_status st = update_range(c, pieces[p].first, pieces[p].second, res[p], lr, mu, s);
+        if (cmn_status st = adam ? update_range_adam(c, pieces[p].first, pieces[p].second, res[p],
+                                                     *adam, s)
+                                 : update_range(c, pieces[p].first, pieces[p].second, res[p], lr, mu, s);
             st != CMN_OK)
             return st;
         if (io && io->params) {

@@ -133,9 +133,8 @@ class MultiNodeOptimizer:
             self._pending = [hi - lo for lo, hi in self.buckets]
         elif self.optimizer == "adam":
             self.t += 1
-            self.comm.allreduce_grads(self._grad_table(), self.dtype)
             a, b1, b2, eps = self.adam
-            self.comm.update_adam(a, b1, b2, eps, self.t)
+            self.comm.step_adam(self._grad_table(), self.dtype, a, b1, b2, eps, self.t)
         else:
             self.comm.step(self._grad_table(), self.dtype, self.lr, self.mu)
 

@@ -123,6 +123,13 @@ def main():
                         comm.update_adam(1e-3, 0.9, 0.999, 1e-8, 1)
                     t_adam = timed(adam, args.iters, stream) - t_ar
                     rec["adam_update_us"] = t_adam
+                    # the whole N = 1 Adam step straight from the gradients
+                    # (28 B/param: read g, w, m, v; write w, m, v)
+                    t_adam_step = timed(lambda: comm.step_adam(gg, dtype, 1e-3, 0.9, 0.999, 1e-8, 1),
+                                        args.iters, stream)
+                    rec["adam_step_us"] = t_adam_step
+                    rec["adam_step_gbs"] = 28 * P / (t_adam_step * 1e-6) / 1e9
+                    rec["adam_step_frac"] = rec["adam_step_gbs"] / peak
                     rec["adam_update_gbs"] = (24 + c) * P / (t_adam * 1e-6) / 1e9
                     rec["adam_update_frac"] = rec["adam_update_gbs"] / peak
                     rec["fused_step_us"] = t_step

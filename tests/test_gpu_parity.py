@@ -857,3 +857,37 @@ def test_value_sets_every_schedule(cmn, orc, value_set, dtype):
                                    f"{sched} {value_set} {dtype} v[{t}] step {s}")
         finally:
             comm.finalize()
+
+
+@pytest.mark.parametrize("N,dtype,pieces", [(1, "fp32", 0), (1, "fp16", 0), (2, "fp32", 3),
+                                            (4, "fp16", 4), (8, "fp32", 0), (3, "fp16", 2)])
+def test_step_adam_parity(cmn, orc, N, dtype, pieces):
+    """cmn_step_adam (NEXT-1 as a whole step): at N = 1 one kernel straight
+    from the gradients, at N > 1 the pipelined schedule (or all-reduce then
+    update with pieces = 0); w, m, v bit-exact with the oracle over 3 steps."""
+    shapes = synth.resnet50_shapes()[:20] + RAGGED
+    sizes = [synth.numel(s) for s in shapes]
+    off, L = orc.layout(sizes)
+    params0 = synth.params(shapes)
+    w_o = [p.copy() for p in params0]
+    m_o = [np.zeros_like(p) for p in params0]
+    v_o = [np.zeros_like(p) for p in params0]
+    comm = cmn.Comm.init(0, 1, 0) if N == 1 else cmn.Comm.simulated_world(N)
+    try:
+        w = to_dev(params0)
+        comm.register_params(w)
+        comm.set_pipeline(pieces)
+        for step in range(1, 4):
+            g = synth.grads(shapes, workers=N, step=step)
+            red = orc.reduce_tree([orc.pack(gw, off, L, dtype) for gw in g], dtype)
+            orc.update_adam(red, dtype, N, 1e-3, 0.9, 0.999, 1e-8, step, off, w_o, m_o, v_o)
+            gd = to_dev(g[0]) if N == 1 else [to_dev(gw) for gw in g]
+            comm.step_adam(gd, dtype, 1e-3, 0.9, 0.999, 1e-8, step)
+            torch.cuda.synchronize()
+            for t in range(len(w)):
+                m, v = comm.adam_state(t)
+                assert_bitwise(w[t].cpu().numpy().reshape(-1), w_o[t], f"adam w[{t}] step {step}")
+                assert_bitwise(m.cpu().numpy().reshape(-1), m_o[t], f"adam m[{t}] step {step}")
+                assert_bitwise(v.cpu().numpy().reshape(-1), v_o[t], f"adam v[{t}] step {step}")
+    finally:
+        comm.finalize()
