@@ -99,7 +99,9 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode, pieces=0):
                 continue                              # fault injection: rank 1 skips a collective
             if mode == "reregister" and s == 1:
                 comm.register_params(w)               # collective; resets momentum (reading R7)
-            if mode == "host":
+            if mode == "adam":
+                comm.step_adam(g, dtype, 1e-3, 0.9, 0.999, 1e-8, s + 1)   # pipelined when pieces >= 2
+            elif mode == "host":
                 # e2e form through pinned host buffers (pipelined: H2D/D2H per piece)
                 sizes = [x.numel() for x in w]
                 off, L = cmn.plan_layout(shapes)[:2]
@@ -299,6 +301,26 @@ def test_ipc_fused_allgather_update(orc, world, dtype, mode):
     for r in res:
         assert np.array_equal(np.frombuffer(r[2], np.uint32), np.concatenate(w).view(np.uint32))
         assert np.array_equal(np.frombuffer(r[3], np.uint32), np.concatenate(v).view(np.uint32))
+
+
+@pytest.mark.parametrize("world,dtype,pieces", [(2, "fp32", 3), (3, "fp16", 0)])
+def test_ipc_step_adam(orc, world, dtype, pieces):
+    """cmn_step_adam across processes (pipelined per-piece Adam, or
+    all-reduce then update): every rank's w bit-exact with the oracle."""
+    res = _run(world, dtype, "twoshot", mode="adam", pieces=pieces)
+    assert all(r[1] == "ok" for r in res), res
+    shapes = synth.mlp_shapes()
+    sizes = [synth.numel(x) for x in shapes]
+    off, L = orc.layout(sizes)
+    w = synth.params(shapes)
+    m = [np.zeros_like(x) for x in w]
+    v = [np.zeros_like(x) for x in w]
+    for s in range(2):
+        g = synth.grads(shapes, workers=world, step=s)
+        red = orc.reduce_tree([orc.pack(gw, off, L, dtype) for gw in g], dtype)
+        orc.update_adam(red, dtype, world, 1e-3, 0.9, 0.999, 1e-8, s + 1, off, w, m, v)
+    for r in res:
+        assert np.array_equal(np.frombuffer(r[2], np.uint32), np.concatenate(w).view(np.uint32)), r[0]
 
 
 @pytest.mark.parametrize("world,dtype,pieces", [(2, "fp32", 3), (3, "fp16", 0)])
