@@ -103,6 +103,11 @@ __device__ __forceinline__ float load_r1(const void *r, int64_t j) {
 #define CMN_PACK_ITEMS 1
 #endif
 constexpr int kPackItems = CMN_PACK_ITEMS;
+#ifndef CMN_PACK_THREADS
+#define CMN_PACK_THREADS 256
+#endif
+constexpr int kPackThreads = CMN_PACK_THREADS;          // threads per pack CTA
+constexpr int kPackVec = kItemElems / 4 / kPackThreads;  // float4s per thread per item
 
 template <int DT>
 __device__ __forceinline__ void pack_store(void *packed, int64_t j, const float4 &x) {
@@ -115,11 +120,11 @@ __device__ __forceinline__ void pack_store(void *packed, int64_t j, const float4
 }
 
 template <int DT, int CAP>
-__global__ void __launch_bounds__(kThreads) k_pack(const __grid_constant__ GradTabN<CAP> g, int t_lo,
+__global__ void __launch_bounds__(kPackThreads) k_pack(const __grid_constant__ GradTabN<CAP> g, int t_lo,
                                                    const Item *__restrict__ items, int i0, int i1,
                                                    void *__restrict__ packed) {
     const int ib = i0 + blockIdx.x * kPackItems;
-    float4 x[kPackItems][kVecPerThread];
+    float4 x[kPackItems][kPackVec];
 #pragma unroll
     for (int j = 0; j < kPackItems; ++j) {
         if (ib + j < i1) {
@@ -127,8 +132,8 @@ __global__ void __launch_bounds__(kThreads) k_pack(const __grid_constant__ GradT
             const float *__restrict__ src = g.p[it.t - t_lo] + it.k0;
             const int nv = it.len >> 2;
 #pragma unroll
-            for (int u = 0; u < kVecPerThread; ++u) {
-                const int v = threadIdx.x + u * kThreads;
+            for (int u = 0; u < kPackVec; ++u) {
+                const int v = threadIdx.x + u * kPackThreads;
                 if (v < nv) x[j][u] = ld_cs_f4(src + 4 * v);
             }
         }
@@ -139,20 +144,20 @@ __global__ void __launch_bounds__(kThreads) k_pack(const __grid_constant__ GradT
         const Item it = items[ib + j];
         const int nv = it.len >> 2;
 #pragma unroll
-        for (int u = 0; u < kVecPerThread; ++u) {
-            const int v = threadIdx.x + u * kThreads;
+        for (int u = 0; u < kPackVec; ++u) {
+            const int v = threadIdx.x + u * kPackThreads;
             if (v < nv) pack_store<DT>(packed, it.base + 4 * v, x[j][u]);
         }
         // ragged tail (numel % 4) and the alignment pad after the tensor
         const float *__restrict__ src = g.p[it.t - t_lo] + it.k0;
-        for (int k = (nv << 2) + threadIdx.x; k < it.len; k += kThreads) {
+        for (int k = (nv << 2) + threadIdx.x; k < it.len; k += kPackThreads) {
             const float sv = src[k];
             if constexpr (DT == 0)
                 static_cast<float *>(packed)[it.base + k] = sv;
             else
                 static_cast<uint16_t *>(packed)[it.base + k] = __half_as_ushort(__float2half_rn(sv));
         }
-        for (int k = threadIdx.x; k < it.pad; k += kThreads) {
+        for (int k = threadIdx.x; k < it.pad; k += kPackThreads) {
             if constexpr (DT == 0)
                 static_cast<float *>(packed)[it.base + it.len + k] = 0.0f;
             else
@@ -821,15 +826,15 @@ cudaError_t launch_pack(const GradTab &g, int ntab, int t_lo, const TensorDesc *
     if (ntab <= kSmallTab) {
         const auto t = shrink<kSmallTab>(g);
         if (dtype == 0)
-            k_pack<0, kSmallTab><<<grid, kThreads, 0, s>>>(t, t_lo, items, i0, i1, packed);
+            k_pack<0, kSmallTab><<<grid, kPackThreads, 0, s>>>(t, t_lo, items, i0, i1, packed);
         else
-            k_pack<1, kSmallTab><<<grid, kThreads, 0, s>>>(t, t_lo, items, i0, i1, packed);
+            k_pack<1, kSmallTab><<<grid, kPackThreads, 0, s>>>(t, t_lo, items, i0, i1, packed);
     } else {
         const auto t = shrink<kGradCap>(g);
         if (dtype == 0)
-            k_pack<0, kGradCap><<<grid, kThreads, 0, s>>>(t, t_lo, items, i0, i1, packed);
+            k_pack<0, kGradCap><<<grid, kPackThreads, 0, s>>>(t, t_lo, items, i0, i1, packed);
         else
-            k_pack<1, kGradCap><<<grid, kThreads, 0, s>>>(t, t_lo, items, i0, i1, packed);
+            k_pack<1, kGradCap><<<grid, kPackThreads, 0, s>>>(t, t_lo, items, i0, i1, packed);
     }
     return cudaGetLastError();
 }
