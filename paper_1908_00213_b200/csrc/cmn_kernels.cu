@@ -792,16 +792,21 @@ __global__ void __launch_bounds__(kThreads) k_nvls(const char *mc_packed, char *
     const uint32_t bv = barrier_value(bar);
     cross_rank_barrier(bar, bv, world, 0);           // every rank's pack is complete
     fence_proxy_alias();
-    for (int64_t tile = v0 + static_cast<int64_t>(blockIdx.x) * kTileVecs; tile < v1;
-         tile += static_cast<int64_t>(gridDim.x) * kTileVecs) {
-        uint4 x[kARVec];
+    // A load-reduce makes a round trip through the switch to every rank, so
+    // keep more bytes in flight than the P2P kernels (which issue N loads per
+    // vector): 8 x 16 B per thread, ~4.8 MB across one CTA per SM.
+    constexpr int kNvlsVec = 8;
+    constexpr int kNvlsTile = kThreads * kNvlsVec;
+    for (int64_t tile = v0 + static_cast<int64_t>(blockIdx.x) * kNvlsTile; tile < v1;
+         tile += static_cast<int64_t>(gridDim.x) * kNvlsTile) {
+        uint4 x[kNvlsVec];
 #pragma unroll
-        for (int u = 0; u < kARVec; ++u) {
+        for (int u = 0; u < kNvlsVec; ++u) {
             const int64_t idx = tile + threadIdx.x + u * kThreads;
             if (idx < v1) x[u] = mm_ld_reduce<DT>(mc_packed + 16 * idx);
         }
 #pragma unroll
-        for (int u = 0; u < kARVec; ++u) {
+        for (int u = 0; u < kNvlsVec; ++u) {
             const int64_t idx = tile + threadIdx.x + u * kThreads;
             if (idx < v1) mm_st(mc_reduced + 16 * idx, x[u]);
         }
