@@ -289,6 +289,18 @@ __global__ void __launch_bounds__(kThreads) k_unpack_avg(const __grid_constant__
         dst[k] = __fmul_rn(load_r1<DT>(reduced, base + k), inv_n);
 }
 
+#ifndef CMN_ADAM_DIRECT_CS
+#define CMN_ADAM_DIRECT_CS 1
+#endif
+constexpr bool kAdamCS = CMN_ADAM_DIRECT_CS != 0;   // streaming hints in k_adam_direct
+#ifndef CMN_ADAM_PASSES
+#define CMN_ADAM_PASSES 1
+#endif
+// Loads in flight per thread: 1 pass = 4 arrays x 4 float4 (measured 2 %
+// faster than 2 passes of 2 and 3 % faster than 4 passes of 1 at N = 1,
+// profiles/r1_adam_ab.jsonl).
+constexpr int kAdamPasses = CMN_ADAM_PASSES;
+
 // NEXT-1: bias-corrected Adam, every operation IEEE round-to-nearest and
 // uncontracted, in the order written in the oracle (orc_update_adam).
 // 28 B/param algorithmic (read r, w, m, v; write w, m, v).
@@ -315,9 +327,12 @@ __global__ void __launch_bounds__(kThreads) k_update_adam(const TensorDesc *__re
     float *__restrict__ m = d.adam_m + it.k0;
     float *__restrict__ v = d.adam_v + it.k0;
     const int nv = it.len >> 2;
-    constexpr int U = kVecPerThread / 2;   // two passes keep 4 arrays x 2 float4 in registers
+    // fp16 payload (its reduced buffer half-resident in L2): 2 passes
+    // measured faster (103.0 vs 112.3 us); fp32: 1 pass (108.4 vs 110.5 us)
+    constexpr int kPasses = DT == 1 ? 2 : kAdamPasses;
+    constexpr int U = kVecPerThread / kPasses;
 #pragma unroll 1
-    for (int pass = 0; pass < 2; ++pass) {
+    for (int pass = 0; pass < kPasses; ++pass) {
         float4 r[U], wv[U], mv[U], vv[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -353,6 +368,8 @@ __global__ void __launch_bounds__(kThreads) k_update_adam(const TensorDesc *__re
     }
 }
 
+
+
 // NEXT-1 at N = 1: Adam straight from the gradients (the all-reduce is the
 // identity, so a = cast(g) and the pack is skipped: 28 instead of 36
 // B/param), addresses from kernel-parameter tables and the packed index
@@ -375,18 +392,18 @@ __global__ void __launch_bounds__(kThreads) k_adam_direct(const __grid_constant_
     float *__restrict__ v = adam_v + it.base;
     const int nv = it.len >> 2;
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    constexpr int U = kVecPerThread / 2;   // two passes keep 4 arrays x 2 float4 in registers
+    constexpr int U = kVecPerThread / kAdamPasses;   // float4s per array per pass
 #pragma unroll 1
-    for (int pass = 0; pass < 2; ++pass) {
+    for (int pass = 0; pass < kAdamPasses; ++pass) {
         float4 r[U], wv[U], mv[U], vv[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int q = threadIdx.x + (pass * U + u) * kThreads;
             if (q < nv) {
-                r[u] = ld_cs_f4(gp + 4 * q);
-                wv[u] = ld_cs_f4(w + 4 * q);
-                mv[u] = ld_cs_f4(m + 4 * q);
-                vv[u] = ld_cs_f4(v + 4 * q);
+                r[u] = ld_f4<kAdamCS>(gp + 4 * q);
+                wv[u] = ld_f4<kAdamCS>(w + 4 * q);
+                mv[u] = ld_f4<kAdamCS>(m + 4 * q);
+                vv[u] = ld_f4<kAdamCS>(v + 4 * q);
             }
         }
 #pragma unroll
@@ -404,9 +421,9 @@ __global__ void __launch_bounds__(kThreads) k_adam_direct(const __grid_constant_
                 adam_elem(a.y, 1.0f, alpha_t, beta1, beta2, c1, c2, eps, wv[u].y, mv[u].y, vv[u].y);
                 adam_elem(a.z, 1.0f, alpha_t, beta1, beta2, c1, c2, eps, wv[u].z, mv[u].z, vv[u].z);
                 adam_elem(a.w, 1.0f, alpha_t, beta1, beta2, c1, c2, eps, wv[u].w, mv[u].w, vv[u].w);
-                st_cs_f4(w + 4 * q, wv[u]);
-                st_cs_f4(m + 4 * q, mv[u]);
-                st_cs_f4(v + 4 * q, vv[u]);
+                st_f4<kAdamCS>(w + 4 * q, wv[u]);
+                st_f4<kAdamCS>(m + 4 * q, mv[u]);
+                st_f4<kAdamCS>(v + 4 * q, vv[u]);
             }
         }
     }
