@@ -17,7 +17,7 @@ from paper_1908_00213_b200 import Comm  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--mode", default="n1", choices=["n1", "sim8", "adam", "fused8", "push8", "sharded8"])
+    ap.add_argument("--mode", default="n1", choices=["n1", "sim8", "adam", "adam_step", "fused8", "push8", "sharded8"])
     ap.add_argument("--dtype", default="fp32")
     ap.add_argument("--algo", default="twoshot")
     ap.add_argument("--iters", type=int, default=3)
@@ -45,6 +45,8 @@ def main():
         comm.update_momentum_sgd(0.1, 0.9)
         if N == 1:
             comm.step(gt, a.dtype, 0.1, 0.9)
+    for k in range(a.iters if a.mode == "adam_step" else 0):
+        comm.step_adam(gt, a.dtype, 1e-3, 0.9, 0.999, 1e-8, k + 1)
     for k in range(a.iters if a.mode == "adam" else 0):
         comm.allreduce_grads(gt, a.dtype)
         comm.update_adam(1e-3, 0.9, 0.999, 1e-8, k + 1)
