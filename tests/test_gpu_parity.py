@@ -891,3 +891,32 @@ def test_step_adam_parity(cmn, orc, N, dtype, pieces):
                 assert_bitwise(v.cpu().numpy().reshape(-1), v_o[t], f"adam v[{t}] step {step}")
     finally:
         comm.finalize()
+
+
+@pytest.mark.parametrize("N", [1, 3])
+def test_degenerate_models(cmn, orc, N):
+    """Degenerate registrations: every tensor empty (L = 0: the step is a
+    no-op that must not fail), and a single 1-element tensor (smaller than
+    one vector, one chunk owner, pads everywhere) -- every schedule."""
+    for shapes in ([(0,), (0, 5)], [(1,)]):
+        grads = [synth.grads(shapes, workers=N, step=s) for s in range(2)]
+        params0 = synth.params(shapes)
+        ora, _, _ = run_oracle(orc, shapes, N, "fp32", grads, params0, 0.1, 0.9)
+        for sched in (("serial", "pipelined", "pull", "push", "sharded") if N > 1 else ("direct",)):
+            comm = cmn.Comm.init(0, 1, 0) if N == 1 else cmn.Comm.simulated_world(N)
+            try:
+                w = [torch.from_numpy(p.copy()).to(DEV).reshape(s) for p, s in zip(params0, shapes)]
+                comm.register_params(w)
+                comm.set_pipeline(2 if sched == "pipelined" else 0)
+                comm.set_fused_update(sched if sched in ("pull", "push") else 0)
+                for s, g in enumerate(grads):
+                    gd = to_dev(g[0]) if N == 1 else [to_dev(gw) for gw in g]
+                    if sched == "sharded":
+                        comm.step_sharded(gd, "fp32", 0.1, 0.9)
+                    else:
+                        comm.step(gd, "fp32", 0.1, 0.9)
+                    torch.cuda.synchronize()
+                    for t in range(len(w)):
+                        assert_bitwise(w[t].cpu().numpy().reshape(-1), ora[s]["w"][t], f"{shapes} {sched} w[{t}]")
+            finally:
+                comm.finalize()
