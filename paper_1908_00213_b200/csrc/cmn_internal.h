@@ -11,8 +11,14 @@ namespace cmn {
 
 constexpr int kMaxWorld = 8;          // == CMN_MAX_WORLD
 constexpr int kAlign = 64;            // == CMN_ALIGN_ELEMS
-constexpr int kThreads = 256;         // threads per CTA, every kernel
-constexpr int kItemElems = 4096;      // elements per work item (tensor-indexed kernels)
+#ifndef CMN_THREADS
+#define CMN_THREADS 256
+#endif
+#ifndef CMN_ITEM_ELEMS
+#define CMN_ITEM_ELEMS 4096
+#endif
+constexpr int kThreads = CMN_THREADS;       // threads per CTA, every kernel
+constexpr int kItemElems = CMN_ITEM_ELEMS;  // elements per work item (tensor-indexed kernels)
 constexpr int kMaxBarrierBlocks = 1024;
 constexpr int kBarrierSlots = 2;      // 0: start (inputs ready), 1: mid (reduce-scatter done)
 constexpr int kGradCap = 256;         // grad pointers carried per launch (kernel params)
