@@ -99,7 +99,22 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode, pieces=0):
                 continue                              # fault injection: rank 1 skips a collective
             if mode == "reregister" and s == 1:
                 comm.register_params(w)               # collective; resets momentum (reading R7)
-            if mode == "adam":
+            if mode == "stress":
+                # long run, schedule / grid / algorithm drawn per step from a
+                # seed shared by all ranks
+                import random
+                rnd = random.Random(1000 + s)
+                sched = rnd.choice(["serial1", "serial2", "pipelined", "pull", "push", "graphless"])
+                comm.set_algo("oneshot" if sched == "serial1" else "twoshot")
+                comm.set_fused_update({"pull": 1, "push": 2}.get(sched, 0))
+                comm.set_pipeline(rnd.choice([2, 3, 5]) if sched == "pipelined" else 0)
+                comm.set_ctas(rnd.choice([0, 1, 7, 148]), rnd.choice([0, 3, 64]))
+                if sched == "graphless":
+                    comm.allreduce_grads(g, dtype)
+                    comm.update_momentum_sgd(0.1, 0.9)
+                else:
+                    comm.step(g, dtype, 0.1, 0.9)
+            elif mode == "adam":
                 comm.step_adam(g, dtype, 1e-3, 0.9, 0.999, 1e-8, s + 1)   # pipelined when pieces >= 2
             elif mode == "host":
                 # e2e form through pinned host buffers (pipelined: H2D/D2H per piece)
@@ -281,6 +296,26 @@ def test_ipc_r50_full_size(orc, dtype, mode, pieces):
     hv = hashlib.sha256(np.concatenate(v).tobytes()).hexdigest()
     for r in res:
         assert r[2] == hw and r[3] == hv, f"rank {r[0]}"
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("world,dtype", [(3, "fp32"), (2, "fp16")])
+def test_ipc_stress_random_schedules(orc, world, dtype):
+    """60 steps across real processes with the schedule, algorithm and grid
+    sizes redrawn every step (same draw on every rank): the per-CTA barrier
+    epochs, buffer parities and inbox reuse stay paired; w and v bit-exact
+    with 60 oracle steps on every rank."""
+    steps = 60
+    res = _run(world, dtype, "twoshot", steps=steps, mode="stress")
+    assert all(r[1] == "ok" for r in res), res
+    shapes = synth.mlp_shapes()
+    w = synth.params(shapes)
+    v = [np.zeros_like(x) for x in w]
+    for s in range(steps):
+        orc.step(synth.grads(shapes, workers=world, step=s), w, v, 0.1, 0.9, dtype)
+    for r in res:
+        assert np.array_equal(np.frombuffer(r[2], np.uint32), np.concatenate(w).view(np.uint32)), r[0]
+        assert np.array_equal(np.frombuffer(r[3], np.uint32), np.concatenate(v).view(np.uint32)), r[0]
 
 
 def test_ipc_single_call_schedule_refuses_capture():
