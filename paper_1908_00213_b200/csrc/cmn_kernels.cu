@@ -20,6 +20,7 @@
 // update, nor in the fp32 update-from-packed).
 #include <cstdint>
 #include <cstdlib>
+#include <utility>
 
 #include "cmn_device.cuh"
 #include "cmn_internal.h"
@@ -123,12 +124,20 @@ template <int DT, int CAP>
 __global__ void __launch_bounds__(kPackThreads) k_pack(const __grid_constant__ GradTabN<CAP> g, int t_lo,
                                                    const Item *__restrict__ items, int i0, int i1,
                                                    void *__restrict__ packed) {
+    // PDL (see launch_pack): the item table is static, so it is read before
+    // waiting for the previous grid; gradients and the packed buffer after.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int ib = i0 + blockIdx.x * kPackItems;
+    Item its[kPackItems];
+#pragma unroll
+    for (int j = 0; j < kPackItems; ++j)
+        if (ib + j < i1) its[j] = items[ib + j];
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     float4 x[kPackItems][kPackVec];
 #pragma unroll
     for (int j = 0; j < kPackItems; ++j) {
         if (ib + j < i1) {
-            const Item it = items[ib + j];
+            const Item it = its[j];
             const float *__restrict__ src = g.p[it.t - t_lo] + it.k0;
             const int nv = it.len >> 2;
 #pragma unroll
@@ -141,7 +150,7 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const __grid_constant__ G
 #pragma unroll
     for (int j = 0; j < kPackItems; ++j) {
         if (ib + j >= i1) break;
-        const Item it = items[ib + j];
+        const Item it = its[j];
         const int nv = it.len >> 2;
 #pragma unroll
         for (int u = 0; u < kPackVec; ++u) {
@@ -176,12 +185,15 @@ __global__ void __launch_bounds__(kThreads) k_update_sgd(const TensorDesc *__res
                                                          const void *__restrict__ reduced,
                                                          float inv_n, float lr, float mu) {
     constexpr bool CS = DT == 1;
+    // PDL (see launch_update_sgd): descriptors are static, read before the wait.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const Item it = items[i0 + blockIdx.x];
     const TensorDesc d = td[it.t];
     float *__restrict__ w = d.w + it.k0;
     float *__restrict__ m = d.mom + it.k0;
     const int64_t base = d.off + it.k0;
     const int nv = it.len >> 2;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     float4 r[kVecPerThread], wv[kVecPerThread], mv[kVecPerThread];
 #pragma unroll
@@ -836,6 +848,40 @@ inline int grid_of(int i0, int i1) { return i1 > i0 ? i1 - i0 : 0; }
 
 }  // namespace
 
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *v = std::getenv("CMN_PDL");
+        return !(v && *v == '0');
+    }();
+    return on;
+}
+
+namespace {
+// Programmatic dependent launch for the stream-local HBM kernels (k_pack,
+// k_update_sgd, k_update_direct, k_adam_direct): each issues
+// griddepcontrol.launch_dependents at entry and griddepcontrol.wait before
+// its first access to data a predecessor may produce, so the next grid's CTAs
+// launch and read their static descriptors while this one drains.  The wait
+// returns only after the previous grid completed and its memory is visible,
+// so the ordering every schedule relies on is unchanged.  Not used for the
+// cross-rank kernels (barrier kernels keep plain launches); a PDL kernel
+// after one of them, or after an event wait or copy, simply starts after it.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int threads, cudaStream_t s,
+                       Args &&...args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(static_cast<unsigned>(threads));
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+}  // namespace
+
 // ----------------------------------------------------------------- launchers
 
 cudaError_t launch_pack(const GradTab &g, int ntab, int t_lo, const TensorDesc *td,
@@ -845,20 +891,17 @@ cudaError_t launch_pack(const GradTab &g, int ntab, int t_lo, const TensorDesc *
     (void)td;
     (void)cudaGetLastError();  // report this launch's error, not a stale one
     const int grid = (n + kPackItems - 1) / kPackItems;
+    cudaError_t e;
     if (ntab <= kSmallTab) {
         const auto t = shrink<kSmallTab>(g);
-        if (dtype == 0)
-            k_pack<0, kSmallTab><<<grid, kPackThreads, 0, s>>>(t, t_lo, items, i0, i1, packed);
-        else
-            k_pack<1, kSmallTab><<<grid, kPackThreads, 0, s>>>(t, t_lo, items, i0, i1, packed);
+        e = dtype == 0 ? launch_pdl(k_pack<0, kSmallTab>, grid, kPackThreads, s, t, t_lo, items, i0, i1, packed)
+                       : launch_pdl(k_pack<1, kSmallTab>, grid, kPackThreads, s, t, t_lo, items, i0, i1, packed);
     } else {
         const auto t = shrink<kGradCap>(g);
-        if (dtype == 0)
-            k_pack<0, kGradCap><<<grid, kPackThreads, 0, s>>>(t, t_lo, items, i0, i1, packed);
-        else
-            k_pack<1, kGradCap><<<grid, kPackThreads, 0, s>>>(t, t_lo, items, i0, i1, packed);
+        e = dtype == 0 ? launch_pdl(k_pack<0, kGradCap>, grid, kPackThreads, s, t, t_lo, items, i0, i1, packed)
+                       : launch_pdl(k_pack<1, kGradCap>, grid, kPackThreads, s, t, t_lo, items, i0, i1, packed);
     }
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_update_sgd(const TensorDesc *td, const Item *items, int i0, int i1,
@@ -867,19 +910,10 @@ cudaError_t launch_update_sgd(const TensorDesc *td, const Item *items, int i0, i
     const int grid = grid_of(i0, i1);
     if (grid == 0) return cudaSuccess;
     (void)cudaGetLastError();  // report this launch's error, not a stale one
-    if (dtype == 0)
-        k_update_sgd<0><<<grid, kThreads, 0, s>>>(td, items, i0, reduced, inv_n, lr, mu);
-    else
-        k_update_sgd<1><<<grid, kThreads, 0, s>>>(td, items, i0, reduced, inv_n, lr, mu);
-    return cudaGetLastError();
-}
-
-bool pdl_enabled() {
-    static const bool on = [] {
-        const char *v = std::getenv("CMN_PDL");
-        return !(v && *v == '0');
-    }();
-    return on;
+    const cudaError_t e =
+        dtype == 0 ? launch_pdl(k_update_sgd<0>, grid, kThreads, s, td, items, i0, reduced, inv_n, lr, mu)
+                   : launch_pdl(k_update_sgd<1>, grid, kThreads, s, td, items, i0, reduced, inv_n, lr, mu);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 // The N = 1 step kernel is launched with programmatic stream serialization
