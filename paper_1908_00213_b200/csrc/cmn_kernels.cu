@@ -333,12 +333,14 @@ __global__ void __launch_bounds__(kThreads) k_update_adam(const TensorDesc *__re
                                                           float inv_n, float alpha_t, float beta1,
                                                           float beta2, float c1, float c2,
                                                           float eps) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // PDL, see launch_pdl
     const Item it = items[i0 + blockIdx.x];
     const TensorDesc d = td[it.t];
     float *__restrict__ w = d.w + it.k0;
     float *__restrict__ m = d.adam_m + it.k0;
     float *__restrict__ v = d.adam_v + it.k0;
     const int nv = it.len >> 2;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     // fp16 payload (its reduced buffer half-resident in L2): 2 passes
     // measured faster (103.0 vs 112.3 us); fp32: 1 pass (108.4 vs 110.5 us)
     constexpr int kPasses = DT == 1 ? 2 : kAdamPasses;
@@ -858,7 +860,7 @@ bool pdl_enabled() {
 
 namespace {
 // Programmatic dependent launch for the stream-local HBM kernels (k_pack,
-// k_update_sgd, k_update_direct, k_adam_direct): each issues
+// k_update_sgd, k_update_adam, k_update_direct, k_adam_direct): each issues
 // griddepcontrol.launch_dependents at entry and griddepcontrol.wait before
 // its first access to data a predecessor may produce, so the next grid's CTAs
 // launch and read their static descriptors while this one drains.  The wait
@@ -919,27 +921,16 @@ cudaError_t launch_update_sgd(const TensorDesc *td, const Item *items, int i0, i
 // The N = 1 step kernel is launched with programmatic stream serialization
 // (PDL): consecutive steps overlap one grid's drain with the next grid's
 // CTA launch and prologue (78.0 -> 75.8 us per R50 step,
-// profiles/r1_pdl_ab.jsonl).  Only this kernel: the cross-rank kernels'
-// barrier reasoning relies on a kernel starting after its predecessor
-// completed.  CMN_PDL=0 disables it (measurement).
+// profiles/r1_pdl_ab.jsonl).  CMN_PDL=0 disables it (measurement).
 template <int CAP>
 cudaError_t update_direct_cap(const GradTab &g, const GradTab &wt, int t_lo, float *mom,
                               const Item *items, int i0, int grid, int dtype, float lr, float mu,
                               cudaStream_t s) {
     const auto tg = shrink<CAP>(g);
     const auto tw = shrink<CAP>(wt);
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(static_cast<unsigned>(grid));
-    cfg.blockDim = dim3(kThreads);
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
     if (dtype == 0)
-        return cudaLaunchKernelEx(&cfg, k_update_direct<0, CAP>, tg, tw, t_lo, mom, items, i0, lr, mu);
-    return cudaLaunchKernelEx(&cfg, k_update_direct<1, CAP>, tg, tw, t_lo, mom, items, i0, lr, mu);
+        return launch_pdl(k_update_direct<0, CAP>, grid, kThreads, s, tg, tw, t_lo, mom, items, i0, lr, mu);
+    return launch_pdl(k_update_direct<1, CAP>, grid, kThreads, s, tg, tw, t_lo, mom, items, i0, lr, mu);
 }
 
 cudaError_t launch_update_direct(const GradTab &g, const GradTab &wt, int ntab, int t_lo,
@@ -975,13 +966,12 @@ cudaError_t launch_update_adam(const TensorDesc *td, const Item *items, int i0, 
     const int grid = grid_of(i0, i1);
     if (grid == 0) return cudaSuccess;
     (void)cudaGetLastError();  // report this launch's error, not a stale one
-    if (dtype == 0)
-        k_update_adam<0><<<grid, kThreads, 0, s>>>(td, items, i0, reduced, inv_n, alpha_t, beta1,
-                                                   beta2, c1, c2, eps);
-    else
-        k_update_adam<1><<<grid, kThreads, 0, s>>>(td, items, i0, reduced, inv_n, alpha_t, beta1,
-                                                   beta2, c1, c2, eps);
-    return cudaGetLastError();
+    const cudaError_t e =
+        dtype == 0 ? launch_pdl(k_update_adam<0>, grid, kThreads, s, td, items, i0, reduced, inv_n,
+                                alpha_t, beta1, beta2, c1, c2, eps)
+                   : launch_pdl(k_update_adam<1>, grid, kThreads, s, td, items, i0, reduced, inv_n,
+                                alpha_t, beta1, beta2, c1, c2, eps);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <int CAP>
@@ -991,20 +981,11 @@ cudaError_t adam_direct_cap(const GradTab &g, const GradTab &wt, int t_lo, float
                             cudaStream_t s) {
     const auto tg = shrink<CAP>(g);
     const auto tw = shrink<CAP>(wt);
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(static_cast<unsigned>(grid));
-    cfg.blockDim = dim3(kThreads);
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
     if (dtype == 0)
-        return cudaLaunchKernelEx(&cfg, k_adam_direct<0, CAP>, tg, tw, t_lo, adam_m, adam_v, items, i0,
-                                  alpha_t, beta1, beta2, c1, c2, eps);
-    return cudaLaunchKernelEx(&cfg, k_adam_direct<1, CAP>, tg, tw, t_lo, adam_m, adam_v, items, i0,
-                              alpha_t, beta1, beta2, c1, c2, eps);
+        return launch_pdl(k_adam_direct<0, CAP>, grid, kThreads, s, tg, tw, t_lo, adam_m, adam_v, items,
+                          i0, alpha_t, beta1, beta2, c1, c2, eps);
+    return launch_pdl(k_adam_direct<1, CAP>, grid, kThreads, s, tg, tw, t_lo, adam_m, adam_v, items, i0,
+                      alpha_t, beta1, beta2, c1, c2, eps);
 }
 
 cudaError_t launch_adam_direct(const GradTab &g, const GradTab &wt, int ntab, int t_lo,

@@ -6,8 +6,8 @@ mkdir -p gpurun_out
 O=gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1 || echo "BUILD FAILED" >> $O/build.log
 rm -f $O/pdl2_ab.jsonl
-for rep in 1 2; do for p in 0 1; do
-  CMN_PDL=$p timeout 600 python scripts/kernel_bench.py --worlds 1,8 2>/dev/null | python -c "
+for rep in ${REPS:-1 2}; do for p in 0 1; do
+  CMN_PDL=$p timeout 600 python scripts/kernel_bench.py --worlds ${WORLDS:-1,8} 2>/dev/null | python -c "
 import sys, json
 for l in sys.stdin:
     d = json.loads(l); d['pdl'] = $p; d['rep'] = $rep; print(json.dumps(d))" >> $O/pdl2_ab.jsonl
