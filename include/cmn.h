@@ -355,6 +355,16 @@ cmn_status cmn_set_fused_update(cmn_comm *comm, int mode);
  * its peers). */
 cmn_status cmn_set_ctas(cmn_comm *comm, int collective_ctas, int update_ctas);
 
+/* cmn_set_stream_ctas -- cap on the grid of the stream-local item kernels
+ * (pack, update from the reduced buffer, Adam update): 0 (default) launches
+ * one CTA per 4096-element work item; max_ctas > 0 launches at most that many
+ * CTAs, which stride over the items.  For overlapping the bucketed
+ * exchange with a concurrent backward: an uncapped
+ * kernel takes every free SM slot and the next GEMM waits for it to drain.
+ * Local to this rank (no cross-rank pairing); results do not depend on it.
+ * max_ctas < 0 gives CMN_ERR_INVALID_ARG. */
+cmn_status cmn_set_stream_ctas(cmn_comm *comm, int max_ctas);
+
 /* cmn_set_kernel_timing -- on: bracket every launch of the step's dominant
  * kernels (the all-reduce kernels -- one-shot / two-shot / NVLS / NCCL --,
  * the reduce-scatter and fused all-gather+update kernels of the fused

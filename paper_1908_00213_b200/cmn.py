@@ -52,6 +52,7 @@ SIGNATURES = [
     ("cmn_set_pipeline", C.c_int, [_P, C.c_int]),
     ("cmn_set_fused_update", C.c_int, [_P, C.c_int]),
     ("cmn_set_ctas", C.c_int, [_P, C.c_int, C.c_int]),
+    ("cmn_set_stream_ctas", C.c_int, [_P, C.c_int]),
     ("cmn_set_kernel_timing", C.c_int, [_P, C.c_int]),
     ("cmn_get_kernel_timing", C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int)]),
     ("cmn_set_timeout", C.c_int, [_P, C.c_uint32]),
@@ -377,6 +378,9 @@ class Comm:
 
     def set_ctas(self, collective_ctas: int = 0, update_ctas: int = 0):
         _check(lib().cmn_set_ctas(self._h, collective_ctas, update_ctas), "cmn_set_ctas")
+
+    def set_stream_ctas(self, max_ctas: int = 0):
+        _check(lib().cmn_set_stream_ctas(self._h, max_ctas), "cmn_set_stream_ctas")
 
     def set_kernel_timing(self, on: bool):
         _check(lib().cmn_set_kernel_timing(self._h, int(bool(on))), "cmn_set_kernel_timing")

@@ -631,6 +631,13 @@ cmn_status cmn_set_ctas(cmn_comm *c, int collective_ctas, int update_ctas) {
     return CMN_OK;
 }
 
+cmn_status cmn_set_stream_ctas(cmn_comm *c, int max_ctas) {
+    if (!c) return fail(CMN_ERR_INVALID_ARG, "comm is NULL");
+    if (max_ctas < 0) return fail(CMN_ERR_INVALID_ARG, "max_ctas must be >= 0 (0 = one CTA per item)");
+    c->stream_ctas = max_ctas;
+    return CMN_OK;
+}
+
 cmn_status cmn_set_kernel_timing(cmn_comm *c, int on) {
     if (!c) return fail(CMN_ERR_INVALID_ARG, "comm is NULL");
     c->ktiming = on != 0;

@@ -121,6 +121,7 @@ struct cmn_comm {
     uint32_t timeout_ms = 30000;
     int ar_blocks = 0;            // cmn_set_ctas: collective grid (0 = default)
     int upd_blocks = 0;           // cmn_set_ctas: barrier-gated update grid (0 = default)
+    int stream_ctas = 0;          // cmn_set_stream_ctas: cap on pack/update grids (0 = none)
     int *h_err = nullptr, *d_err = nullptr;
     uint64_t launches = 0;
     // cmn_set_kernel_timing: CUDA events around every launch of the step's

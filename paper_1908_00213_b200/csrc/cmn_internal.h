@@ -81,13 +81,16 @@ struct PeerBufs {
 
 // a1: pack items [i0, i1) (tensors of those items lie in [t_lo, t_lo + ntab),
 // ntab <= kGradCap: the table's used entries; small tables launch smaller).
+// max_ctas > 0 caps the grid (CTAs then stride over the items; results do
+// not depend on it) -- cmn_set_stream_ctas, for sharing SMs with compute.
 cudaError_t launch_pack(const GradTab &g, int ntab, int t_lo, const TensorDesc *td,
-                        const Item *items, int i0, int i1, int dtype, void *packed, cudaStream_t s);
+                        const Item *items, int i0, int i1, int dtype, void *packed, cudaStream_t s,
+                        int max_ctas = 0);
 
 // a3: update from a reduced packed buffer (payload dtype), momentum SGD.
 cudaError_t launch_update_sgd(const TensorDesc *td, const Item *items, int i0, int i1,
                               const void *reduced, int dtype, float inv_n, float lr, float mu,
-                              cudaStream_t s);
+                              cudaStream_t s, int max_ctas = 0);
 
 // a1'+a3 at N = 1: read g directly (cast through fp16 if dtype == 1).
 // wt: the parameter pointers of the same tensors; mom: momentum base (tensor
@@ -105,7 +108,7 @@ cudaError_t launch_unpack_avg(const GradTab &out, int t_lo, const TensorDesc *td
 cudaError_t launch_update_adam(const TensorDesc *td, const Item *items, int i0, int i1,
                                const void *reduced, int dtype, float inv_n, float alpha_t,
                                float beta1, float beta2, float c1, float c2, float eps,
-                               cudaStream_t s);
+                               cudaStream_t s, int max_ctas = 0);
 
 // NEXT-1 at N = 1: Adam straight from the gradients (no pack); m, v at
 // adam_m / adam_v + packed index; programmatic dependent launch.

@@ -120,19 +120,11 @@ __device__ __forceinline__ void pack_store(void *packed, int64_t j, const float4
     }
 }
 
+// One CTA's share of the pack: items its[0..kPackItems) starting at ib,
+// all loads issued before the first store.
 template <int DT, int CAP>
-__global__ void __launch_bounds__(kPackThreads) k_pack(const __grid_constant__ GradTabN<CAP> g, int t_lo,
-                                                   const Item *__restrict__ items, int i0, int i1,
-                                                   void *__restrict__ packed) {
-    // PDL (see launch_pack): the item table is static, so it is read before
-    // waiting for the previous grid; gradients and the packed buffer after.
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    const int ib = i0 + blockIdx.x * kPackItems;
-    Item its[kPackItems];
-#pragma unroll
-    for (int j = 0; j < kPackItems; ++j)
-        if (ib + j < i1) its[j] = items[ib + j];
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+__device__ __forceinline__ void pack_items(const GradTabN<CAP> &g, int t_lo, const Item (&its)[kPackItems],
+                                           int ib, int i1, void *__restrict__ packed) {
     float4 x[kPackItems][kPackVec];
 #pragma unroll
     for (int j = 0; j < kPackItems; ++j) {
@@ -175,26 +167,48 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const __grid_constant__ G
     }
 }
 
+// STRIDE = false: one CTA per kPackItems items (the default grid).  STRIDE =
+// true: a grid capped by cmn_set_stream_ctas strides over the items (a
+// separate instantiation, so the default one keeps its registers).
+template <int DT, int CAP, bool STRIDE>
+__global__ void __launch_bounds__(kPackThreads) k_pack(const __grid_constant__ GradTabN<CAP> g, int t_lo,
+                                                   const Item *__restrict__ items, int i0, int i1,
+                                                   void *__restrict__ packed) {
+    // PDL (see launch_pdl): the item table is static, so it is read before
+    // waiting for the previous grid; gradients and the packed buffer after.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    int ib = i0 + blockIdx.x * kPackItems;
+    Item its[kPackItems];
+#pragma unroll
+    for (int j = 0; j < kPackItems; ++j)
+        if (ib + j < i1) its[j] = items[ib + j];
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if constexpr (!STRIDE) {
+        pack_items<DT, CAP>(g, t_lo, its, ib, i1, packed);
+    } else {
+        while (ib < i1) {
+            pack_items<DT, CAP>(g, t_lo, its, ib, i1, packed);
+            ib += gridDim.x * kPackItems;
+#pragma unroll
+            for (int j = 0; j < kPackItems; ++j)
+                if (ib + j < i1) its[j] = items[ib + j];
+        }
+    }
+}
+
 // ------------------------------------------------------------------- a3
 // Streaming hints only for the fp16 payload: the .cs A/B
 // (profiles/r1_hints_ab.jsonl) measured plain accesses 1-4 % faster for the
 // fp32 payload and .cs ~4 % faster for fp16.
 template <int DT>
-__global__ void __launch_bounds__(kThreads) k_update_sgd(const TensorDesc *__restrict__ td,
-                                                         const Item *__restrict__ items, int i0,
-                                                         const void *__restrict__ reduced,
-                                                         float inv_n, float lr, float mu) {
+__device__ __forceinline__ void update_sgd_item(const Item &it, const TensorDesc &d,
+                                                const void *__restrict__ reduced, float inv_n,
+                                                float lr, float mu) {
     constexpr bool CS = DT == 1;
-    // PDL (see launch_update_sgd): descriptors are static, read before the wait.
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    const Item it = items[i0 + blockIdx.x];
-    const TensorDesc d = td[it.t];
     float *__restrict__ w = d.w + it.k0;
     float *__restrict__ m = d.mom + it.k0;
     const int64_t base = d.off + it.k0;
     const int nv = it.len >> 2;
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-
     float4 r[kVecPerThread], wv[kVecPerThread], mv[kVecPerThread];
 #pragma unroll
     for (int u = 0; u < kVecPerThread; ++u) {
@@ -219,6 +233,30 @@ __global__ void __launch_bounds__(kThreads) k_update_sgd(const TensorDesc *__res
         sgd_elem(load_r1<DT>(reduced, base + k), inv_n, lr, mu, wk, mk);
         w[k] = wk;
         m[k] = mk;
+    }
+}
+
+template <int DT, bool STRIDE>
+__global__ void __launch_bounds__(kThreads) k_update_sgd(const TensorDesc *__restrict__ td,
+                                                         const Item *__restrict__ items, int i0,
+                                                         int i1, const void *__restrict__ reduced,
+                                                         float inv_n, float lr, float mu) {
+    // PDL (see launch_pdl): descriptors are static, read before the wait.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    int ib = i0 + blockIdx.x;
+    Item it = items[ib];
+    TensorDesc d = td[it.t];
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if constexpr (!STRIDE) {
+        update_sgd_item<DT>(it, d, reduced, inv_n, lr, mu);
+    } else {
+        for (;;) {
+            update_sgd_item<DT>(it, d, reduced, inv_n, lr, mu);
+            ib += gridDim.x;
+            if (ib >= i1) break;
+            it = items[ib];
+            d = td[it.t];
+        }
     }
 }
 
@@ -327,20 +365,14 @@ __device__ __forceinline__ void adam_elem(float r, float inv_n, float alpha_t, f
 }
 
 template <int DT>
-__global__ void __launch_bounds__(kThreads) k_update_adam(const TensorDesc *__restrict__ td,
-                                                          const Item *__restrict__ items, int i0,
-                                                          const void *__restrict__ reduced,
-                                                          float inv_n, float alpha_t, float beta1,
-                                                          float beta2, float c1, float c2,
-                                                          float eps) {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // PDL, see launch_pdl
-    const Item it = items[i0 + blockIdx.x];
-    const TensorDesc d = td[it.t];
+__device__ __forceinline__ void update_adam_item(const Item &it, const TensorDesc &d,
+                                                 const void *__restrict__ reduced, float inv_n,
+                                                 float alpha_t, float beta1, float beta2, float c1,
+                                                 float c2, float eps) {
     float *__restrict__ w = d.w + it.k0;
     float *__restrict__ m = d.adam_m + it.k0;
     float *__restrict__ v = d.adam_v + it.k0;
     const int nv = it.len >> 2;
-    asm volatile("griddepcontrol.wait;" ::: "memory");
     // fp16 payload (its reduced buffer half-resident in L2): 2 passes
     // measured faster (103.0 vs 112.3 us); fp32: 1 pass (108.4 vs 110.5 us)
     constexpr int kPasses = DT == 1 ? 2 : kAdamPasses;
@@ -382,7 +414,30 @@ __global__ void __launch_bounds__(kThreads) k_update_adam(const TensorDesc *__re
     }
 }
 
-
+template <int DT, bool STRIDE>
+__global__ void __launch_bounds__(kThreads) k_update_adam(const TensorDesc *__restrict__ td,
+                                                          const Item *__restrict__ items, int i0,
+                                                          int i1, const void *__restrict__ reduced,
+                                                          float inv_n, float alpha_t, float beta1,
+                                                          float beta2, float c1, float c2,
+                                                          float eps) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // PDL, see launch_pdl
+    int ib = i0 + blockIdx.x;
+    Item it = items[ib];
+    TensorDesc d = td[it.t];
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if constexpr (!STRIDE) {
+        update_adam_item<DT>(it, d, reduced, inv_n, alpha_t, beta1, beta2, c1, c2, eps);
+    } else {
+        for (;;) {
+            update_adam_item<DT>(it, d, reduced, inv_n, alpha_t, beta1, beta2, c1, c2, eps);
+            ib += gridDim.x;
+            if (ib >= i1) break;
+            it = items[ib];
+            d = td[it.t];
+        }
+    }
+}
 
 // NEXT-1 at N = 1: Adam straight from the gradients (the all-reduce is the
 // identity, so a = cast(g) and the pack is skipped: 28 instead of 36
@@ -886,35 +941,53 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int threads, cudaStre
 
 // ----------------------------------------------------------------- launchers
 
+// Grid of the stream-local item kernels: one CTA per item (per kPackItems
+// items for the pack), or at most `max_ctas` grid-striding CTAs.
+inline int capped(int n, int max_ctas) { return max_ctas > 0 && n > max_ctas ? max_ctas : n; }
+
+namespace {
+template <int DT, int CAP>
+cudaError_t pack_launch(int grid, bool stride, cudaStream_t s, const GradTab &g, int t_lo,
+                        const Item *items, int i0, int i1, void *packed) {
+    const auto t = shrink<CAP>(g);
+    return stride ? launch_pdl(k_pack<DT, CAP, true>, grid, kPackThreads, s, t, t_lo, items, i0, i1, packed)
+                  : launch_pdl(k_pack<DT, CAP, false>, grid, kPackThreads, s, t, t_lo, items, i0, i1, packed);
+}
+}  // namespace
+
 cudaError_t launch_pack(const GradTab &g, int ntab, int t_lo, const TensorDesc *td,
-                        const Item *items, int i0, int i1, int dtype, void *packed, cudaStream_t s) {
+                        const Item *items, int i0, int i1, int dtype, void *packed, cudaStream_t s,
+                        int max_ctas) {
     const int n = grid_of(i0, i1);
     if (n == 0) return cudaSuccess;
     (void)td;
     (void)cudaGetLastError();  // report this launch's error, not a stale one
-    const int grid = (n + kPackItems - 1) / kPackItems;
-    cudaError_t e;
-    if (ntab <= kSmallTab) {
-        const auto t = shrink<kSmallTab>(g);
-        e = dtype == 0 ? launch_pdl(k_pack<0, kSmallTab>, grid, kPackThreads, s, t, t_lo, items, i0, i1, packed)
-                       : launch_pdl(k_pack<1, kSmallTab>, grid, kPackThreads, s, t, t_lo, items, i0, i1, packed);
-    } else {
-        const auto t = shrink<kGradCap>(g);
-        e = dtype == 0 ? launch_pdl(k_pack<0, kGradCap>, grid, kPackThreads, s, t, t_lo, items, i0, i1, packed)
-                       : launch_pdl(k_pack<1, kGradCap>, grid, kPackThreads, s, t, t_lo, items, i0, i1, packed);
-    }
+    const int full = (n + kPackItems - 1) / kPackItems;
+    const int grid = capped(full, max_ctas);
+    const bool stride = grid < full;
+    const cudaError_t e =
+        ntab <= kSmallTab
+            ? (dtype == 0 ? pack_launch<0, kSmallTab>(grid, stride, s, g, t_lo, items, i0, i1, packed)
+                          : pack_launch<1, kSmallTab>(grid, stride, s, g, t_lo, items, i0, i1, packed))
+            : (dtype == 0 ? pack_launch<0, kGradCap>(grid, stride, s, g, t_lo, items, i0, i1, packed)
+                          : pack_launch<1, kGradCap>(grid, stride, s, g, t_lo, items, i0, i1, packed));
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_update_sgd(const TensorDesc *td, const Item *items, int i0, int i1,
                               const void *reduced, int dtype, float inv_n, float lr, float mu,
-                              cudaStream_t s) {
-    const int grid = grid_of(i0, i1);
-    if (grid == 0) return cudaSuccess;
+                              cudaStream_t s, int max_ctas) {
+    const int n = grid_of(i0, i1);
+    if (n == 0) return cudaSuccess;
+    const int grid = capped(n, max_ctas);
     (void)cudaGetLastError();  // report this launch's error, not a stale one
-    const cudaError_t e =
-        dtype == 0 ? launch_pdl(k_update_sgd<0>, grid, kThreads, s, td, items, i0, reduced, inv_n, lr, mu)
-                   : launch_pdl(k_update_sgd<1>, grid, kThreads, s, td, items, i0, reduced, inv_n, lr, mu);
+    cudaError_t e;
+    if (grid < n)
+        e = dtype == 0 ? launch_pdl(k_update_sgd<0, true>, grid, kThreads, s, td, items, i0, i1, reduced, inv_n, lr, mu)
+                       : launch_pdl(k_update_sgd<1, true>, grid, kThreads, s, td, items, i0, i1, reduced, inv_n, lr, mu);
+    else
+        e = dtype == 0 ? launch_pdl(k_update_sgd<0, false>, grid, kThreads, s, td, items, i0, i1, reduced, inv_n, lr, mu)
+                       : launch_pdl(k_update_sgd<1, false>, grid, kThreads, s, td, items, i0, i1, reduced, inv_n, lr, mu);
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
@@ -962,15 +1035,22 @@ cudaError_t launch_unpack_avg(const GradTab &out, int t_lo, const TensorDesc *td
 cudaError_t launch_update_adam(const TensorDesc *td, const Item *items, int i0, int i1,
                                const void *reduced, int dtype, float inv_n, float alpha_t,
                                float beta1, float beta2, float c1, float c2, float eps,
-                               cudaStream_t s) {
-    const int grid = grid_of(i0, i1);
-    if (grid == 0) return cudaSuccess;
+                               cudaStream_t s, int max_ctas) {
+    const int n = grid_of(i0, i1);
+    if (n == 0) return cudaSuccess;
+    const int grid = capped(n, max_ctas);
     (void)cudaGetLastError();  // report this launch's error, not a stale one
-    const cudaError_t e =
-        dtype == 0 ? launch_pdl(k_update_adam<0>, grid, kThreads, s, td, items, i0, reduced, inv_n,
-                                alpha_t, beta1, beta2, c1, c2, eps)
-                   : launch_pdl(k_update_adam<1>, grid, kThreads, s, td, items, i0, reduced, inv_n,
-                                alpha_t, beta1, beta2, c1, c2, eps);
+    cudaError_t e;
+    if (grid < n)
+        e = dtype == 0 ? launch_pdl(k_update_adam<0, true>, grid, kThreads, s, td, items, i0, i1, reduced,
+                                    inv_n, alpha_t, beta1, beta2, c1, c2, eps)
+                       : launch_pdl(k_update_adam<1, true>, grid, kThreads, s, td, items, i0, i1, reduced,
+                                    inv_n, alpha_t, beta1, beta2, c1, c2, eps);
+    else
+        e = dtype == 0 ? launch_pdl(k_update_adam<0, false>, grid, kThreads, s, td, items, i0, i1, reduced,
+                                    inv_n, alpha_t, beta1, beta2, c1, c2, eps)
+                       : launch_pdl(k_update_adam<1, false>, grid, kThreads, s, td, items, i0, i1, reduced,
+                                    inv_n, alpha_t, beta1, beta2, c1, c2, eps);
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 

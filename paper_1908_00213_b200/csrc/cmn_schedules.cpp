@@ -22,7 +22,7 @@ cmn_status pack_phase(cmn_comm *c, int ta, int tb, const float *const *grads, in
         cmn_status st = for_groups(c, ta, tb, [&](int lo, int hi, int i0, int i1) {
             return launched(c,
                             launch_pack(make_tab(g, lo, hi), hi - lo, lo, c->d_td, c->d_items, i0, i1, dtype,
-                                        dst, s),
+                                        dst, s, c->stream_ctas),
                             "pack");
         });
         if (st != CMN_OK) return st;
@@ -169,7 +169,7 @@ cmn_status update_range(cmn_comm *c, int ta, int tb, const ArResult &res, float 
     return for_groups(c, ta, tb, [&](int, int, int i0, int i1) {
         return launched(c,
                         launch_update_sgd(c->d_td, c->d_items, i0, i1, reduced_ptr(c, res, 0),
-                                          res.dtype, inv_n, lr, mu, s),
+                                          res.dtype, inv_n, lr, mu, s, c->stream_ctas),
                         "update_sgd");
     });
 }
@@ -205,7 +205,7 @@ cmn_status update_range_adam(cmn_comm *c, int ta, int tb, const ArResult &res, c
         return launched(c,
                         launch_update_adam(c->d_td, c->d_items, i0, i1, reduced_ptr(c, res, 0),
                                            res.dtype, inv_n, a.alpha_t, a.beta1, a.beta2, a.c1,
-                                           a.c2, a.eps, s),
+                                           a.c2, a.eps, s, c->stream_ctas),
                         "update_adam");
     });
 }

@@ -32,8 +32,12 @@ from .cmn import Comm, PtrTable
 class MultiNodeOptimizer:
     def __init__(self, params, comm: Comm, lr: float = 0.1, momentum: float = 0.9,
                  dtype: str = "fp32", bucket_bytes: int | None = None, optimizer: str = "momentum_sgd",
-                 adam=(1e-3, 0.9, 0.999, 1e-8)):
+                 adam=(1e-3, 0.9, 0.999, 1e-8), stream_ctas: int = 0):
         self.comm = comm
+        # overlap: cap the pack/update grids so they share SMs with the
+        # backward instead of taking every free slot (cmn_set_stream_ctas;
+        # 64 measured best on one B200, profiles/r1_overlap_sweep.jsonl)
+        comm.set_stream_ctas(stream_ctas)
         self.lr, self.mu, self.dtype = lr, momentum, dtype
         self.bucket_bytes = bucket_bytes
         self.optimizer = optimizer

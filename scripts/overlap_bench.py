@@ -63,6 +63,16 @@ def main():
     ap.add_argument("--bucket-mb", type=float, default=25.0)
     ap.add_argument("--dtype", default="fp32")
     ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--launch", default="graph", choices=["graph", "eager"],
+                    help="graph: each timed step (backward, comm, overlapped step) is one captured "
+                         "CUDA graph (no host launch cost; N = 1 / simulated only); eager: per-bucket "
+                         "library calls from Python after per-bucket graph replays")
+    ap.add_argument("--carveout", type=int, default=0,
+                    help="SMs the backward's GEMMs leave free (torch cuBLAS SM carveout)")
+    ap.add_argument("--stream-ctas", type=int, default=0,
+                    help="cmn_set_stream_ctas: cap on the pack / update grids (0 = one CTA per item)")
+    ap.add_argument("--ar-ctas", type=int, default=0,
+                    help="cmn_set_ctas collective grid (N > 1; 0 = library default)")
     ap.add_argument("--reps", type=int, default=15,
                     help="interleaved measurement rounds (T_bwd, T_comm, T_step each); medians reported")
     a = ap.parse_args()
@@ -82,6 +92,9 @@ def main():
     p0 = synth.params(shapes)
     w = [torch.from_numpy(p.copy()).cuda() for p in p0]
     comm.register_params(w)
+    comm.set_stream_ctas(a.stream_ctas)
+    if a.ar_ctas:
+        comm.set_ctas(a.ar_ctas, 0)
     nb = comm.plan_buckets(int(a.bucket_mb * (1 << 20)))
     buckets = [comm.get_bucket(b) for b in range(nb)]
     host_g = synth.grads(shapes, workers=nranks)
@@ -90,6 +103,11 @@ def main():
     g = [[torch.empty_like(x) for x in gw] for gw in src]
     table = comm.prepare(g if a.sim else g[0])
 
+    if a.launch == "graph" and world > 1:
+        raise SystemExit("--launch graph needs N = 1 or --sim (multi-process single-call "
+                         "bucket collectives refuse capture); use --launch eager under torchrun")
+    if a.carveout:
+        torch._C._set_sm_carveout_experimental(a.carveout)
     # synthetic backward kernels: per-layer bf16 GEMM sized by FLOP share
     stages = stage_of_r50()
     per_stage = {s: stages.count(s) for s in STAGE_SHARE}
@@ -147,9 +165,47 @@ def main():
         torch.cuda.synchronize()
         return graphs
 
-    seg_graphs = capture()
+    def body(with_comm, bwd=True):
+        """One step issued on the current stream: the backward segments and,
+        after each, that bucket's all-reduce + update forked onto comm_stream."""
+        cur = torch.cuda.current_stream()
+        for b, (lo, hi) in enumerate(buckets):
+            if bwd:
+                produce(lo, hi)
+            if with_comm:
+                ev = torch.cuda.Event()
+                ev.record(cur)
+                comm_stream.wait_event(ev)
+                comm.allreduce_bucket(b, table, a.dtype, comm_stream)
+                comm.update_bucket(b, 0.1, 0.9, comm_stream)
+        if with_comm:
+            cur.wait_stream(comm_stream)
+
+    def capture_steps():
+        """CUDA graphs of the three timed steps (--launch graph)."""
+        side = torch.cuda.Stream()
+        side.wait_stream(comp)
+        with torch.cuda.stream(side):
+            body(True)                     # warm-up outside capture (cuBLAS workspaces)
+        torch.cuda.synchronize()
+        out = {}
+        for name, wc, bw in (("bwd", False, True), ("comm", True, False), ("step", True, True)):
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                body(wc, bw)
+            out[name] = gr
+        torch.cuda.synchronize()
+        return out
+
+    if a.launch == "graph":
+        step_graphs = capture_steps()
+    else:
+        seg_graphs = capture()
 
     def backward(with_comm: bool):
+        if a.launch == "graph":
+            step_graphs["step" if with_comm else "bwd"].replay()
+            return
         for b in range(nb):
             seg_graphs[b].replay()
             if with_comm:
@@ -162,6 +218,9 @@ def main():
             comp.wait_stream(comm_stream)
 
     def comm_only():
+        if a.launch == "graph":
+            step_graphs["comm"].replay()
+            return
         for b in range(nb):
             comm.allreduce_bucket(b, table, a.dtype, comp)
             comm.update_bucket(b, 0.1, 0.9, comp)
@@ -199,7 +258,10 @@ def main():
             break
         scale *= a.bwd_ms / got
         reps = plan_reps(scale)
-        seg_graphs = capture()
+        if a.launch == "graph":
+            step_graphs = capture_steps()
+        else:
+            seg_graphs = capture()
 
     # interleaved rounds: slow drift (clocks, power) hits all three alike
     tb, tc, ts = [], [], []
@@ -215,7 +277,7 @@ def main():
         x.copy_(torch.from_numpy(p))
     comm.register_params(w)          # resets momentum
     comm.plan_buckets(int(a.bucket_mb * (1 << 20)))
-    backward(True)
+    body(True)                       # eager: the captured graphs hold the old registration
     torch.cuda.synchronize()
     wb = torch.cat([x.reshape(-1) for x in w]).clone()
     for x, p in zip(w, p0):
@@ -240,6 +302,8 @@ def main():
                           "timing": f"medians of {a.reps} interleaved rounds x {a.iters} steps "
                                     "(CUDA events on the compute stream, max over ranks)",
                           "bwd_target_ms": a.bwd_ms, "bwd_scale": scale,
+                          "launch": a.launch, "gemm_sm_carveout": a.carveout,
+                          "stream_ctas": a.stream_ctas, "ar_ctas": a.ar_ctas,
                           "bucketed_equals_unbucketed_bitwise": same,
                           "gemm_1024_ms": gemm_ms}))
     comm.finalize()

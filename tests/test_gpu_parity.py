@@ -920,3 +920,75 @@ def test_degenerate_models(cmn, orc, N):
                         assert_bitwise(w[t].cpu().numpy().reshape(-1), ora[s]["w"][t], f"{shapes} {sched} w[{t}]")
             finally:
                 comm.finalize()
+
+
+@pytest.mark.parametrize("N,dtype,max_ctas", [(1, "fp32", 1), (1, "fp16", 5), (3, "fp32", 148),
+                                              (3, "fp16", 7), (2, "fp32", 100000)])
+def test_stream_ctas_parity(cmn, orc, N, dtype, max_ctas):
+    """cmn_set_stream_ctas caps the pack / update / Adam grids; the capped
+    CTAs stride over the work items.  Results are the oracle's, bitwise, for
+    the whole-model call pair, the bucketed calls, and the Adam update (3
+    steps each, ragged shapes spanning several items and tails)."""
+    shapes = synth.resnet50_shapes()[:20] + RAGGED
+    sizes = [synth.numel(s) for s in shapes]
+    params0 = synth.params(shapes)
+    grads = [synth.grads(shapes, workers=N, step=s) for s in range(3)]
+    ora, off, L = run_oracle(orc, shapes, N, dtype, grads, params0, 0.1, 0.9)
+    for bucketed in (False, True):
+        comm = cmn.Comm.simulated_world(N) if N > 1 else cmn.Comm.init(0, 1, 0)
+        try:
+            w = to_dev(params0)
+            comm.register_params(w)
+            comm.set_stream_ctas(max_ctas)
+            nb = comm.plan_buckets(1 << 18) if bucketed else 0
+            for s, g in enumerate(grads):
+                gd = [to_dev(gw) for gw in g] if N > 1 else to_dev(g[0])
+                if bucketed:
+                    table = comm.prepare(gd)
+                    for b in range(nb):
+                        comm.allreduce_bucket(b, table, dtype)
+                    for b in range(nb):
+                        comm.update_bucket(b, 0.1, 0.9)
+                else:
+                    comm.allreduce_grads(gd, dtype)
+                    comm.update_momentum_sgd(0.1, 0.9)
+                torch.cuda.synchronize()
+                for t in range(len(w)):
+                    what = f"{'bucketed' if bucketed else 'whole'} step {s}"
+                    assert_bitwise(w[t].cpu().numpy().reshape(-1), ora[s]["w"][t], f"{what} w[{t}]")
+                    assert_bitwise(comm.momentum(t).cpu().numpy().reshape(-1), ora[s]["v"][t],
+                                   f"{what} v[{t}]")
+        finally:
+            comm.finalize()
+    # Adam from the reduced buffer under the cap
+    w_o = [p.copy() for p in params0]
+    m_o = [np.zeros_like(p) for p in params0]
+    v_o = [np.zeros_like(p) for p in params0]
+    comm = cmn.Comm.simulated_world(N) if N > 1 else cmn.Comm.init(0, 1, 0)
+    try:
+        w = to_dev(params0)
+        comm.register_params(w)
+        comm.set_stream_ctas(max_ctas)
+        for step, g in enumerate(grads, start=1):
+            red = orc.reduce_tree([orc.pack(gw, off, L, dtype) for gw in g], dtype)
+            orc.update_adam(red, dtype, N, 1e-3, 0.9, 0.999, 1e-8, step, off, w_o, m_o, v_o)
+            comm.allreduce_grads([to_dev(gw) for gw in g] if N > 1 else to_dev(g[0]), dtype)
+            comm.update_adam(1e-3, 0.9, 0.999, 1e-8, step)
+            torch.cuda.synchronize()
+            for t in range(len(w)):
+                m, v = comm.adam_state(t)
+                assert_bitwise(w[t].cpu().numpy().reshape(-1), w_o[t], f"adam w[{t}] step {step}")
+                assert_bitwise(m.cpu().numpy().reshape(-1), m_o[t], f"adam m[{t}] step {step}")
+                assert_bitwise(v.cpu().numpy().reshape(-1), v_o[t], f"adam v[{t}] step {step}")
+    finally:
+        comm.finalize()
+
+
+def test_stream_ctas_invalid(cmn):
+    comm = cmn.Comm.simulated_world(2)
+    try:
+        with pytest.raises(cmn.CmnError):
+            comm.set_stream_ctas(-1)
+        comm.set_stream_ctas(0)
+    finally:
+        comm.finalize()
