@@ -133,3 +133,61 @@ def test_bucket_plan(bucket_mb):
             assert nbytes + 4 * sizes[b - 1] > cap    # maximal
     if cap == 0:
         assert len(plan) == 1
+
+
+# ---- property-based host-logic checks (random shapes, sizes, world sizes)
+from hypothesis import given, settings, strategies as st  # noqa: E402
+
+_dims = st.lists(st.integers(min_value=0, max_value=70), min_size=1, max_size=3)
+
+
+@settings(max_examples=200, deadline=None)
+@given(shapes=st.lists(_dims, min_size=1, max_size=40))
+def test_plan_layout_matches_oracle_random(lib, orc, shapes):
+    """The library's layout (a0) equals the oracle's on random shapes, zero-size
+    dimensions included; offsets are 64-aligned and non-decreasing."""
+    shapes = [tuple(s) for s in shapes]
+    sizes = [int(__import__("numpy").prod(s)) for s in shapes]
+    off, L, _ = cmn.plan_layout(shapes)
+    o_off, o_L = orc.layout(sizes)
+    assert list(off) == [int(x) for x in o_off] and L == o_L
+    assert all(o % 64 == 0 for o in off)
+    assert all(off[t + 1] - off[t] >= sizes[t] for t in range(len(sizes)))
+
+
+@settings(max_examples=300, deadline=None)
+@given(blocks=st.integers(min_value=0, max_value=1 << 22), N=st.integers(min_value=1, max_value=8))
+def test_plan_chunks_partition_random(lib, blocks, N):
+    """§8(e): chunks partition [0, L) into N contiguous 64-aligned pieces of
+    align64(ceil(L/N)) elements (the last one shorter, possibly empty)."""
+    L = 64 * blocks
+    s, e = cmn.plan_chunks(L, N)
+    c = min(L, -(-(-(-L // N)) // 64) * 64)
+    pos = 0
+    for r in range(N):
+        assert s[r] == pos and s[r] % 64 == 0
+        assert e[r] - s[r] == max(0, min(c, L - pos))
+        pos = e[r]
+    assert pos == L
+
+
+@settings(max_examples=200, deadline=None)
+@given(sizes=st.lists(st.integers(min_value=0, max_value=3_000_000), min_size=1, max_size=60),
+       cap=st.sampled_from([0, 1, 4096, 1 << 16, 1 << 20, 4 << 20, 25 << 20]))
+def test_bucket_plan_random(sizes, cap):
+    """a4 buckets on random tensor sizes: contiguous reverse-order ranges
+    covering every tensor once, within the byte cap unless a single tensor,
+    and maximal (the next tensor would not fit)."""
+    plan = cmn.plan_bucket_ranges(sizes, cap)
+    assert plan[0][1] == len(sizes) and plan[-1][0] == 0
+    for (b0, _), (_, e1) in zip(plan, plan[1:]):
+        assert e1 == b0
+    for b, e in plan:
+        assert e > b
+        nbytes = 4 * sum(sizes[b:e])
+        if cap == 0:
+            assert (b, e) == (0, len(sizes))
+            continue
+        assert nbytes <= cap or e - b == 1
+        if b > 0:
+            assert nbytes + 4 * sizes[b - 1] > cap
