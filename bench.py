@@ -198,27 +198,46 @@ def _oracle_sample(n_workers: int):
 
 
 def oracle_step_time(n_workers: int, dtype: str, budget_s: float = 0.0, steps: int = 0,
-                     warmup: int = 0):
+                     warmup: int = 0, threads: int = 1):
     """Time the CPU oracle (single-threaded, as it stands) on a bounded
     sample of the ResNet-50 workload: either for ~budget_s seconds, or for
     `warmup` untimed + `steps` timed sample steps.  Returns (us per
-    full-workload step, sample description)."""
+    full-workload step, sample description).  threads > 1 times the same
+    oracle under SURVEY §8(d) d.5 (ii)'s elementwise partition across host
+    threads (oracle.step_threaded, bit-identical output)."""
     import oracle
     take, acc, P, g, w, v = _oracle_sample(n_workers)
+    if threads > 1:
+        def one():
+            oracle.step_threaded(g, w, v, 0.1, 0.9, dtype, threads=threads)
+    else:
+        def one():
+            oracle.step(g, w, v, 0.1, 0.9, dtype)
     for _ in range(warmup):
-        oracle.step(g, w, v, 0.1, 0.9, dtype)
+        one()
     times = []
     t_end = time.time() + budget_s
     while (steps and len(times) < steps) or (not steps and (time.time() < t_end or len(times) < 2)):
         t0 = time.perf_counter()
-        oracle.step(g, w, v, 0.1, 0.9, dtype)
+        one()
         times.append(time.perf_counter() - t0)
     per_param = statistics.median(times) / acc
-    desc = (f"oracle/cmn_oracle.c orc_step (pack+tree-reduce+momentum-SGD, 1 thread) on the first "
+    how = "1 thread" if threads <= 1 else f"{threads} threads, elementwise partition"
+    desc = (f"oracle/cmn_oracle.c orc_step (pack+tree-reduce+momentum-SGD, {how}) on the first "
             f"{take} of 161 ResNet-50 tensors ({acc:,} params), {n_workers} simulated worker(s), "
             f"{dtype}, median of {len(times)} timed sample steps, scaled x{P / acc:.2f} to the "
             f"full {P:,}-param set")
     return per_param * P * 1e6, desc
+
+
+def _cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def run_reference(args):
@@ -235,7 +254,8 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": us / 1e3,
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded counter-hash, synth/)", "config": cfg,
-            "cpu_baseline": {"value": us, "unit": "us", "cores": 1, "kind": "oracle", "sample": desc},
+            "cpu_baseline": {"value": us, "unit": "us", "cores": 1, "kind": "oracle", "sample": desc,
+                             "cpu": _cpu_model()},
             "e2e": {"value": us, "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
@@ -678,7 +698,13 @@ def main():
     cpu = None
     if not args.no_cpu_baseline and world == 1:      # the contract: rank 0 at N = 1 only
         cus, desc = oracle_step_time(world, args.dtype, budget_s=args.cpu_budget_s)
-        cpu = {"value": cus, "unit": "us", "cores": 1, "kind": "oracle", "sample": desc}
+        cpu = {"value": cus, "unit": "us", "cores": 1, "kind": "oracle", "sample": desc,
+               "cpu": _cpu_model()}
+        nth = os.cpu_count() or 1
+        if nth > 1:  # same oracle, elements partitioned over all cores
+            tus, tdesc = oracle_step_time(world, args.dtype, budget_s=args.cpu_budget_s / 2,
+                                          threads=nth)
+            cpu["threaded"] = {"value": tus, "unit": "us", "cores": nth, "sample": tdesc}
 
     cfg = {"workload": workload_name(P, args.dtype),
            "n_tensors": T, "n_params": P, "padded_len": L, "comm_dtype": args.dtype,

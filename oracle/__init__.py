@@ -220,3 +220,51 @@ def step(grads_per_worker, w, v, lr, mu, dtype="fp32", align: int = ALIGN, want_
     if rc != 0:
         raise RuntimeError("orc_step failed")
     return {"off": off, "L": L, "reduced": r, "avg": a}
+
+
+def step_threaded(grads_per_worker, w, v, lr, mu, dtype="fp32", threads: int = 0):
+    """The same step with the elements partitioned across host threads
+    ("elementwise partition across nproc threads,
+    which gives bit-identical output").  Timing aid for bench.py only.
+
+    Every quantity of c.1 steps 2-6 for element j depends only on element j
+    of each worker's gradient and of w, v (pack/cast, tree sum over workers,
+    1/N, momentum update), so the flattened parameter space is cut into
+    `threads` contiguous element ranges (split inside tensors where needed)
+    and each range is run through the unchanged single-threaded `step` on its
+    own thread (ctypes releases the GIL during the C call).  w and v are
+    updated in place; the reduced buffer and its layout are not returned
+    (each range has its own).  Arithmetic is exactly `step`'s."""
+    import concurrent.futures as cf
+    threads = threads or os.cpu_count() or 1
+    N = len(grads_per_worker)
+    wf = [np.asarray(x).reshape(-1) for x in w]
+    vf = [np.asarray(x).reshape(-1) for x in v]
+    for x in wf + vf:  # reshape must be a view: w, v are updated in place
+        _f32c(x)
+    gf = [[_f32c(g).reshape(-1) for g in gw] for gw in grads_per_worker]
+    total = sum(x.size for x in wf)
+    per = -(-total // threads) if total else 0
+    parts = []  # per thread: list of (tensor index, lo, hi)
+    t, k = 0, 0
+    for _ in range(threads):
+        need, part = per, []
+        while need > 0 and t < len(wf):
+            take = min(need, wf[t].size - k)
+            if take > 0:
+                part.append((t, k, k + take))
+            need -= take
+            k += take
+            if k >= wf[t].size:
+                t, k = t + 1, 0
+        if part:
+            parts.append(part)
+
+    def run(part):
+        g = [[gf[i][t][lo:hi] for (t, lo, hi) in part] for i in range(N)]
+        step(g, [wf[t][lo:hi] for (t, lo, hi) in part], [vf[t][lo:hi] for (t, lo, hi) in part],
+             lr, mu, dtype)
+
+    with cf.ThreadPoolExecutor(max_workers=max(1, len(parts))) as ex:
+        list(ex.map(run, parts))
+    return len(parts)

@@ -992,3 +992,18 @@ def test_stream_ctas_invalid(cmn):
         comm.set_stream_ctas(0)
     finally:
         comm.finalize()
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4])
+@pytest.mark.parametrize("dtype", ["fp32", "fp16"])
+def test_robustness_seeds_parity(cmn, orc, seed, dtype):
+    """seeds 1-4 beside the base seed, MLP (config 1) and a
+    ResNet-50 prefix with ragged tails, N = 2 and 5, both algorithms."""
+    for shapes in (synth.mlp_shapes(), synth.resnet50_shapes()[:12] + [(4097,), (3,)]):
+        for N in (2, 5):
+            grads = [synth.grads(shapes, workers=N, step=s, seed=seed) for s in range(2)]
+            params0 = synth.params(shapes, seed=seed)
+            ora, _, _ = run_oracle(orc, shapes, N, dtype, grads, params0, 0.1, 0.9)
+            for algo in ("oneshot", "twoshot"):
+                gpu, _, _ = run_gpu(cmn, shapes, N, dtype, algo, grads, params0, 0.1, 0.9)
+                compare(gpu, ora, N)

@@ -188,3 +188,24 @@ def test_adam_constant_gradient_trajectory_closed_form(orc, steps):
     b1f = float(np.float32(b1))
     assert np.allclose(m[0], (1 - b1f ** steps) * g64, rtol=1e-5, atol=0)
     assert np.allclose(v[0], (1 - b2f ** steps) * g64 * g64, rtol=1e-4, atol=0)
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "fp16"])
+@pytest.mark.parametrize("threads", [1, 3, 8, 17])
+def test_threaded_partition_bitwise_equal(orc, dtype, threads):
+    """the elementwise partition across host threads
+    (bench.py's cpu_baseline timing aid) gives bit-identical w, v.  Ragged
+    shapes force ranges that split tensors and threads > elements of some
+    ranges; 3 steps carry momentum across the partition."""
+    shapes = [(5,), (4097,), (3, 7), (1,), (64, 65), (0,), (12289,)]
+    N = 3
+    w1 = synth.params(shapes, seed=5)
+    w2 = [x.copy() for x in w1]
+    v1 = [np.zeros_like(x) for x in w1]
+    v2 = [np.zeros_like(x) for x in w1]
+    for s in range(3):
+        g = synth.grads(shapes, workers=N, step=s, seed=5)
+        orc.step(g, w1, v1, 0.1, 0.9, dtype)
+        orc.step_threaded(g, w2, v2, 0.1, 0.9, dtype, threads=threads)
+    for a, b in zip(w1 + v1, w2 + v2):
+        assert a.tobytes() == b.tobytes()
