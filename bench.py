@@ -53,8 +53,8 @@ SCHEDULES = {
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=100)  # SURVEY d.1: 100 timed
+    ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="cmn", choices=["cmn", "reference"])
     ap.add_argument("--dtype", default="fp32", choices=["fp32", "fp16"])
     ap.add_argument("--algo", default="auto", choices=["auto", "oneshot", "twoshot", "nccl", "nvls"])
