@@ -73,6 +73,9 @@ def main():
                     help="cmn_set_stream_ctas: cap on the pack / update grids (0 = one CTA per item)")
     ap.add_argument("--ar-ctas", type=int, default=0,
                     help="cmn_set_ctas collective grid (N > 1; 0 = library default)")
+    ap.add_argument("--comm-priority", default="high", choices=["high", "low"],
+                    help="priority of the communication stream relative to the backward's stream "
+                         "(high: the block scheduler places pending comm CTAs first)")
     ap.add_argument("--reps", type=int, default=15,
                     help="interleaved measurement rounds (T_bwd, T_comm, T_step each); medians reported")
     a = ap.parse_args()
@@ -137,8 +140,13 @@ def main():
 
     reps = plan_reps(1.0)
 
+    if a.comm_priority == "low":
+        # backward on a high-priority stream, comm on a normal one: pending
+        # GEMM CTAs are placed before pending pack/update CTAs
+        torch.cuda.set_stream(torch.cuda.Stream(priority=-1))
     comp = torch.cuda.current_stream()
-    comm_stream = torch.cuda.Stream(priority=-1)
+    comm_stream = torch.cuda.Stream(priority=-1 if a.comm_priority == "high" else 0)
+    cap_stream = torch.cuda.Stream(priority=-1 if a.comm_priority == "low" else 0)
     # Backward segments: bucket b (reverse order) covers tensors [lo, hi); the
     # producer for those layers is captured once into a CUDA graph so the
     # synthetic backward is not bound by Python launch overhead.
@@ -159,7 +167,7 @@ def main():
         torch.cuda.synchronize()
         for lo, hi in buckets:
             gr = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gr):
+            with torch.cuda.graph(gr, stream=cap_stream):
                 produce(lo, hi)
             graphs.append(gr)
         torch.cuda.synchronize()
@@ -191,7 +199,7 @@ def main():
         out = {}
         for name, wc, bw in (("bwd", False, True), ("comm", True, False), ("step", True, True)):
             gr = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gr):
+            with torch.cuda.graph(gr, stream=cap_stream):
                 body(wc, bw)
             out[name] = gr
         torch.cuda.synchronize()
@@ -304,6 +312,7 @@ def main():
                           "bwd_target_ms": a.bwd_ms, "bwd_scale": scale,
                           "launch": a.launch, "gemm_sm_carveout": a.carveout,
                           "stream_ctas": a.stream_ctas, "ar_ctas": a.ar_ctas,
+                          "comm_priority": a.comm_priority,
                           "bucketed_equals_unbucketed_bitwise": same,
                           "gemm_1024_ms": gemm_ms}))
     comm.finalize()
