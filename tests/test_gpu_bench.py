@@ -52,6 +52,10 @@ def test_bench_n1_contract():
     assert len(lines) == 1, p.stdout
     d = _check(lines[0], 1)
     assert d["roofline"]["bound"] == "hbm" and d["cpu_baseline"]["kind"] == "oracle"
+    assert d["cpu_baseline"]["cores"] == 1
+    if (os.cpu_count() or 1) > 1:  # SURVEY d.5 (ii): the partitioned oracle on every core
+        th = d["cpu_baseline"]["threaded"]
+        assert th["cores"] == os.cpu_count() and th["value"] > 0
 
 
 def test_bench_n2_torchrun_contract():
