@@ -117,7 +117,7 @@ def compare(gpu, ora, N, check_buffers=True):
 RAGGED = [(1,), (3,), (4097,), (8191,), (100, 100), (65,), (2, 3, 5), (12289,), (7,)]
 
 
-@pytest.mark.parametrize("N", [1, 2, 3, 4, 5, 8])
+@pytest.mark.parametrize("N", [1, 2, 3, 4, 5, 6, 7, 8])
 @pytest.mark.parametrize("dtype", ["fp32", "fp16"])
 @pytest.mark.parametrize("algo", ["oneshot", "twoshot"])
 def test_mlp_parity_bitexact(cmn, orc, N, dtype, algo):
