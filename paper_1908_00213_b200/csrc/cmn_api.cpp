@@ -342,6 +342,14 @@ cmn_status cmn_step_host_packed(cmn_comm *c, const float *host_grads, float *hos
     // N = 1: pipeline H2D(piece p+1) || update(piece p) || D2H(piece p-1) on
     // two copy engines and the caller's stream, over item ranges.
     if (cmn_status st = ensure_side_streams(c); st != CMN_OK) return st;
+    // Separate parameter tensors: each piece's updated params are first
+    // packed (fp32, on the caller's stream, 8 B/param of HBM) into a staging
+    // buffer in the packed layout, so the piece leaves in ONE device->host
+    // copy instead of one per tensor (every extra pinned copy costs ~15-30 us
+    // of copy-engine time while the other direction is busy).
+    const bool stage_params = host_params && !c->params_flat && !env_size("CMN_E2E_PER_TENSOR_D2H", 0);
+    if (stage_params)
+        if (cmn_status st = ensure_pstage(c, s); st != CMN_OK) return st;
     const auto pieces = e2e_item_pieces(c);
     const int I = c->item_begin[c->T];
     int last = c->T - 1;                  // end of the last tensor's data: contiguous
@@ -371,13 +379,27 @@ cmn_status cmn_step_host_packed(cmn_comm *c, const float *host_grads, float *hos
                             "update_direct");
         });
         if (st != CMN_OK) return st;
+        if (stage_params) {
+            st = for_groups(c, 0, c->T, [&](int lo, int hi, int g0, int g1) {
+                const int a = g0 > i0 ? g0 : i0, b = g1 < i1 ? g1 : i1;
+                if (a >= b) return CMN_OK;
+                return launched(c,
+                                launch_pack(make_tab(const_cast<const float *const *>(c->params.data()),
+                                                     lo, hi),
+                                            hi - lo, lo, c->d_td, c->d_items, a, b, CMN_FP32,
+                                            c->d_pstage, s),
+                                "pack_params");
+            });
+            if (st != CMN_OK) return st;
+        }
         if (host_params) {
             CMN_CUDA(cudaEventRecord(ev_upd, s));
             CMN_CUDA(cudaStreamWaitEvent(c->d2h, ev_upd, 0));
-            if (c->params_flat) {
+            if (c->params_flat || stage_params) {
+                const float *src = stage_params ? c->d_pstage : c->params[0];
                 const int64_t hi = e1 < flat_end ? e1 : flat_end;
                 if (hi > e0)
-                    CMN_CUDA(cudaMemcpyAsync(host_params + e0, c->params[0] + e0,
+                    CMN_CUDA(cudaMemcpyAsync(host_params + e0, src + e0,
                                              static_cast<size_t>(hi - e0) * 4,
                                              cudaMemcpyDeviceToHost, c->d2h));
             } else {

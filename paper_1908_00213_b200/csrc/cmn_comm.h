@@ -109,6 +109,7 @@ struct cmn_comm {
     float *d_mom = nullptr;       // L floats, tensor t at off[t]
     float *d_adam = nullptr;      // 2 L floats (m then v), lazily
     float *d_staging = nullptr;   // host e2e staging, world_sim * L floats
+    float *d_pstage = nullptr;    // N = 1 e2e: params packed for one D2H per piece, L floats
     size_t region_bytes = 0;
     RankBufs rb[kMaxWorld];
 
@@ -205,6 +206,7 @@ cmn_status copy_tensors(cmn_comm *c, const float *const *src, float *const *dst,
                         cudaMemcpyKind kind, cudaStream_t s);
 bool params_are_flat(const cmn_comm *c);
 cmn_status ensure_staging(cmn_comm *c);
+cmn_status ensure_pstage(cmn_comm *c, cudaStream_t s);
 cmn_status ensure_side_streams(cmn_comm *c);
 
 // ------------------------------------------ step schedules (cmn_schedules.cpp)

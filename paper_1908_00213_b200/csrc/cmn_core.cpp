@@ -96,6 +96,8 @@ void free_registration(cmn_comm *c) {
     cudaFree(c->d_mom);
     cudaFree(c->d_adam);
     cudaFree(c->d_staging);
+    cudaFree(c->d_pstage);
+    c->d_pstage = nullptr;
     c->d_td = nullptr;
     c->d_items = nullptr;
     c->d_mom = c->d_adam = c->d_staging = nullptr;
@@ -392,6 +394,14 @@ cmn_status ensure_staging(cmn_comm *c) {
     const int nsim = c->simulated ? c->world : 1;
     const size_t b = static_cast<size_t>(c->L > 0 ? c->L : 1) * 4 * nsim;
     if (cudaMalloc(&c->d_staging, b) != cudaSuccess) return fail(CMN_ERR_OOM, "staging alloc");
+    return CMN_OK;
+}
+
+cmn_status ensure_pstage(cmn_comm *c, cudaStream_t s) {
+    if (c->d_pstage) return CMN_OK;
+    const size_t b = static_cast<size_t>(c->L > 0 ? c->L : 1) * 4;
+    if (cudaMalloc(&c->d_pstage, b) != cudaSuccess) return fail(CMN_ERR_OOM, "param staging alloc");
+    CMN_CUDA(cudaMemsetAsync(c->d_pstage, 0, b, s));   // pads stay +0 (only items are packed)
     return CMN_OK;
 }
 

@@ -6,6 +6,7 @@
 #include "cmn_comm.h"
 
 #include <cmath>
+#include <cstdlib>
 #include <iterator>
 
 namespace cmn::rt {
@@ -212,12 +213,24 @@ cmn_status update_range_adam(cmn_comm *c, int ta, int tb, const ArResult &res, c
 
 // Item ranges [i0, i1) of the N = 1 host-buffer pipeline (item = 4096
 // elements of one tensor, so a tensor may straddle pieces), sized by
-// kE2EWeights -- or CMN_E2E_PIECES equal pieces (measurement).
+// kE2EWeights -- or CMN_E2E_PIECES equal pieces, or CMN_E2E_WEIGHTS="w0,w1,..."
+// (measurement switches).
 std::vector<std::pair<int, int>> e2e_item_pieces(const cmn_comm *c) {
     const int I = c->item_begin[c->T];
     std::vector<int> wts(std::begin(kE2EWeights), std::end(kE2EWeights));
     if (const size_t n = env_size("CMN_E2E_PIECES", 0); n > 0)
         wts.assign(n < static_cast<size_t>(kE2EMaxPieces) ? n : kE2EMaxPieces, 1);
+    if (const char *e = std::getenv("CMN_E2E_WEIGHTS"); e && *e) {
+        std::vector<int> w;
+        for (const char *q = e; *q && static_cast<int>(w.size()) < kE2EMaxPieces;) {
+            char *end = nullptr;
+            const long v = std::strtol(q, &end, 10);
+            if (end == q) break;
+            if (v > 0) w.push_back(static_cast<int>(v));
+            q = *end == ',' ? end + 1 : end;
+        }
+        if (!w.empty()) wts = w;
+    }
     int64_t total = 0;
     for (int w : wts) total += w;
     std::vector<std::pair<int, int>> out;
@@ -272,7 +285,9 @@ cmn_status ensure_comm_stream(cmn_comm *c, size_t n_events) {
 
 // Device->host copy of the parameters of tensors [ta, tb) into the packed
 // host layout: one copy when the params are one flat allocation (stopping
-// at the last tensor's end), else one per tensor.
+// at the last tensor's end); separate tensors are first packed into the
+// staging buffer d_pstage on `s` and leave in one copy as well (per-tensor
+// copies with CMN_E2E_PER_TENSOR_D2H=1, measurement switch).
 cmn_status d2h_params(cmn_comm *c, int ta, int tb, float *host_params, cudaStream_t s) {
     if (c->params_flat) {
         int last = c->T - 1;
@@ -284,9 +299,30 @@ cmn_status d2h_params(cmn_comm *c, int ta, int tb, float *host_params, cudaStrea
                                      cudaMemcpyDeviceToHost, s));
         return CMN_OK;
     }
+    if (tb <= ta) return CMN_OK;
+    std::vector<const float *> src(c->params.begin(), c->params.end());
+    if (!env_size("CMN_E2E_PER_TENSOR_D2H", 0)) {
+        // separate tensors: pack them (fp32, on `s`) into the staging buffer
+        // in the packed layout, then ONE copy for the whole range
+        if (cmn_status st = ensure_pstage(c, s); st != CMN_OK) return st;
+        if (cmn_status st = for_groups(c, ta, tb, [&](int lo, int hi, int i0, int i1) {
+                return launched(c,
+                                launch_pack(make_tab(src.data(), lo, hi), hi - lo, lo, c->d_td,
+                                            c->d_items, i0, i1, CMN_FP32, c->d_pstage, s),
+                                "pack_params");
+            });
+            st != CMN_OK)
+            return st;
+        int last = tb - 1;
+        while (last > ta && c->numel[last] == 0) --last;
+        const int64_t e0 = c->off[ta], e1 = c->off[last] + c->numel[last];
+        if (e1 > e0)
+            CMN_CUDA(cudaMemcpyAsync(host_params + e0, c->d_pstage + e0, static_cast<size_t>(e1 - e0) * 4,
+                                     cudaMemcpyDeviceToHost, s));
+        return CMN_OK;
+    }
     std::vector<float *> hp(c->T);
     for (int t = 0; t < c->T; ++t) hp[t] = host_params + c->off[t];
-    std::vector<const float *> src(c->params.begin(), c->params.end());
     return copy_tensors(c, src.data(), hp.data(), ta, tb, cudaMemcpyDeviceToHost, s);
 }
 

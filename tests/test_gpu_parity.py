@@ -1007,3 +1007,34 @@ def test_robustness_seeds_parity(cmn, orc, seed, dtype):
             for algo in ("oneshot", "twoshot"):
                 gpu, _, _ = run_gpu(cmn, shapes, N, dtype, algo, grads, params0, 0.1, 0.9)
                 compare(gpu, ora, N)
+
+
+@pytest.mark.parametrize("per_tensor", ["0", "1"])
+def test_step_host_packed_param_staging(cmn, orc, monkeypatch, per_tensor):
+    """N = 1 e2e with separate parameter tensors: the updated params leave
+    through the packed staging buffer (one D2H copy per piece; default) or
+    per tensor (CMN_E2E_PER_TENSOR_D2H=1) -- same bits.  Re-registering a
+    larger model re-sizes the staging buffer."""
+    monkeypatch.setenv("CMN_E2E_PER_TENSOR_D2H", per_tensor)
+    comm = cmn.Comm.init(0, 1, 0)
+    try:
+        for shapes in (synth.resnet50_shapes()[:9], RAGGED + synth.resnet50_shapes()[:40]):
+            sizes = [synth.numel(s) for s in shapes]
+            off, L = orc.layout(sizes)
+            params0 = synth.params(shapes, seed=3)
+            w_o = [p.copy() for p in params0]
+            v_o = [np.zeros_like(p) for p in params0]
+            comm.register_params([torch.from_numpy(p.copy()).to(DEV) for p in params0])
+            hg = torch.zeros(L, dtype=torch.float32).pin_memory()
+            hw = torch.full((L,), float("nan"), dtype=torch.float32).pin_memory()
+            for s in range(2):
+                g = synth.grads(shapes, workers=1, step=s, seed=3)
+                for t in range(len(sizes)):
+                    hg[off[t]: off[t] + sizes[t]].copy_(torch.from_numpy(g[0][t].reshape(-1)))
+                orc.step(g, w_o, v_o, 0.1, 0.9, "fp32")
+                comm.step_host_packed(hg, hw, "fp32", 0.1, 0.9)
+                torch.cuda.synchronize()
+                for t in range(len(sizes)):
+                    assert_bitwise(hw.numpy()[off[t]: off[t] + sizes[t]].copy(), w_o[t], f"host w[{t}] step {s}")
+    finally:
+        comm.finalize()
