@@ -21,9 +21,9 @@
  *   3. all-reduce r[j] = tree(b_0[j], ..., b_{N-1}[j]), fp32 additions
  *                 ("obtain and distribute the sum of gradients", §6.1.2)
  *   4. fp16 only  r[j] <- fp16_RNE(r[j]) (payload stays half precision)
- *   5. average    a = r * fl32(1/N)
+ *   5. average    a = r / N, one IEEE fp32 division (correctly rounded)
  *                 ("calculates the average of gradients by dividing the sum by the
- *                  number of replicas", §6.1.2)
+ *                  number of replicas", §6.1.2; reading R3)
  *   6. update     v' = fmaf(mu, v, a); w' = fmaf(-lr, v', w)   (momentum SGD,
  *                 the optimizer multi_node_optimizer wraps, §6.3;
  *                 form v = mu v + g, w -= lr v from SPEC.md:462)
@@ -187,13 +187,13 @@ void orc_update_momentum_sgd(int T, const int64_t *n, const int64_t *off,
                              const void *r, int dtype, int N, float lr, float mu,
                              float *const *w, float *const *v, float *const *a_out)
 {
-    float inv_n = 1.0f / (float)N;
+    float n_rep = (float)N;              /* "dividing the sum by the number of replicas" */
     for (int t = 0; t < T; ++t) {
         for (int64_t k = 0; k < n[t]; ++k) {
             int64_t j = off[t] + k;
             float rj = dtype == ORC_FP32 ? ((const float *)r)[j]
                                          : orc_f16_to_f32(((const uint16_t *)r)[j]);
-            float a = rj * inv_n;
+            float a = rj / n_rep;
             float vn = fmaf(mu, v[t][k], a);
             float wn = fmaf(-lr, vn, w[t][k]);
             v[t][k] = vn;
@@ -216,7 +216,7 @@ void orc_update_adam(int T, const int64_t *n, const int64_t *off,
                      float beta2, float eps, int step,
                      float *const *w, float *const *m, float *const *v)
 {
-    float inv_n = 1.0f / (float)N;
+    float n_rep = (float)N;
     double b1t = pow((double)beta1, (double)step);
     double b2t = pow((double)beta2, (double)step);
     float alpha_t = (float)((double)alpha * sqrt(1.0 - b2t) / (1.0 - b1t));
@@ -226,7 +226,7 @@ void orc_update_adam(int T, const int64_t *n, const int64_t *off,
             int64_t j = off[t] + k;
             float rj = dtype == ORC_FP32 ? ((const float *)r)[j]
                                          : orc_f16_to_f32(((const uint16_t *)r)[j]);
-            float a = rj * inv_n;
+            float a = rj / n_rep;
             float mn = beta1 * m[t][k] + c1 * a;
             float vn = beta2 * v[t][k] + c2 * (a * a);
             float den = sqrtf(vn) + eps;

@@ -58,19 +58,19 @@ def test_reduce_bruteforce_exact_bound(orc, N):
 
 @pytest.mark.parametrize("N", [1, 2, 4, 8])
 def test_identical_workers_return_gradient(orc, N):
-    """N identical workers -> r * (1/N) == g bit-exact (north star invariant)."""
+    """N identical workers -> r / N == g bit-exact (north star invariant)."""
     shapes = synth.mlp_shapes()
     sizes = [synth.numel(s) for s in shapes]
     off, L = orc.layout(sizes)
     g = synth.grads(shapes, workers=N, value_set="identical")
     packed = [orc.pack(gw, off, L, "fp32") for gw in g]
     r = orc.reduce_tree(packed, "fp32")
-    a = (r * np.float32(1.0 / N)).astype(np.float32)
+    a = (r / np.float32(N)).astype(np.float32)
     assert np.array_equal(a.view(np.uint32), packed[0].view(np.uint32))
     # fp16 payload: tree(N * h) = N*h exactly, rounded once -> h; avg -> widen(h)
     p16 = [orc.pack(gw, off, L, "fp16") for gw in g]
     r16 = orc.reduce_tree(p16, "fp16")
-    a16 = orc.f16_to_f32(r16) * np.float32(1.0 / N)
+    a16 = orc.f16_to_f32(r16) / np.float32(N)
     assert np.array_equal(a16.astype(np.float32), orc.f16_to_f32(p16[0]))
 
 

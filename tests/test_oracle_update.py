@@ -50,6 +50,22 @@ def test_spec_average_example(orc):
     assert np.array_equal(a, (g * np.float32(ex["expected_factor"])).astype(np.float32))
 
 
+def test_average_divides_by_replica_count_n3(orc):
+    """Hand-derived pin of reading R3 at N = 3 ("dividing
+    the sum by the number of replicas"), where dividing and multiplying by
+    the rounded reciprocal differ.  Workers send 5, 0, 0: the tree sum is 5
+    exactly.  5/3 = 1.0101010...(binary); rounded to 24 bits the discarded
+    tail 0.1010... of an ulp is above a half -> 1.01010101010101010101011
+    = 0x3FD55555 (1.66666662693...).  The reciprocal route gives
+    5 * RN(1/3) = 5 * 0x3EAAAAAB = 55924055 / 2^25 = 1.66666671633...,
+    which rounds to 0x3FD55556 -- so a dropped division shows up here."""
+    w = np.zeros(1, np.float32)
+    v = np.zeros(1, np.float32)
+    a = _one_tensor_step(orc, [[5.0], [0.0], [0.0]], w, v, 0.0, 0.0)
+    assert int(a.view(np.uint32)[0]) == 0x3FD55555
+    assert int(v.view(np.uint32)[0]) == 0x3FD55555      # mu = 0: v' = a
+
+
 def test_momentum_zero_is_sgd_exact_rounding(orc):
     """mu = 0: v' = a, w' = round(w - lr*a) correctly rounded (one fma)."""
     rng = np.random.default_rng(7)
@@ -65,10 +81,12 @@ def test_momentum_zero_is_sgd_exact_rounding(orc):
         assert w[k] == round_f32(Fraction(float(w0[k])) - Fraction(float(lr)) * Fraction(float(g[k])))
 
 
-@pytest.mark.parametrize("N", [1, 2, 3, 8])
+@pytest.mark.parametrize("N", [1, 2, 3, 5, 6, 7, 8])
 def test_update_is_correctly_rounded_fma(orc, N):
     """v' = RN(mu v + a), w' = RN(w - lr v') checked in exact rationals, with
-    a = RN(r * RN(1/N)) and r the oracle's reduced sum (pinned elsewhere)."""
+    a = RN(r / N) ("dividing the sum by the number of replicas",
+    PAPER.md:453-454; reading R3) and r the oracle's reduced sum (pinned
+    elsewhere)."""
     rng = np.random.default_rng(11 + N)
     n = 200
     gs = [rng.standard_normal(n).astype(np.float32) for _ in range(N)]
@@ -78,9 +96,8 @@ def test_update_is_correctly_rounded_fma(orc, N):
     w, v = w0.copy(), v0.copy()
     res = orc.step([[g] for g in gs], [w], [v], lr, mu, "fp32", want_avg=True)
     r = res["reduced"]
-    inv = round_f32(Fraction(1, N))
     for k in range(n):
-        a = round_f32(Fraction(float(r[k])) * Fraction(float(inv)))
+        a = round_f32(Fraction(float(r[k])) / N)
         assert res["avg"][0][k] == a
         vn = fma_f32(mu, v0[k], a)
         wn = fma_f32(-lr, vn, w0[k])
