@@ -132,16 +132,34 @@ def _stream(stream) -> int:
     return stream.cuda_stream
 
 
-def _data_ptrs(tensors) -> list:
+def _data_ptrs(tensors, device=None) -> list:
+    """Raw pointers of fp32 tensors.  The kernels treat every pointer as
+    contiguous fp32 on the communicator's device, so anything else is
+    refused here (CMN_ERR_INVALID_ARG) instead of faulting on the GPU:
+    device=int requires CUDA tensors on that device, device="cpu" host
+    tensors (the host-buffer step), None skips the placement check."""
     out = []
     for t in tensors:
         if isinstance(t, int):
             out.append(t)
             continue
+        if t.dtype != _torch().float32:
+            raise CmnError(1, "marshal", f"tensors must be float32 (got {t.dtype})")
         if not t.is_contiguous():
             raise CmnError(1, "marshal", "tensors must be contiguous")
+        if device == "cpu":
+            if t.is_cuda:
+                raise CmnError(1, "marshal", "host-buffer calls take CPU (pinned) tensors")
+        elif device is not None:
+            if not t.is_cuda or t.device.index != device:
+                raise CmnError(1, "marshal", f"tensors must be on cuda:{device} (got {t.device})")
         out.append(t.data_ptr())
     return out
+
+
+def _torch():
+    import torch
+    return torch
 
 
 class PtrTable:
@@ -149,12 +167,12 @@ class PtrTable:
     every step, as a framework's persistent .grad buffers are): building it
     costs ~1 us per tensor in Python, so hot loops build it once."""
 
-    def __init__(self, tensors):
+    def __init__(self, tensors, device=None):
         if tensors and isinstance(tensors[0], (list, tuple)):
             tensors = [g for gw in tensors for g in gw]
         self.tensors = list(tensors)          # keep the storage alive
         self.n = len(self.tensors)
-        self.arr = _ptr_array(_data_ptrs(self.tensors))
+        self.arr = _ptr_array(_data_ptrs(self.tensors, device))
 
 
 class _DevArray:
@@ -277,7 +295,7 @@ class Comm:
     def register_params(self, params) -> None:
         shapes = [tuple(p.shape) for p in params]
         nd, dims = _shapes_args(shapes)
-        arr = _ptr_array(_data_ptrs(params))
+        arr = _ptr_array(_data_ptrs(params, self.device))
         _check(lib().cmn_register_params(self._h, len(params), nd, dims, arr), "cmn_register_params")
         self.T = len(params)
         self.shapes = shapes
@@ -292,7 +310,7 @@ class Comm:
     # the step ---------------------------------------------------------------
     def prepare(self, grads) -> PtrTable:
         """Marshal a gradient table once (see PtrTable)."""
-        return PtrTable(grads)
+        return PtrTable(grads, self.device)
 
     def _grad_table(self, grads):
         if isinstance(grads, PtrTable):
@@ -301,7 +319,7 @@ class Comm:
             flat = [g for gw in grads for g in gw]
         else:
             flat = list(grads)
-        return _ptr_array(_data_ptrs(flat))
+        return _ptr_array(_data_ptrs(flat, self.device))
 
     def allreduce_grads(self, grads, dtype="fp32", stream=None):
         _check(lib().cmn_allreduce_grads(self._h, self._grad_table(grads), _dt(dtype), _stream(stream)),
@@ -319,20 +337,23 @@ class Comm:
                                       _stream(stream)), "cmn_step_sharded")
 
     def step_host(self, host_grads, host_params=None, dtype="fp32", lr=0.1, mu=0.9, stream=None):
-        g = self._grad_table(host_grads)
-        p = _ptr_array(_data_ptrs(host_params)) if host_params is not None else None
+        flat = [x for gw in host_grads for x in gw] if host_grads and isinstance(host_grads[0], (list, tuple)) \
+            else list(host_grads)
+        g = _ptr_array(_data_ptrs(flat, "cpu"))
+        p = _ptr_array(_data_ptrs(host_params, "cpu")) if host_params is not None else None
         _check(lib().cmn_step_host(self._h, g, p, _dt(dtype), lr, mu, _stream(stream)), "cmn_step_host")
 
     def step_host_packed(self, host_grads_flat, host_params_flat=None, dtype="fp32", lr=0.1, mu=0.9,
                          stream=None):
         """host_grads_flat: pinned float32 tensor of L (x world, simulated) elements in the
         packed layout; host_params_flat: None or L elements receiving the new params."""
+        _data_ptrs([host_grads_flat] + ([host_params_flat] if host_params_flat is not None else []), "cpu")
         hp = host_params_flat.data_ptr() if host_params_flat is not None else None
         _check(lib().cmn_step_host_packed(self._h, host_grads_flat.data_ptr(), hp, _dt(dtype), lr, mu,
                                           _stream(stream)), "cmn_step_host_packed")
 
     def unpack_avg_grads(self, out, stream=None):
-        _check(lib().cmn_unpack_avg_grads(self._h, _ptr_array(_data_ptrs(out)), _stream(stream)),
+        _check(lib().cmn_unpack_avg_grads(self._h, _ptr_array(_data_ptrs(out, self.device)), _stream(stream)),
                "cmn_unpack_avg_grads")
 
     def step_adam(self, grads, dtype="fp32", alpha=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, step=1,

@@ -44,6 +44,7 @@ cmn_status cmn_finalize(cmn_comm *c) {
     if (c->d2h) cudaStreamDestroy(c->d2h);
     free_registration(c);
     if (c->h_err) cudaFreeHost(c->h_err);
+    if (c->d_errdev) cudaFree(c->d_errdev);
     delete c;
     return CMN_OK;
 }
@@ -252,6 +253,7 @@ cmn_status cmn_step(cmn_comm *c, const float *const *grads, cmn_dtype dtype, flo
     if (cmn_status st = set_device(c); st != CMN_OK) return st;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     c->fresh = false;
+    NvtxRange nv("cmn.step.direct");
     return timed(c, s, [&] {
         return for_groups(c, 0, c->T, [&](int lo, int hi, int i0, int i1) {
             return launched(c,
@@ -341,6 +343,7 @@ cmn_status cmn_step_host_packed(cmn_comm *c, const float *host_grads, float *hos
 
     // N = 1: pipeline H2D(piece p+1) || update(piece p) || D2H(piece p-1) on
     // two copy engines and the caller's stream, over item ranges.
+    NvtxRange nv("cmn.step.host_packed");
     if (cmn_status st = ensure_side_streams(c); st != CMN_OK) return st;
     // Separate parameter tensors: each piece's updated params are first
     // packed (fp32, on the caller's stream, 8 B/param of HBM) into a staging
@@ -430,13 +433,14 @@ cmn_status cmn_unpack_avg_grads(cmn_comm *c, float *const *out, void *stream) {
     if (!grads_ok(c, const_cast<const float *const *>(out), c->T, why))
         return fail(CMN_ERR_INVALID_ARG, why);
     if (cmn_status st = set_device(c); st != CMN_OK) return st;
-    const float inv_n = 1.0f / static_cast<float>(c->world);
+    const float n_rep = static_cast<float>(c->world);   // a = r / N (reading R3)
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     return for_groups(c, 0, c->T, [&](int lo, int hi, int i0, int i1) {
         return launched(c,
                         launch_unpack_avg(make_tab(const_cast<const float *const *>(out), lo, hi),
                                           lo, c->d_td, c->d_items, i0, i1,
-                                          reduced_ptr(c, c->last, 0), c->last.dtype, inv_n, s),
+                                          reduced_ptr(c, c->last, 0), c->last.dtype, n_rep,
+                                          c->d_errdev, s),
                         "unpack_avg");
     });
 }

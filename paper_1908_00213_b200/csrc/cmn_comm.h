@@ -23,6 +23,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "cmn_internal.h"
 #include "cmn_nvls.h"
@@ -123,7 +124,8 @@ struct cmn_comm {
     int ar_blocks = 0;            // cmn_set_ctas: collective grid (0 = default)
     int upd_blocks = 0;           // cmn_set_ctas: barrier-gated update grid (0 = default)
     int stream_ctas = 0;          // cmn_set_stream_ctas: cap on pack/update grids (0 = none)
-    int *h_err = nullptr, *d_err = nullptr;
+    int *h_err = nullptr, *d_err = nullptr;   // host-mapped error word (host view, device view)
+    int *d_errdev = nullptr;      // the same code in device memory: later kernels skip their stores
     uint64_t launches = 0;
     // cmn_set_kernel_timing: CUDA events around every launch of the step's
     // dominant kernels (all-reduce, fused all-gather+update, the N = 1
@@ -194,7 +196,13 @@ int ar_blocks_for(const cmn_comm *c);
 int upd_blocks_for(const cmn_comm *c, int items);
 bool grads_ok(const cmn_comm *c, const float *const *g, int count, std::string &why);
 GradTab make_tab(const float *const *g, int lo, int hi);
-Barrier make_barrier(cmn_comm *c, int tag);
+// Kernel kinds in the barrier call tag (a peer in another kind of collective
+// at the same epoch is a call-sequence mismatch).
+enum BarrierKind : int {
+    kBarOneshot = 0, kBarTwoshot = 1, kBarNvls = 2, kBarUpdateGather = 3,
+    kBarGatherParams = 4, kBarPackPush = 5
+};
+Barrier make_barrier(cmn_comm *c, int dtype, BarrierKind kind, int64_t e0 = 0, int64_t e1 = 0);
 cmn_algo choose_algo(const cmn_comm *c, size_t bytes);
 void chunk_plan(int64_t e0, int64_t e1, int world, int64_t *s, int64_t *e);
 cmn_status require_registered(const cmn_comm *c);
@@ -213,7 +221,7 @@ cmn_status ensure_side_streams(cmn_comm *c);
 cmn_status pack_phase(cmn_comm *c, int ta, int tb, const float *const *grads, int dtype, int par,
                       cudaStream_t s, void *dst_override = nullptr);
 cmn_status reduce_phase(cmn_comm *c, int ta, int tb, int dtype, uint32_t seq, cmn_algo algo,
-                        cudaStream_t s);
+                        cudaStream_t s, bool end_barrier = false);
 cmn_status begin_collective(cmn_comm *c, int ta, int tb, int dtype, cmn_algo &algo,
                             cudaStream_t s, bool graph_safe);
 cmn_status allreduce_range(cmn_comm *c, int ta, int tb, const float *const *grads, int dtype,
@@ -236,6 +244,17 @@ cmn_status step_sharded(cmn_comm *c, const float *const *grads, int dtype, float
                         cudaStream_t s);
 cmn_status step_fused(cmn_comm *c, const float *const *grads, int dtype, float lr, float mu,
                       cudaStream_t s);
+
+// NVTX range over one phase's host-side enqueue (SURVEY §5 tracing): names
+// "cmn.pack", "cmn.allreduce", "cmn.update", "cmn.step.*", so nsys / ncu
+// --nvtx captures separate the phases.  Header-only NVTX3: without an
+// attached tool each push/pop is a null-callback check.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 // ------------------------------------------------------------ templates
 // Run `f` (kernel launches on stream s) between two timing events when

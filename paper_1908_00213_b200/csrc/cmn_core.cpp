@@ -262,15 +262,20 @@ GradTab make_tab(const float *const *g, int lo, int hi) {
     return tab;
 }
 
-Barrier make_barrier(cmn_comm *c, int tag) {
+Barrier make_barrier(cmn_comm *c, int dtype, BarrierKind kind, int64_t e0, int64_t e1) {
     Barrier b{};
     for (int r = 0; r < c->world; ++r) b.flags[r] = c->rb[r].flags;
     b.epoch = c->rb[c->rank].epoch;
     b.rank = c->rank;
     b.enabled = c->simulated ? 0 : 1;
-    b.tag = static_cast<uint32_t>(tag & 3);
+    // call tag: dtype | kind | 4-bit hash of the packed range (cmn_internal.h)
+    const int64_t range[2] = {e0, e1};
+    const uint32_t h = static_cast<uint32_t>(fnv1a(0xcbf29ce484222325ull, range, sizeof(range)));
+    b.tag = (static_cast<uint32_t>(dtype) & 1u) | ((static_cast<uint32_t>(kind) & 7u) << 1) |
+            (((h ^ (h >> 4) ^ (h >> 8) ^ (h >> 12)) & 15u) << 4);
     b.timeout_ns = static_cast<uint64_t>(c->timeout_ms) * 1000000ull;
     b.err = c->d_err;
+    b.derr = c->d_errdev;
     return b;
 }
 
@@ -343,6 +348,11 @@ cmn_status init_common(int rank, int world, int dev, bool sim, cmn_allgather_fn 
         return fail(CMN_ERR_CUDA, "cannot allocate the mapped error word");
     }
     *c->h_err = 0;
+    if (cudaMalloc(&c->d_errdev, 256) != cudaSuccess || cudaMemset(c->d_errdev, 0, 256) != cudaSuccess) {
+        cudaFreeHost(c->h_err);
+        delete c;
+        return fail(CMN_ERR_CUDA, "cannot allocate the device error word");
+    }
     if (const char *a = std::getenv("CMN_ALGO")) {
         if (!std::strcmp(a, "oneshot")) c->algo = CMN_ALGO_ONESHOT;
         if (!std::strcmp(a, "twoshot")) c->algo = CMN_ALGO_TWOSHOT;

@@ -130,25 +130,48 @@ __device__ __forceinline__ uint32_t barrier_value(const Barrier &bar) {
     if (threadIdx.x == 0) {
         const uint32_t e = bar.epoch[blockIdx.x] + 1u;
         bar.epoch[blockIdx.x] = e;
-        s_val = (e << 2) | (bar.tag & 3u);
+        s_val = (e << kTagBits) | (bar.tag & kTagMask);
     }
     __syncthreads();
     return s_val;
 }
 
+// Has a collective of this communicator failed (timeout or mismatch)?  The
+// device-memory error word is set by the barrier that detected it; every
+// later kernel of the step checks it and leaves its outputs untouched.
+__device__ __forceinline__ bool comm_failed(const int *derr) {
+    return derr && *reinterpret_cast<const volatile int *>(derr) != 0;
+}
+
+__device__ __forceinline__ void record_failure(const Barrier &bar, int code) {
+    *reinterpret_cast<volatile int *>(bar.derr) = code;
+    __threadfence();
+    *reinterpret_cast<volatile int *>(bar.err) = code;
+}
+
 // Pairwise per-CTA barrier across ranks: CTA b of rank r tells CTA b of
 // every rank "my inputs for this phase are published" and waits for the
 // same from all of them.  Flag values only grow, so no reset is needed; a
-// peer at the same epoch with another tag (payload dtype or algorithm) is a
-// call-sequence mismatch.  Spins are bounded by %globaltimer (default 30 s,
-// SPEC.md:569).  Because a kernel starts only after the previous kernel on
-// its stream completed, passing the barrier also proves every peer finished
-// all its earlier collective kernels.
-__device__ __forceinline__ void cross_rank_barrier(const Barrier &bar, uint32_t value, int world,
+// peer at the same epoch with another tag (payload dtype, algorithm, kernel
+// kind or packed range) is a call-sequence mismatch.  Spins are bounded by
+// %globaltimer (default 30 s).  Because a kernel starts only
+// after the previous kernel on its stream completed, passing the barrier
+// also proves every peer finished all its earlier collective kernels.
+//
+// Returns false when the CTA must not touch data: an earlier collective of
+// this communicator already failed (the barrier is not even entered), or
+// this wait timed out / saw a mismatch.  Callers return immediately, so a
+// failed call leaves its outputs (and, through comm_failed, the parameters
+// and optimizer state the update kernels would write) untouched.
+__device__ __forceinline__ bool cross_rank_barrier(const Barrier &bar, uint32_t value, int world,
                                                    int slot) {
-    if (!bar.enabled) return;
+    if (!bar.enabled) return true;
+    __shared__ int s_dead;
+    if (threadIdx.x == 0) s_dead = comm_failed(bar.derr) ? 1 : 0;
     __syncthreads();
+    if (s_dead) return false;
     const int tid = threadIdx.x;
+    int bad = 0;
     if (tid < world) {
         const size_t cell = (static_cast<size_t>(slot) * kMaxBarrierBlocks + blockIdx.x) * kMaxWorld;
         __threadfence_system();
@@ -157,8 +180,9 @@ __device__ __forceinline__ void cross_rank_barrier(const Barrier &bar, uint32_t 
         uint64_t t0 = 0;
         for (uint32_t spin = 1;; ++spin) {
             const uint32_t v = ld_acquire_sys(mine);
-            if ((v >> 2) == (value >> 2) && v != value) {
-                *reinterpret_cast<volatile int *>(bar.err) = 2;
+            if ((v >> kTagBits) == (value >> kTagBits) && v != value) {
+                record_failure(bar, 2);
+                bad = 1;
                 break;
             }
             if (static_cast<int32_t>(v - value) >= 0) break;
@@ -167,13 +191,14 @@ __device__ __forceinline__ void cross_rank_barrier(const Barrier &bar, uint32_t 
                 if (t0 == 0) {
                     t0 = t;
                 } else if (t - t0 > bar.timeout_ns) {
-                    *reinterpret_cast<volatile int *>(bar.err) = 1;
+                    record_failure(bar, 1);
+                    bad = 1;
                     break;
                 }
             }
         }
     }
-    __syncthreads();
+    return __syncthreads_or(bad) == 0;
 }
 
 }  // namespace cmn

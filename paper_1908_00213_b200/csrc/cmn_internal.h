@@ -22,6 +22,13 @@ constexpr int kItemElems = CMN_ITEM_ELEMS;  // elements per work item (tensor-in
 constexpr int kMaxBarrierBlocks = 1024;
 constexpr int kBarrierSlots = 2;      // 0: start (inputs ready), 1: mid (reduce-scatter done)
 constexpr int kGradCap = 256;         // grad pointers carried per launch (kernel params)
+// Barrier flag value = (per-CTA epoch << kTagBits) | call tag.  The tag
+// (make_barrier): payload dtype (bit 0), kernel kind (bits 1-3) and a 4-bit
+// hash of the packed element range (bits 4-7), so a peer that issued a
+// different collective -- another dtype, algorithm or piece -- at the same
+// epoch is reported as CMN_ERR_MISMATCH instead of being paired with it.
+constexpr uint32_t kTagBits = 8;
+constexpr uint32_t kTagMask = (1u << kTagBits) - 1u;
 
 // One registered tensor (device-resident table built at registration).
 struct TensorDesc {
@@ -55,7 +62,7 @@ struct GradTab {
 // Cross-rank signalling for the P2P all-reduce.  flags[r] points at rank r's
 // signal pad (IPC-mapped for peers); pad layout:
 //   uint32 [kBarrierSlots][kMaxBarrierBlocks][kMaxWorld]
-// The value CTA b signals in a call is ((epoch[b] + 1) << 2) | tag, where
+// The value CTA b signals in a call is ((epoch[b] + 1) << kTagBits) | tag, where
 // epoch[b] is a per-CTA call counter in the rank's own device memory that
 // the kernel itself advances -- nothing call-specific is a kernel argument,
 // so a captured CUDA graph replays with fresh values.  Every rank issues the
@@ -65,10 +72,12 @@ struct Barrier {
     uint32_t *epoch;    // kMaxBarrierBlocks per-CTA counters (own memory)
     int rank;
     int enabled;        // 0 in simulated mode: stream order replaces barriers
-    uint32_t tag;       // 2 bits: payload dtype | algorithm; a same-epoch
-                        // different-tag peer is a call-sequence mismatch
+    uint32_t tag;       // kTagBits bits (dtype, kernel kind, range hash); a
+                        // same-epoch different-tag peer is a call-sequence mismatch
     uint64_t timeout_ns;
     int *err;           // host-mapped error word: 0 ok, 1 timeout, 2 mismatch
+    int *derr;          // the same code in device memory, read by every later
+                        // kernel of the communicator (comm_failed) to skip its stores
 };
 
 // Peer buffer table (packed or reduced) in 16-byte units.
@@ -88,9 +97,11 @@ cudaError_t launch_pack(const GradTab &g, int ntab, int t_lo, const TensorDesc *
                         int max_ctas = 0);
 
 // a3: update from a reduced packed buffer (payload dtype), momentum SGD.
+// derr: the communicator's device error word (NULL = unchecked); when set
+// (an earlier collective failed) the kernel leaves w and v untouched.
 cudaError_t launch_update_sgd(const TensorDesc *td, const Item *items, int i0, int i1,
-                              const void *reduced, int dtype, float inv_n, float lr, float mu,
-                              cudaStream_t s, int max_ctas = 0);
+                              const void *reduced, int dtype, float n_rep, float lr, float mu,
+                              const int *derr, cudaStream_t s, int max_ctas = 0);
 
 // a1'+a3 at N = 1: read g directly (cast through fp16 if dtype == 1).
 // wt: the parameter pointers of the same tensors; mom: momentum base (tensor
@@ -99,16 +110,16 @@ cudaError_t launch_update_direct(const GradTab &g, const GradTab &wt, int ntab, 
                                  float *mom, const Item *items, int i0, int i1, int dtype, float lr,
                                  float mu, cudaStream_t s);
 
-// write a = r * inv_n into out tensors (test hook / Chainer semantics).
+// write a = r / n_rep into out tensors (test hook / Chainer semantics).
 cudaError_t launch_unpack_avg(const GradTab &out, int t_lo, const TensorDesc *td,
                               const Item *items, int i0, int i1, const void *reduced, int dtype,
-                              float inv_n, cudaStream_t s);
+                              float n_rep, const int *derr, cudaStream_t s);
 
 // NEXT-1 Adam.
 cudaError_t launch_update_adam(const TensorDesc *td, const Item *items, int i0, int i1,
-                               const void *reduced, int dtype, float inv_n, float alpha_t,
+                               const void *reduced, int dtype, float n_rep, float alpha_t,
                                float beta1, float beta2, float c1, float c2, float eps,
-                               cudaStream_t s, int max_ctas = 0);
+                               const int *derr, cudaStream_t s, int max_ctas = 0);
 
 // NEXT-1 at N = 1: Adam straight from the gradients (no pack); m, v at
 // adam_m / adam_v + packed index; programmatic dependent launch.
@@ -118,10 +129,11 @@ cudaError_t launch_adam_direct(const GradTab &g, const GradTab &wt, int ntab, in
                                float c2, float eps, cudaStream_t s);
 
 // a2 one-shot: out[j] = tree_i(in_i[j]) for j in [e0, e1) (elements; e0, e1
-// multiples of kAlign).  Barrier slot 0 at entry when enabled.
+// multiples of kAlign).  Barrier slot 0 at entry when enabled; with
+// end_barrier also slot 1 at exit (every peer finished reading `in`).
 cudaError_t launch_allreduce_oneshot(const PeerBufs &in, int world, void *out, int64_t e0,
-                                     int64_t e1, int dtype, const Barrier &bar, int blocks,
-                                     cudaStream_t s);
+                                     int64_t e1, int dtype, bool end_barrier, const Barrier &bar,
+                                     int blocks, cudaStream_t s);
 
 // a2 two-shot.  phase bit 1: reduce-scatter of rank `rank`'s chunk from all
 // `in` buffers into red[rank]; phase bit 2: all-gather of every other
@@ -136,8 +148,8 @@ cudaError_t launch_allreduce_twoshot(const PeerBufs &in, const PeerBufs &red, in
 // NEXT-4 sharded update: momentum SGD on the items of the own chunk, also
 // writing w' into the fp32 exchange buffer (packed layout).
 cudaError_t launch_update_chunk(const TensorDesc *td, const Item *items, int i0, int i1,
-                                const void *reduced, int dtype, float *exch, float inv_n, float lr,
-                                float mu, cudaStream_t s);
+                                const void *reduced, int dtype, float *exch, float n_rep, float lr,
+                                float mu, const int *derr, cudaStream_t s);
 
 // NEXT-4 all-gather of parameters: start barrier, then copy items [i0, i1)
 // minus [s0, s1) from the owner's exchange buffer (Item.reserved = owner).
@@ -148,7 +160,7 @@ cudaError_t launch_gather_params(const TensorDesc *td, const Item *items, int i0
 // Fused all-gather + update: start barrier, then momentum SGD over the
 // chunk-clipped items [i0, i1) reading r from red.p[Item.reserved].
 cudaError_t launch_update_gather(const TensorDesc *td, const Item *items, int i0, int i1,
-                                 const PeerBufs &red, int world, int dtype, float inv_n, float lr,
+                                 const PeerBufs &red, int world, int dtype, float n_rep, float lr,
                                  float mu, const Barrier &bar, int blocks, cudaStream_t s);
 
 // Fused pack + reduce-scatter transfer (push): start barrier, then cast and

@@ -47,20 +47,33 @@ GradTabN<CAP> shrink(const GradTab &g) {
 }
 static_assert(kItemElems % (4 * kThreads) == 0, "item must be a whole number of CTA vectors");
 
-// a = r * fl(1/N); v = fma(mu, v, a); w = fma(-lr, v, w)   (readings R3, R6)
-__device__ __forceinline__ void sgd_elem(float r, float inv_n, float lr, float mu, float &w,
-                                         float &v) {
-    const float a = __fmul_rn(r, inv_n);
+// a = r / N ("dividing the sum by the number of replicas", PAPER.md:453-454,
+// reading R3: one IEEE division, __fdiv_rn); v = fma(mu, v, a);
+// w = fma(-lr, v, w) (reading R6).
+__device__ __forceinline__ float average(float r, float n_rep) { return __fdiv_rn(r, n_rep); }
+
+__device__ __forceinline__ void sgd_core(float a, float lr, float mu, float &w, float &v) {
     v = __fmaf_rn(mu, v, a);
     w = __fmaf_rn(-lr, v, w);
 }
+__device__ __forceinline__ void sgd_elem(float r, float n_rep, float lr, float mu, float &w,
+                                         float &v) {
+    sgd_core(average(r, n_rep), lr, mu, w, v);
+}
 
-__device__ __forceinline__ void sgd_vec(const float4 &r, float inv_n, float lr, float mu,
+__device__ __forceinline__ void sgd_vec(const float4 &r, float n_rep, float lr, float mu,
                                         float4 &w, float4 &v) {
-    sgd_elem(r.x, inv_n, lr, mu, w.x, v.x);
-    sgd_elem(r.y, inv_n, lr, mu, w.y, v.y);
-    sgd_elem(r.z, inv_n, lr, mu, w.z, v.z);
-    sgd_elem(r.w, inv_n, lr, mu, w.w, v.w);
+    sgd_elem(r.x, n_rep, lr, mu, w.x, v.x);
+    sgd_elem(r.y, n_rep, lr, mu, w.y, v.y);
+    sgd_elem(r.z, n_rep, lr, mu, w.z, v.z);
+    sgd_elem(r.w, n_rep, lr, mu, w.w, v.w);
+}
+// N = 1: the average is the identity (r / 1 == r exactly), no division.
+__device__ __forceinline__ void sgd_vec1(const float4 &a, float lr, float mu, float4 &w, float4 &v) {
+    sgd_core(a.x, lr, mu, w.x, v.x);
+    sgd_core(a.y, lr, mu, w.y, v.y);
+    sgd_core(a.z, lr, mu, w.z, v.z);
+    sgd_core(a.w, lr, mu, w.w, v.w);
 }
 
 // 16-byte accesses with (CS) or without the streaming hint.
@@ -202,8 +215,8 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const __grid_constant__ G
 // fp32 payload and .cs ~4 % faster for fp16.
 template <int DT>
 __device__ __forceinline__ void update_sgd_item(const Item &it, const TensorDesc &d,
-                                                const void *__restrict__ reduced, float inv_n,
-                                                float lr, float mu) {
+                                                const void *__restrict__ reduced, float n_rep,
+                                                float lr, float mu, const int *derr) {
     constexpr bool CS = DT == 1;
     float *__restrict__ w = d.w + it.k0;
     float *__restrict__ m = d.mom + it.k0;
@@ -219,18 +232,21 @@ __device__ __forceinline__ void update_sgd_item(const Item &it, const TensorDesc
             mv[u] = ld_f4<CS>(m + 4 * v);
         }
     }
+    // a failed collective (timeout / mismatch) left r stale: keep w, v
+    // (checked after the data loads are in flight, so it adds no latency)
+    if (comm_failed(derr)) return;
 #pragma unroll
     for (int u = 0; u < kVecPerThread; ++u) {
         const int v = threadIdx.x + u * kThreads;
         if (v < nv) {
-            sgd_vec(r[u], inv_n, lr, mu, wv[u], mv[u]);
+            sgd_vec(r[u], n_rep, lr, mu, wv[u], mv[u]);
             st_f4<CS>(w + 4 * v, wv[u]);
             st_f4<CS>(m + 4 * v, mv[u]);
         }
     }
     for (int k = (nv << 2) + threadIdx.x; k < it.len; k += kThreads) {
         float wk = w[k], mk = m[k];
-        sgd_elem(load_r1<DT>(reduced, base + k), inv_n, lr, mu, wk, mk);
+        sgd_elem(load_r1<DT>(reduced, base + k), n_rep, lr, mu, wk, mk);
         w[k] = wk;
         m[k] = mk;
     }
@@ -240,7 +256,8 @@ template <int DT, bool STRIDE>
 __global__ void __launch_bounds__(kThreads) k_update_sgd(const TensorDesc *__restrict__ td,
                                                          const Item *__restrict__ items, int i0,
                                                          int i1, const void *__restrict__ reduced,
-                                                         float inv_n, float lr, float mu) {
+                                                         float n_rep, float lr, float mu,
+                                                         const int *derr) {
     // PDL (see launch_pdl): descriptors are static, read before the wait.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     int ib = i0 + blockIdx.x;
@@ -248,10 +265,10 @@ __global__ void __launch_bounds__(kThreads) k_update_sgd(const TensorDesc *__res
     TensorDesc d = td[it.t];
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if constexpr (!STRIDE) {
-        update_sgd_item<DT>(it, d, reduced, inv_n, lr, mu);
+        update_sgd_item<DT>(it, d, reduced, n_rep, lr, mu, derr);
     } else {
         for (;;) {
-            update_sgd_item<DT>(it, d, reduced, inv_n, lr, mu);
+            update_sgd_item<DT>(it, d, reduced, n_rep, lr, mu, derr);
             ib += gridDim.x;
             if (ib >= i1) break;
             it = items[ib];
@@ -262,7 +279,7 @@ __global__ void __launch_bounds__(kThreads) k_update_sgd(const TensorDesc *__res
 
 // a1' + a3 at N = 1: the all-reduce is the identity, so r = cast(g) and the
 // pack is skipped (20 B/param instead of 28).  Bitwise equal to the
-// unfused path: a = cast(g) * 1.0f.
+// unfused path: a = cast(g) / 1 = cast(g).
 //
 // Addresses come from kernel-parameter tables (w) and the packed index
 // (momentum at d_mom + base): no dependent descriptor load before the first
@@ -311,7 +328,7 @@ __global__ void __launch_bounds__(kThreads) k_update_direct(const __grid_constan
                 a.z = round_through_half(a.z);
                 a.w = round_through_half(a.w);
             }
-            sgd_vec(a, 1.0f, lr, mu, wv[u], mv[u]);
+            sgd_vec1(a, lr, mu, wv[u], mv[u]);
             st(w + 4 * v, wv[u]);
             st(m + 4 * v, mv[u]);
         }
@@ -320,7 +337,7 @@ __global__ void __launch_bounds__(kThreads) k_update_direct(const __grid_constan
         float a = gp[k];
         if constexpr (DT == 1) a = round_through_half(a);
         float wk = w[k], mk = m[k];
-        sgd_elem(a, 1.0f, lr, mu, wk, mk);
+        sgd_core(a, lr, mu, wk, mk);
         w[k] = wk;
         m[k] = mk;
     }
@@ -331,12 +348,13 @@ __global__ void __launch_bounds__(kThreads) k_unpack_avg(const __grid_constant__
                                                          const TensorDesc *__restrict__ td,
                                                          const Item *__restrict__ items, int i0,
                                                          const void *__restrict__ reduced,
-                                                         float inv_n) {
+                                                         float n_rep, const int *derr) {
+    if (comm_failed(derr)) return;
     const Item it = items[i0 + blockIdx.x];
     const int64_t base = td[it.t].off + it.k0;
     float *dst = const_cast<float *>(out.p[it.t - t_lo]) + it.k0;
     for (int k = threadIdx.x; k < it.len; k += kThreads)
-        dst[k] = __fmul_rn(load_r1<DT>(reduced, base + k), inv_n);
+        dst[k] = average(load_r1<DT>(reduced, base + k), n_rep);
 }
 
 #ifndef CMN_ADAM_DIRECT_CS
@@ -354,21 +372,25 @@ constexpr int kAdamPasses = CMN_ADAM_PASSES;
 // NEXT-1: bias-corrected Adam, every operation IEEE round-to-nearest and
 // uncontracted, in the order written in the oracle (orc_update_adam).
 // 28 B/param algorithmic (read r, w, m, v; write w, m, v).
-__device__ __forceinline__ void adam_elem(float r, float inv_n, float alpha_t, float beta1,
-                                          float beta2, float c1, float c2, float eps, float &w,
-                                          float &m, float &v) {
-    const float a = __fmul_rn(r, inv_n);
+__device__ __forceinline__ void adam_core(float a, float alpha_t, float beta1, float beta2,
+                                          float c1, float c2, float eps, float &w, float &m,
+                                          float &v) {
     m = __fadd_rn(__fmul_rn(beta1, m), __fmul_rn(c1, a));
     v = __fadd_rn(__fmul_rn(beta2, v), __fmul_rn(c2, __fmul_rn(a, a)));
     const float den = __fadd_rn(__fsqrt_rn(v), eps);
     w = __fsub_rn(w, __fmul_rn(alpha_t, __fdiv_rn(m, den)));
 }
+__device__ __forceinline__ void adam_elem(float r, float n_rep, float alpha_t, float beta1,
+                                          float beta2, float c1, float c2, float eps, float &w,
+                                          float &m, float &v) {
+    adam_core(average(r, n_rep), alpha_t, beta1, beta2, c1, c2, eps, w, m, v);
+}
 
 template <int DT>
 __device__ __forceinline__ void update_adam_item(const Item &it, const TensorDesc &d,
-                                                 const void *__restrict__ reduced, float inv_n,
+                                                 const void *__restrict__ reduced, float n_rep,
                                                  float alpha_t, float beta1, float beta2, float c1,
-                                                 float c2, float eps) {
+                                                 float c2, float eps, const int *derr) {
     float *__restrict__ w = d.w + it.k0;
     float *__restrict__ m = d.adam_m + it.k0;
     float *__restrict__ v = d.adam_v + it.k0;
@@ -390,14 +412,15 @@ __device__ __forceinline__ void update_adam_item(const Item &it, const TensorDes
                 vv[u] = ld_cs_f4(v + 4 * q);
             }
         }
+        if (comm_failed(derr)) return;      // failed collective: keep w, m, v
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int q = threadIdx.x + (pass * U + u) * kThreads;
             if (q < nv) {
-                adam_elem(r[u].x, inv_n, alpha_t, beta1, beta2, c1, c2, eps, wv[u].x, mv[u].x, vv[u].x);
-                adam_elem(r[u].y, inv_n, alpha_t, beta1, beta2, c1, c2, eps, wv[u].y, mv[u].y, vv[u].y);
-                adam_elem(r[u].z, inv_n, alpha_t, beta1, beta2, c1, c2, eps, wv[u].z, mv[u].z, vv[u].z);
-                adam_elem(r[u].w, inv_n, alpha_t, beta1, beta2, c1, c2, eps, wv[u].w, mv[u].w, vv[u].w);
+                adam_elem(r[u].x, n_rep, alpha_t, beta1, beta2, c1, c2, eps, wv[u].x, mv[u].x, vv[u].x);
+                adam_elem(r[u].y, n_rep, alpha_t, beta1, beta2, c1, c2, eps, wv[u].y, mv[u].y, vv[u].y);
+                adam_elem(r[u].z, n_rep, alpha_t, beta1, beta2, c1, c2, eps, wv[u].z, mv[u].z, vv[u].z);
+                adam_elem(r[u].w, n_rep, alpha_t, beta1, beta2, c1, c2, eps, wv[u].w, mv[u].w, vv[u].w);
                 st_cs_f4(w + 4 * q, wv[u]);
                 st_cs_f4(m + 4 * q, mv[u]);
                 st_cs_f4(v + 4 * q, vv[u]);
@@ -406,7 +429,7 @@ __device__ __forceinline__ void update_adam_item(const Item &it, const TensorDes
     }
     for (int k = (nv << 2) + threadIdx.x; k < it.len; k += kThreads) {
         float wk = w[k], mk = m[k], vk = v[k];
-        adam_elem(load_r1<DT>(reduced, it.base + k), inv_n, alpha_t, beta1, beta2, c1, c2, eps,
+        adam_elem(load_r1<DT>(reduced, it.base + k), n_rep, alpha_t, beta1, beta2, c1, c2, eps,
                   wk, mk, vk);
         w[k] = wk;
         m[k] = mk;
@@ -418,19 +441,19 @@ template <int DT, bool STRIDE>
 __global__ void __launch_bounds__(kThreads) k_update_adam(const TensorDesc *__restrict__ td,
                                                           const Item *__restrict__ items, int i0,
                                                           int i1, const void *__restrict__ reduced,
-                                                          float inv_n, float alpha_t, float beta1,
+                                                          float n_rep, float alpha_t, float beta1,
                                                           float beta2, float c1, float c2,
-                                                          float eps) {
+                                                          float eps, const int *derr) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // PDL, see launch_pdl
     int ib = i0 + blockIdx.x;
     Item it = items[ib];
     TensorDesc d = td[it.t];
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if constexpr (!STRIDE) {
-        update_adam_item<DT>(it, d, reduced, inv_n, alpha_t, beta1, beta2, c1, c2, eps);
+        update_adam_item<DT>(it, d, reduced, n_rep, alpha_t, beta1, beta2, c1, c2, eps, derr);
     } else {
         for (;;) {
-            update_adam_item<DT>(it, d, reduced, inv_n, alpha_t, beta1, beta2, c1, c2, eps);
+            update_adam_item<DT>(it, d, reduced, n_rep, alpha_t, beta1, beta2, c1, c2, eps, derr);
             ib += gridDim.x;
             if (ib >= i1) break;
             it = items[ib];
@@ -444,7 +467,7 @@ __global__ void __launch_bounds__(kThreads) k_update_adam(const TensorDesc *__re
 // B/param), addresses from kernel-parameter tables and the packed index
 // (m at adam_m + base, v at adam_v + base), launched with programmatic
 // dependent launch like k_update_direct.  Same arithmetic as k_update_adam
-// with inv_n = 1, so bitwise equal to the unfused path.
+// with n_rep = 1, so bitwise equal to the unfused path.
 template <int DT, int CAP>
 __global__ void __launch_bounds__(kThreads) k_adam_direct(const __grid_constant__ GradTabN<CAP> g,
                                                           const __grid_constant__ GradTabN<CAP> wt,
@@ -486,10 +509,10 @@ __global__ void __launch_bounds__(kThreads) k_adam_direct(const __grid_constant_
                     a.z = round_through_half(a.z);
                     a.w = round_through_half(a.w);
                 }
-                adam_elem(a.x, 1.0f, alpha_t, beta1, beta2, c1, c2, eps, wv[u].x, mv[u].x, vv[u].x);
-                adam_elem(a.y, 1.0f, alpha_t, beta1, beta2, c1, c2, eps, wv[u].y, mv[u].y, vv[u].y);
-                adam_elem(a.z, 1.0f, alpha_t, beta1, beta2, c1, c2, eps, wv[u].z, mv[u].z, vv[u].z);
-                adam_elem(a.w, 1.0f, alpha_t, beta1, beta2, c1, c2, eps, wv[u].w, mv[u].w, vv[u].w);
+                adam_core(a.x, alpha_t, beta1, beta2, c1, c2, eps, wv[u].x, mv[u].x, vv[u].x);
+                adam_core(a.y, alpha_t, beta1, beta2, c1, c2, eps, wv[u].y, mv[u].y, vv[u].y);
+                adam_core(a.z, alpha_t, beta1, beta2, c1, c2, eps, wv[u].z, mv[u].z, vv[u].z);
+                adam_core(a.w, alpha_t, beta1, beta2, c1, c2, eps, wv[u].w, mv[u].w, vv[u].w);
                 st_f4<kAdamCS>(w + 4 * q, wv[u]);
                 st_f4<kAdamCS>(m + 4 * q, mv[u]);
                 st_f4<kAdamCS>(v + 4 * q, vv[u]);
@@ -500,7 +523,7 @@ __global__ void __launch_bounds__(kThreads) k_adam_direct(const __grid_constant_
         float a = gp[k];
         if constexpr (DT == 1) a = round_through_half(a);
         float wk = w[k], mk = m[k], vk = v[k];
-        adam_elem(a, 1.0f, alpha_t, beta1, beta2, c1, c2, eps, wk, mk, vk);
+        adam_core(a, alpha_t, beta1, beta2, c1, c2, eps, wk, mk, vk);
         w[k] = wk;
         m[k] = mk;
         v[k] = vk;
@@ -547,13 +570,17 @@ constexpr int kARVec = 2;                       // 16-B vectors per thread per t
 constexpr int kTileVecs = kThreads * kARVec;    // 8 KB tile
 
 // One-shot: every rank reduces the whole range [v0, v1) (16-B units).
+// With end_barrier, a second barrier (slot 1) after the loop proves every
+// peer finished reading this call's packed buffers (the pipelined step's
+// last piece needs it: its next pack into the same region is ordered only
+// after this kernel, see step_pipelined).
 template <int N, int DT>
 __global__ void __launch_bounds__(kThreads) k_oneshot(const __grid_constant__ PeerBufs in,
                                                       void *__restrict__ out, int64_t v0,
-                                                      int64_t v1,
+                                                      int64_t v1, int end_barrier,
                                                       const __grid_constant__ Barrier bar) {
     const uint32_t bv = barrier_value(bar);
-    cross_rank_barrier(bar, bv, N, 0);
+    if (!cross_rank_barrier(bar, bv, N, 0)) return;
     for (int64_t tile = v0 + static_cast<int64_t>(blockIdx.x) * kTileVecs; tile < v1;
          tile += static_cast<int64_t>(gridDim.x) * kTileVecs) {
         uint4 x[kARVec][N];
@@ -571,6 +598,7 @@ __global__ void __launch_bounds__(kThreads) k_oneshot(const __grid_constant__ Pe
             if (idx < v1) st_u4(static_cast<uint4 *>(out) + idx, reduce_lanes<N, DT>(x[u]));
         }
     }
+    if (end_barrier) cross_rank_barrier(bar, bv, N, 1);
 }
 
 struct Chunks {
@@ -590,7 +618,7 @@ __global__ void __launch_bounds__(kThreads) k_twoshot(const __grid_constant__ Pe
                                                       const __grid_constant__ Barrier bar) {
     const uint32_t bv = barrier_value(bar);
     if (phases & 1) {
-        cross_rank_barrier(bar, bv, N, 0);
+        if (!cross_rank_barrier(bar, bv, N, 0)) return;
         const int64_t s = ch.s[rank], e = ch.e[rank];
         uint4 *dst = static_cast<uint4 *>(const_cast<void *>(red.p[rank]));
         for (int64_t tile = s + static_cast<int64_t>(blockIdx.x) * kTileVecs; tile < e;
@@ -612,7 +640,7 @@ __global__ void __launch_bounds__(kThreads) k_twoshot(const __grid_constant__ Pe
         }
     }
     if (phases & 2) {
-        cross_rank_barrier(bar, bv, N, 1);
+        if (!cross_rank_barrier(bar, bv, N, 1)) return;
         uint4 *dst = static_cast<uint4 *>(const_cast<void *>(red.p[rank]));
         int64_t maxlen = 0;
 #pragma unroll
@@ -651,8 +679,8 @@ template <int DT>
 __global__ void __launch_bounds__(kThreads) k_update_chunk(const TensorDesc *__restrict__ td,
                                                            const Item *__restrict__ items, int i0,
                                                            const void *__restrict__ reduced,
-                                                           float *__restrict__ exch, float inv_n,
-                                                           float lr, float mu) {
+                                                           float *__restrict__ exch, float n_rep,
+                                                           float lr, float mu, const int *derr) {
     const Item it = items[i0 + blockIdx.x];
     const TensorDesc d = td[it.t];
     float *__restrict__ w = d.w + it.k0;
@@ -669,11 +697,12 @@ __global__ void __launch_bounds__(kThreads) k_update_chunk(const TensorDesc *__r
             mv[u] = ld_cs_f4(m + 4 * v);
         }
     }
+    if (comm_failed(derr)) return;          // failed reduce-scatter: keep w, v
 #pragma unroll
     for (int u = 0; u < kVecPerThread; ++u) {
         const int v = threadIdx.x + u * kThreads;
         if (v < nv) {
-            sgd_vec(r[u], inv_n, lr, mu, wv[u], mv[u]);
+            sgd_vec(r[u], n_rep, lr, mu, wv[u], mv[u]);
             st_cs_f4(w + 4 * v, wv[u]);
             st_cs_f4(m + 4 * v, mv[u]);
             st_u4(x + 4 * v, make_uint4(__float_as_uint(wv[u].x), __float_as_uint(wv[u].y),
@@ -682,7 +711,7 @@ __global__ void __launch_bounds__(kThreads) k_update_chunk(const TensorDesc *__r
     }
     for (int k = (nv << 2) + threadIdx.x; k < it.len; k += kThreads) {
         float wk = w[k], mk = m[k];
-        sgd_elem(load_r1<DT>(reduced, it.base + k), inv_n, lr, mu, wk, mk);
+        sgd_elem(load_r1<DT>(reduced, it.base + k), n_rep, lr, mu, wk, mk);
         w[k] = wk;
         m[k] = mk;
         x[k] = wk;
@@ -701,7 +730,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_params(const TensorDesc *__
                                                             int world,
                                                             const __grid_constant__ Barrier bar) {
     const uint32_t bv = barrier_value(bar);
-    cross_rank_barrier(bar, bv, world, 0);
+    if (!cross_rank_barrier(bar, bv, world, 0)) return;
     for (int i = i0 + blockIdx.x; i < i1; i += gridDim.x) {
         if (i >= s0 && i < s1) continue;
         const Item it = items[i];
@@ -734,11 +763,11 @@ __global__ void __launch_bounds__(kThreads) k_update_gather(const TensorDesc *__
                                                             const Item *__restrict__ items, int i0,
                                                             int i1,
                                                             const __grid_constant__ PeerBufs red,
-                                                            int world, float inv_n, float lr,
+                                                            int world, float n_rep, float lr,
                                                             float mu,
                                                             const __grid_constant__ Barrier bar) {
     const uint32_t bv = barrier_value(bar);
-    cross_rank_barrier(bar, bv, world, 0);
+    if (!cross_rank_barrier(bar, bv, world, 0)) return;
     for (int i = i0 + blockIdx.x; i < i1; i += gridDim.x) {
         const Item it = items[i];
         const TensorDesc d = td[it.t];
@@ -767,14 +796,14 @@ __global__ void __launch_bounds__(kThreads) k_update_gather(const TensorDesc *__
         for (int u = 0; u < kVecPerThread; ++u) {
             const int v = threadIdx.x + u * kThreads;
             if (v < nv) {
-                sgd_vec(r[u], inv_n, lr, mu, wv[u], mv[u]);
+                sgd_vec(r[u], n_rep, lr, mu, wv[u], mv[u]);
                 st_cs_f4(w + 4 * v, wv[u]);
                 st_cs_f4(m + 4 * v, mv[u]);
             }
         }
         for (int k = (nv << 2) + threadIdx.x; k < it.len; k += kThreads) {
             float wk = w[k], mk = m[k];
-            sgd_elem(load_r1<DT>(src, it.base + k), inv_n, lr, mu, wk, mk);
+            sgd_elem(load_r1<DT>(src, it.base + k), n_rep, lr, mu, wk, mk);
             w[k] = wk;
             m[k] = mk;
         }
@@ -797,7 +826,7 @@ __global__ void __launch_bounds__(kThreads) k_pack_push(const __grid_constant__ 
                                                         int world,
                                                         const __grid_constant__ Barrier bar) {
     const uint32_t bv = barrier_value(bar);
-    cross_rank_barrier(bar, bv, world, 0);
+    if (!cross_rank_barrier(bar, bv, world, 0)) return;
     for (int i = i0 + blockIdx.x; i < i1; i += gridDim.x) {
         const Item it = items[i];
         const float *__restrict__ src = g.p[it.t - t_lo] + it.k0;
@@ -876,7 +905,7 @@ __global__ void __launch_bounds__(kThreads) k_nvls(const char *mc_packed, char *
                                                    int64_t v0, int64_t v1, int world,
                                                    const __grid_constant__ Barrier bar) {
     const uint32_t bv = barrier_value(bar);
-    cross_rank_barrier(bar, bv, world, 0);           // every rank's pack is complete
+    if (!cross_rank_barrier(bar, bv, world, 0)) return;   // every rank's pack is complete
     fence_proxy_alias();
     // A load-reduce makes a round trip through the switch to every rank, so
     // keep more bytes in flight than the P2P kernels (which issue N loads per
@@ -975,19 +1004,19 @@ cudaError_t launch_pack(const GradTab &g, int ntab, int t_lo, const TensorDesc *
 }
 
 cudaError_t launch_update_sgd(const TensorDesc *td, const Item *items, int i0, int i1,
-                              const void *reduced, int dtype, float inv_n, float lr, float mu,
-                              cudaStream_t s, int max_ctas) {
+                              const void *reduced, int dtype, float n_rep, float lr, float mu,
+                              const int *derr, cudaStream_t s, int max_ctas) {
     const int n = grid_of(i0, i1);
     if (n == 0) return cudaSuccess;
     const int grid = capped(n, max_ctas);
     (void)cudaGetLastError();  // report this launch's error, not a stale one
     cudaError_t e;
     if (grid < n)
-        e = dtype == 0 ? launch_pdl(k_update_sgd<0, true>, grid, kThreads, s, td, items, i0, i1, reduced, inv_n, lr, mu)
-                       : launch_pdl(k_update_sgd<1, true>, grid, kThreads, s, td, items, i0, i1, reduced, inv_n, lr, mu);
+        e = dtype == 0 ? launch_pdl(k_update_sgd<0, true>, grid, kThreads, s, td, items, i0, i1, reduced, n_rep, lr, mu, derr)
+                       : launch_pdl(k_update_sgd<1, true>, grid, kThreads, s, td, items, i0, i1, reduced, n_rep, lr, mu, derr);
     else
-        e = dtype == 0 ? launch_pdl(k_update_sgd<0, false>, grid, kThreads, s, td, items, i0, i1, reduced, inv_n, lr, mu)
-                       : launch_pdl(k_update_sgd<1, false>, grid, kThreads, s, td, items, i0, i1, reduced, inv_n, lr, mu);
+        e = dtype == 0 ? launch_pdl(k_update_sgd<0, false>, grid, kThreads, s, td, items, i0, i1, reduced, n_rep, lr, mu, derr)
+                       : launch_pdl(k_update_sgd<1, false>, grid, kThreads, s, td, items, i0, i1, reduced, n_rep, lr, mu, derr);
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
@@ -1020,22 +1049,22 @@ cudaError_t launch_update_direct(const GradTab &g, const GradTab &wt, int ntab, 
 
 cudaError_t launch_unpack_avg(const GradTab &out, int t_lo, const TensorDesc *td,
                               const Item *items, int i0, int i1, const void *reduced, int dtype,
-                              float inv_n, cudaStream_t s) {
+                              float n_rep, const int *derr, cudaStream_t s) {
     const int grid = grid_of(i0, i1);
     if (grid == 0) return cudaSuccess;
     (void)cudaGetLastError();  // report this launch's error, not a stale one
     const auto t = shrink<kGradCap>(out);
     if (dtype == 0)
-        k_unpack_avg<0, kGradCap><<<grid, kThreads, 0, s>>>(t, t_lo, td, items, i0, reduced, inv_n);
+        k_unpack_avg<0, kGradCap><<<grid, kThreads, 0, s>>>(t, t_lo, td, items, i0, reduced, n_rep, derr);
     else
-        k_unpack_avg<1, kGradCap><<<grid, kThreads, 0, s>>>(t, t_lo, td, items, i0, reduced, inv_n);
+        k_unpack_avg<1, kGradCap><<<grid, kThreads, 0, s>>>(t, t_lo, td, items, i0, reduced, n_rep, derr);
     return cudaGetLastError();
 }
 
 cudaError_t launch_update_adam(const TensorDesc *td, const Item *items, int i0, int i1,
-                               const void *reduced, int dtype, float inv_n, float alpha_t,
+                               const void *reduced, int dtype, float n_rep, float alpha_t,
                                float beta1, float beta2, float c1, float c2, float eps,
-                               cudaStream_t s, int max_ctas) {
+                               const int *derr, cudaStream_t s, int max_ctas) {
     const int n = grid_of(i0, i1);
     if (n == 0) return cudaSuccess;
     const int grid = capped(n, max_ctas);
@@ -1043,14 +1072,14 @@ cudaError_t launch_update_adam(const TensorDesc *td, const Item *items, int i0, 
     cudaError_t e;
     if (grid < n)
         e = dtype == 0 ? launch_pdl(k_update_adam<0, true>, grid, kThreads, s, td, items, i0, i1, reduced,
-                                    inv_n, alpha_t, beta1, beta2, c1, c2, eps)
+                                    n_rep, alpha_t, beta1, beta2, c1, c2, eps, derr)
                        : launch_pdl(k_update_adam<1, true>, grid, kThreads, s, td, items, i0, i1, reduced,
-                                    inv_n, alpha_t, beta1, beta2, c1, c2, eps);
+                                    n_rep, alpha_t, beta1, beta2, c1, c2, eps, derr);
     else
         e = dtype == 0 ? launch_pdl(k_update_adam<0, false>, grid, kThreads, s, td, items, i0, i1, reduced,
-                                    inv_n, alpha_t, beta1, beta2, c1, c2, eps)
+                                    n_rep, alpha_t, beta1, beta2, c1, c2, eps, derr)
                        : launch_pdl(k_update_adam<1, false>, grid, kThreads, s, td, items, i0, i1, reduced,
-                                    inv_n, alpha_t, beta1, beta2, c1, c2, eps);
+                                    n_rep, alpha_t, beta1, beta2, c1, c2, eps, derr);
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
@@ -1086,9 +1115,9 @@ cudaError_t launch_adam_direct(const GradTab &g, const GradTab &wt, int ntab, in
 
 namespace {
 template <int N, int DT>
-void oneshot_n(const PeerBufs &in, void *out, int64_t v0, int64_t v1, const Barrier &bar,
+void oneshot_n(const PeerBufs &in, void *out, int64_t v0, int64_t v1, int end_bar, const Barrier &bar,
                int blocks, cudaStream_t s) {
-    k_oneshot<N, DT><<<blocks, kThreads, 0, s>>>(in, out, v0, v1, bar);
+    k_oneshot<N, DT><<<blocks, kThreads, 0, s>>>(in, out, v0, v1, end_bar, bar);
 }
 template <int N, int DT>
 void twoshot_n(const PeerBufs &in, const PeerBufs &red, int rank, const Chunks &ch, int phases,
@@ -1097,16 +1126,16 @@ void twoshot_n(const PeerBufs &in, const PeerBufs &red, int rank, const Chunks &
 }
 template <int DT>
 bool oneshot_dispatch(int world, const PeerBufs &in, void *out, int64_t v0, int64_t v1,
-                      const Barrier &bar, int blocks, cudaStream_t s) {
+                      int end_bar, const Barrier &bar, int blocks, cudaStream_t s) {
     switch (world) {
-        case 1: oneshot_n<1, DT>(in, out, v0, v1, bar, blocks, s); return true;
-        case 2: oneshot_n<2, DT>(in, out, v0, v1, bar, blocks, s); return true;
-        case 3: oneshot_n<3, DT>(in, out, v0, v1, bar, blocks, s); return true;
-        case 4: oneshot_n<4, DT>(in, out, v0, v1, bar, blocks, s); return true;
-        case 5: oneshot_n<5, DT>(in, out, v0, v1, bar, blocks, s); return true;
-        case 6: oneshot_n<6, DT>(in, out, v0, v1, bar, blocks, s); return true;
-        case 7: oneshot_n<7, DT>(in, out, v0, v1, bar, blocks, s); return true;
-        case 8: oneshot_n<8, DT>(in, out, v0, v1, bar, blocks, s); return true;
+        case 1: oneshot_n<1, DT>(in, out, v0, v1, end_bar, bar, blocks, s); return true;
+        case 2: oneshot_n<2, DT>(in, out, v0, v1, end_bar, bar, blocks, s); return true;
+        case 3: oneshot_n<3, DT>(in, out, v0, v1, end_bar, bar, blocks, s); return true;
+        case 4: oneshot_n<4, DT>(in, out, v0, v1, end_bar, bar, blocks, s); return true;
+        case 5: oneshot_n<5, DT>(in, out, v0, v1, end_bar, bar, blocks, s); return true;
+        case 6: oneshot_n<6, DT>(in, out, v0, v1, end_bar, bar, blocks, s); return true;
+        case 7: oneshot_n<7, DT>(in, out, v0, v1, end_bar, bar, blocks, s); return true;
+        case 8: oneshot_n<8, DT>(in, out, v0, v1, end_bar, bar, blocks, s); return true;
         default: return false;
     }
 }
@@ -1131,13 +1160,14 @@ inline int64_t to_vec(int64_t elems, int dtype) { return dtype == 0 ? elems / 4 
 }  // namespace
 
 cudaError_t launch_allreduce_oneshot(const PeerBufs &in, int world, void *out, int64_t e0,
-                                     int64_t e1, int dtype, const Barrier &bar, int blocks,
-                                     cudaStream_t s) {
+                                     int64_t e1, int dtype, bool end_barrier, const Barrier &bar,
+                                     int blocks, cudaStream_t s) {
     if (blocks <= 0 || blocks > kMaxBarrierBlocks) return cudaErrorInvalidValue;
     (void)cudaGetLastError();
     const int64_t v0 = to_vec(e0, dtype), v1 = to_vec(e1, dtype);
-    const bool ok = dtype == 0 ? oneshot_dispatch<0>(world, in, out, v0, v1, bar, blocks, s)
-                               : oneshot_dispatch<1>(world, in, out, v0, v1, bar, blocks, s);
+    const int eb = end_barrier ? 1 : 0;
+    const bool ok = dtype == 0 ? oneshot_dispatch<0>(world, in, out, v0, v1, eb, bar, blocks, s)
+                               : oneshot_dispatch<1>(world, in, out, v0, v1, eb, bar, blocks, s);
     return ok ? cudaGetLastError() : cudaErrorInvalidValue;
 }
 
@@ -1159,15 +1189,15 @@ cudaError_t launch_allreduce_twoshot(const PeerBufs &in, const PeerBufs &red, in
 }
 
 cudaError_t launch_update_chunk(const TensorDesc *td, const Item *items, int i0, int i1,
-                                const void *reduced, int dtype, float *exch, float inv_n, float lr,
-                                float mu, cudaStream_t s) {
+                                const void *reduced, int dtype, float *exch, float n_rep, float lr,
+                                float mu, const int *derr, cudaStream_t s) {
     const int grid = grid_of(i0, i1);
     if (grid == 0) return cudaSuccess;
     (void)cudaGetLastError();
     if (dtype == 0)
-        k_update_chunk<0><<<grid, kThreads, 0, s>>>(td, items, i0, reduced, exch, inv_n, lr, mu);
+        k_update_chunk<0><<<grid, kThreads, 0, s>>>(td, items, i0, reduced, exch, n_rep, lr, mu, derr);
     else
-        k_update_chunk<1><<<grid, kThreads, 0, s>>>(td, items, i0, reduced, exch, inv_n, lr, mu);
+        k_update_chunk<1><<<grid, kThreads, 0, s>>>(td, items, i0, reduced, exch, n_rep, lr, mu, derr);
     return cudaGetLastError();
 }
 
@@ -1181,15 +1211,15 @@ cudaError_t launch_gather_params(const TensorDesc *td, const Item *items, int i0
 }
 
 cudaError_t launch_update_gather(const TensorDesc *td, const Item *items, int i0, int i1,
-                                 const PeerBufs &red, int world, int dtype, float inv_n, float lr,
+                                 const PeerBufs &red, int world, int dtype, float n_rep, float lr,
                                  float mu, const Barrier &bar, int blocks, cudaStream_t s) {
     if (blocks <= 0 || blocks > kMaxBarrierBlocks) return cudaErrorInvalidValue;
     (void)cudaGetLastError();
     if (dtype == 0)
-        k_update_gather<0><<<blocks, kThreads, 0, s>>>(td, items, i0, i1, red, world, inv_n, lr, mu,
+        k_update_gather<0><<<blocks, kThreads, 0, s>>>(td, items, i0, i1, red, world, n_rep, lr, mu,
                                                        bar);
     else
-        k_update_gather<1><<<blocks, kThreads, 0, s>>>(td, items, i0, i1, red, world, inv_n, lr, mu,
+        k_update_gather<1><<<blocks, kThreads, 0, s>>>(td, items, i0, i1, red, world, n_rep, lr, mu,
                                                        bar);
     return cudaGetLastError();
 }

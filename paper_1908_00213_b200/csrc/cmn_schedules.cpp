@@ -15,6 +15,7 @@ namespace cmn::rt {
 // packed buffer of parity `par`.
 cmn_status pack_phase(cmn_comm *c, int ta, int tb, const float *const *grads, int dtype, int par,
                       cudaStream_t s, void *dst_override) {
+    NvtxRange nv("cmn.pack");
     const int nsim = c->simulated ? c->world : 1;
     for (int i = 0; i < nsim; ++i) {
         const int r = c->simulated ? i : c->rank;
@@ -34,7 +35,7 @@ cmn_status pack_phase(cmn_comm *c, int ta, int tb, const float *const *grads, in
 // a2 over the packed range of tensors [ta, tb) for the collective call with
 // sequence number `seq` (its buffers have parity seq & 1).
 cmn_status reduce_phase_launch(cmn_comm *c, int ta, int tb, int dtype, uint32_t seq, cmn_algo algo,
-                               cudaStream_t s) {
+                               cudaStream_t s, bool end_barrier) {
     const int par = static_cast<int>(seq & 1u);
     const int64_t e0 = c->off[ta], e1 = c->off[tb];
     const size_t esz = dtype == 0 ? 4 : 2;
@@ -45,7 +46,7 @@ cmn_status reduce_phase_launch(cmn_comm *c, int ta, int tb, int dtype, uint32_t 
     if (algo == CMN_ALGO_NVLS) {
         int64_t cs[kMaxWorld], ce[kMaxWorld];
         chunk_plan(e0, e1, c->world, cs, ce);
-        const Barrier bar = make_barrier(c, dtype | 2);
+        const Barrier bar = make_barrier(c, dtype, kBarNvls, e0, e1);
         return launched(c,
                         launch_nvls_allreduce(c->nvls.packed_mc(), c->nvls.reduced_mc(),
                                               cs[c->rank], ce[c->rank], c->world, dtype, bar,
@@ -69,14 +70,13 @@ cmn_status reduce_phase_launch(cmn_comm *c, int ta, int tb, int dtype, uint32_t 
         red.p[r] = c->rb[r].reduced[par];
     }
     const int blocks = ar_blocks_for(c);
-    const int tag = dtype | (algo == CMN_ALGO_TWOSHOT ? 2 : 0);
-    const Barrier bar = make_barrier(c, tag);
+    const Barrier bar = make_barrier(c, dtype, algo == CMN_ALGO_TWOSHOT ? kBarTwoshot : kBarOneshot, e0, e1);
     if (algo == CMN_ALGO_ONESHOT) {
         for (int i = 0; i < nsim; ++i) {
             const int r = c->simulated ? i : c->rank;
             cmn_status st = launched(c,
                                      launch_allreduce_oneshot(in, c->world, c->rb[r].reduced[par],
-                                                              e0, e1, dtype, bar, blocks, s),
+                                                              e0, e1, dtype, end_barrier, bar, blocks, s),
                                      "allreduce_oneshot");
             if (st != CMN_OK) return st;
         }
@@ -102,9 +102,10 @@ cmn_status reduce_phase_launch(cmn_comm *c, int ta, int tb, int dtype, uint32_t 
 }
 
 cmn_status reduce_phase(cmn_comm *c, int ta, int tb, int dtype, uint32_t seq, cmn_algo algo,
-                        cudaStream_t s) {
+                        cudaStream_t s, bool end_barrier) {
     if (c->world == 1 && algo != CMN_ALGO_NCCL && algo != CMN_ALGO_NVLS) return CMN_OK;
-    return timed(c, s, [&] { return reduce_phase_launch(c, ta, tb, dtype, seq, algo, s); });
+    NvtxRange nv("cmn.allreduce");
+    return timed(c, s, [&] { return reduce_phase_launch(c, ta, tb, dtype, seq, algo, s, end_barrier); });
 }
 
 // Validate and choose the algorithm for one collective over [ta, tb).
@@ -166,11 +167,12 @@ const void *reduced_ptr(const cmn_comm *c, const ArResult &res, int rank) {
 
 cmn_status update_range(cmn_comm *c, int ta, int tb, const ArResult &res, float lr, float mu,
                         cudaStream_t s) {
-    const float inv_n = 1.0f / static_cast<float>(c->world);
+    NvtxRange nv("cmn.update");
+    const float n_rep = static_cast<float>(c->world);   // a = r / N (reading R3)
     return for_groups(c, ta, tb, [&](int, int, int i0, int i1) {
         return launched(c,
                         launch_update_sgd(c->d_td, c->d_items, i0, i1, reduced_ptr(c, res, 0),
-                                          res.dtype, inv_n, lr, mu, s, c->stream_ctas),
+                                          res.dtype, n_rep, lr, mu, c->d_errdev, s, c->stream_ctas),
                         "update_sgd");
     });
 }
@@ -201,12 +203,13 @@ AdamArgs adam_args(float alpha, float beta1, float beta2, float eps, int step) {
 
 cmn_status update_range_adam(cmn_comm *c, int ta, int tb, const ArResult &res, const AdamArgs &a,
                              cudaStream_t s) {
-    const float inv_n = 1.0f / static_cast<float>(c->world);
+    NvtxRange nv("cmn.update_adam");
+    const float n_rep = static_cast<float>(c->world);   // a = r / N (reading R3)
     return for_groups(c, ta, tb, [&](int, int, int i0, int i1) {
         return launched(c,
                         launch_update_adam(c->d_td, c->d_items, i0, i1, reduced_ptr(c, res, 0),
-                                           res.dtype, inv_n, a.alpha_t, a.beta1, a.beta2, a.c1,
-                                           a.c2, a.eps, s, c->stream_ctas),
+                                           res.dtype, n_rep, a.alpha_t, a.beta1, a.beta2, a.c1,
+                                           a.c2, a.eps, c->d_errdev, s, c->stream_ctas),
                         "update_adam");
     });
 }
@@ -330,9 +333,14 @@ cmn_status d2h_params(cmn_comm *c, int ta, int tb, float *host_params, cudaStrea
 // piece is one collective call.  Caller stream s: pack(0..P-1), then
 // update(p) after all-reduce(p); communication stream: all-reduce(p) after
 // pack(p).  HBM-bound packs/updates overlap the NVLink-bound all-reduces.
-// Buffer reuse is safe for P >= 2: a piece's next pack (seq + P) is issued
-// after update(P-1), i.e. after our all-reduce at seq + P - 1 passed its
-// start barrier, so every peer finished all-reduce calls <= seq + P - 2.
+// Buffer reuse: a piece's next pack (next step, or the next replay of a
+// captured step) is issued after update(P-1), i.e. after our all-reduce of
+// the last piece passed its start barrier, so every peer finished the
+// all-reduces of pieces 0..P-2.  The last piece itself is covered by that
+// all-reduce's own end: two-shot's mid barrier (every peer finished its
+// reduce-scatter reads of our packed buffer) or NVLS's end barrier, and for
+// one-shot -- which reads every packed buffer to the end and has no later
+// barrier -- an explicit end barrier on the last piece (slot 1).
 // With `io`, the e2e form: H2D(piece p) on a copy stream feeds pack(p), and
 // D2H(piece p) on a second copy stream follows update(p), so PCIe in both
 // directions overlaps the packs, NVLink all-reduces and updates of the
@@ -340,6 +348,7 @@ cmn_status d2h_params(cmn_comm *c, int ta, int tb, float *host_params, cudaStrea
 // pointers `grads` are).
 cmn_status step_pipelined(cmn_comm *c, const float *const *grads, int dtype, float lr, float mu,
                           cudaStream_t s, const HostIO *io, const AdamArgs *adam) {
+    NvtxRange nv("cmn.step.pipelined");
     const auto pieces = equal_ranges(c, c->pipe_pieces);
     const size_t P = pieces.size();
     if (cmn_status st = ensure_comm_stream(c, 2 * P + 1); st != CMN_OK) return st;
@@ -386,7 +395,7 @@ cmn_status step_pipelined(cmn_comm *c, const float *const *grads, int dtype, flo
         CMN_CUDA(cudaEventRecord(c->pev[2 * p], s));
         CMN_CUDA(cudaStreamWaitEvent(c->sc, c->pev[2 * p], 0));
         if (cmn_status st = reduce_phase(c, pieces[p].first, pieces[p].second, dtype, seq, algo[p],
-                                         c->sc);
+                                         c->sc, p + 1 == P);
             st != CMN_OK)
             return st;
         CMN_CUDA(cudaEventRecord(c->pev[2 * p + 1], c->sc));
@@ -424,6 +433,7 @@ cmn_status step_pipelined(cmn_comm *c, const float *const *grads, int dtype, flo
 // momentum is sharded (valid on the owner rank only).
 cmn_status step_sharded(cmn_comm *c, const float *const *grads, int dtype, float lr, float mu,
                         cudaStream_t s) {
+    NvtxRange nv("cmn.step.sharded");
     cmn_algo algo = CMN_ALGO_AUTO;
     if (cmn_status st = begin_collective(c, 0, c->T, dtype, algo, s, true); st != CMN_OK) return st;
     const int nsim = c->simulated ? c->world : 1;
@@ -439,7 +449,7 @@ cmn_status step_sharded(cmn_comm *c, const float *const *grads, int dtype, float
     int64_t cs[kMaxWorld], ce[kMaxWorld];
     chunk_plan(0, c->L, c->world, cs, ce);
     const int blocks = ar_blocks_for(c);
-    const Barrier bar = make_barrier(c, dtype | 2);
+    const Barrier bar = make_barrier(c, dtype, kBarTwoshot, 0, c->L);
     for (int i = 0; i < nsim; ++i) {
         const int r = c->simulated ? i : c->rank;
         cmn_status st = launched(c,
@@ -448,19 +458,19 @@ cmn_status step_sharded(cmn_comm *c, const float *const *grads, int dtype, float
                                  "reduce_scatter");
         if (st != CMN_OK) return st;
     }
-    const float inv_n = 1.0f / static_cast<float>(c->world);
+    const float n_rep = static_cast<float>(c->world);   // a = r / N (reading R3)
     for (int i = 0; i < nsim; ++i) {
         const int r = c->simulated ? i : c->rank;
         cmn_status st = launched(c,
                                  launch_update_chunk(c->d_td, c->d_sitems, c->sitem_begin[r],
                                                      c->sitem_begin[r + 1], c->rb[r].reduced[0], dtype,
-                                                     static_cast<float *>(c->rb[r].reduced[1]), inv_n,
-                                                     lr, mu, s),
+                                                     static_cast<float *>(c->rb[r].reduced[1]), n_rep,
+                                                     lr, mu, c->d_errdev, s),
                                  "update_chunk");
         if (st != CMN_OK) return st;
     }
     ++c->seq;
-    const Barrier bar2 = make_barrier(c, 3);
+    const Barrier bar2 = make_barrier(c, dtype, kBarGatherParams);
     const int total = c->sitem_begin[c->world];
     const int gblocks = upd_blocks_for(c, total);
     for (int i = 0; i < nsim; ++i) {
@@ -482,6 +492,7 @@ cmn_status step_sharded(cmn_comm *c, const float *const *grads, int dtype, float
 // sharded step), so the schedule is graph-safe.
 cmn_status step_fused(cmn_comm *c, const float *const *grads, int dtype, float lr, float mu,
                       cudaStream_t s) {
+    NvtxRange nv("cmn.step.fused");
     cmn_algo algo = CMN_ALGO_AUTO;
     if (cmn_status st = begin_collective(c, 0, c->T, dtype, algo, s, true); st != CMN_OK) return st;
     const int nsim = c->simulated ? c->world : 1;
@@ -493,7 +504,7 @@ cmn_status step_fused(cmn_comm *c, const float *const *grads, int dtype, float l
     chunk_plan(0, c->L, c->world, cs, ce);
     const int blocks = ar_blocks_for(c);
     const int total = c->sitem_begin[c->world];
-    const Barrier bar = make_barrier(c, dtype | 2);
+    const Barrier bar = make_barrier(c, dtype, kBarTwoshot, 0, c->L);
     // Push form (fused_update == 2, one grad table): owner o's inbox is its
     // packed[0] buffer, slot i (rank i's contribution to chunk o) at
     // i * cmax payload elements; view(o, i) + j addresses packed index j.
@@ -507,7 +518,7 @@ cmn_status step_fused(cmn_comm *c, const float *const *grads, int dtype, float l
     };
     cmn_status st = CMN_OK;
     if (push) {
-        const Barrier bar0 = make_barrier(c, dtype | 2);
+        const Barrier bar0 = make_barrier(c, dtype, kBarPackPush);
         st = timed(c, s, [&] {
             for (int i = 0; i < nsim; ++i) {
                 const int r = c->simulated ? i : c->rank;
@@ -543,13 +554,13 @@ cmn_status step_fused(cmn_comm *c, const float *const *grads, int dtype, float l
     });
     if (st != CMN_OK) return st;
     ++c->seq;
-    const Barrier bar2 = make_barrier(c, dtype);
+    const Barrier bar2 = make_barrier(c, dtype, kBarUpdateGather);
     const int gblocks = upd_blocks_for(c, total);
     // simulated ranks share one parameter replica: one launch updates it all
     st = timed(c, s, [&] {
         return launched(c,
                         launch_update_gather(c->d_td, c->d_sitems, 0, total, red, c->world, dtype,
-                                             1.0f / static_cast<float>(c->world), lr, mu, bar2,
+                                             static_cast<float>(c->world), lr, mu, bar2,
                                              gblocks, s),
                         "update_gather");
     });

@@ -20,9 +20,17 @@ Overlap: with bucket_bytes set, a post-accumulate-grad
 hook counts ready gradients per bucket (buckets are reverse-order contiguous
 tensor ranges) and launches cmn_allreduce_bucket on a communication stream
 as soon as a bucket is complete, while backward keeps running; step() then
-waits and applies cmn_update_bucket per bucket.
+waits and applies cmn_update_bucket per bucket.  Buckets assume ONE backward
+per step(); gradient-accumulation micro-batches run under no_sync() (their
+hooks launch nothing, the last backward outside it does), and a second
+backward that would re-launch a bucket before step() raises instead of
+silently all-reducing a partial gradient.  Bucketed overlap is momentum-SGD
+only (the bucket update is cmn_update_bucket); optimizer="adam" with
+bucket_bytes is refused.
 """
 from __future__ import annotations
+
+import contextlib
 
 import torch
 
@@ -33,6 +41,11 @@ class MultiNodeOptimizer:
     def __init__(self, params, comm: Comm, lr: float = 0.1, momentum: float = 0.9,
                  dtype: str = "fp32", bucket_bytes: int | None = None, optimizer: str = "momentum_sgd",
                  adam=(1e-3, 0.9, 0.999, 1e-8), stream_ctas: int = 0):
+        if bucket_bytes and optimizer != "momentum_sgd":
+            raise ValueError("bucketed overlap (bucket_bytes) applies momentum SGD per bucket; "
+                             f"optimizer={optimizer!r} is not supported with it")
+        if optimizer not in ("momentum_sgd", "adam"):
+            raise ValueError(f"unknown optimizer {optimizer!r}")
         self.comm = comm
         # overlap: cap the pack/update grids so they share SMs with the
         # backward instead of taking every free slot (cmn_set_stream_ctas;
@@ -47,6 +60,7 @@ class MultiNodeOptimizer:
         self._hooks = []
         self._stream = None
         self._launched = set()
+        self._no_sync = False
         self._table, self._table_key = None, None
         self._setup(list(params))
 
@@ -60,6 +74,9 @@ class MultiNodeOptimizer:
         self.registrations += 1
         self.t = 0
         self._sig = [(id(p), tuple(p.shape)) for p in params]
+        # bucket indices of the old plan mean nothing under the new one
+        self._launched = set()
+        self._pending = []
         self.buckets = []
         if self.bucket_bytes:
             nb = self.comm.plan_buckets(self.bucket_bytes)
@@ -83,11 +100,27 @@ class MultiNodeOptimizer:
         return False
 
     # ----------------------------------------------------------------- overlap
+    @contextlib.contextmanager
+    def no_sync(self):
+        """Gradient accumulation: backwards inside launch no bucket
+        all-reduce; the step's last backward (outside) does."""
+        prev, self._no_sync = self._no_sync, True
+        try:
+            yield
+        finally:
+            self._no_sync = prev
+
     def _make_hook(self, t):
         def hook(_p):
+            if self._no_sync:
+                return
             b = self._bucket_of[t]
+            if b in self._launched:
+                raise RuntimeError(
+                    "multi_node_optimizer: a second backward before step() would all-reduce a "
+                    "bucket twice; run accumulation micro-batches under no_sync()")
             self._pending[b] -= 1
-            if self._pending[b] == 0 and b not in self._launched:
+            if self._pending[b] == 0:
                 lo, hi = self.buckets[b]
                 if all(q.grad is not None for q in self.params[lo:hi]):
                     ev = torch.cuda.Event()
@@ -106,7 +139,7 @@ class MultiNodeOptimizer:
         ts = [p.grad if p.grad is not None else p for p in self.params]
         key = tuple(t.data_ptr() for t in ts)
         if key != self._table_key:
-            self._table, self._table_key = PtrTable(ts), key
+            self._table, self._table_key = PtrTable(ts, self.comm.device), key
             # the pointed-to storage is kept alive by the parameters' .grad
             # (the key matched it); holding the tensors here would pin old
             # gradients across zero_grad(set_to_none)
