@@ -65,7 +65,11 @@ def parse():
                     help="keep warming up (untimed) at least this long so the clock sampler sees load")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-budget-s", type=float, default=12.0)
+    ap.add_argument("--cpu-budget-s", type=float, default=10.0,
+                    help="cpu_baseline: time full-workload oracle steps for about this long (>= 3 steps)")
+    ap.add_argument("--tune-budget-s", type=float, default=30.0,
+                    help="N > 1 schedule autotune: stop trying candidates after this long "
+                         "(candidates in a fixed order, the default schedule first)")
     return ap.parse_args()
 
 
@@ -172,41 +176,51 @@ def workload():
     return shapes, [synth.numel(s) for s in shapes]
 
 
-def workload_name(P: int, dtype: str) -> str:
+def workload_name(P: int, dtype: str, world: int) -> str:
     """config.workload, identical for both arms."""
-    return (f"ResNet-50 gradient set (161 tensors, {P:,} fp32 params), {dtype} payload, "
-            f"pack+allreduce+momentum-SGD step (BASELINE config {'2' if dtype == 'fp32' else '3'})")
+    head = f"ResNet-50 gradient set (161 tensors, {P:,} fp32 params), {dtype} payload, "
+    cfg = "BASELINE config 2" if dtype == "fp32" else "BASELINE config 3's fp16 payload"
+    if world == 1:
+        return (head + "data-parallel update step at N=1: the all-reduce is the identity, so the "
+                f"step is the fused average + momentum-SGD update straight from the gradients, no pack ({cfg})")
+    return (head + f"pack(+cast) -> all-reduce over {world} GPUs -> average + momentum-SGD step ({cfg})")
+
+
+def common_config(P: int, T: int, L: int, dtype: str, world: int) -> dict:
+    """The `config` object, identical in both arms (the driver compares them);
+    everything arm-specific goes under the line's `details`."""
+    return {"workload": workload_name(P, dtype, world), "n_tensors": T, "n_params": P, "padded_len": L,
+            "comm_dtype": dtype, "lr": 0.1, "mu": 0.9, "parallelism": f"dp{world}",
+            "l2": "inputs larger than L2: 20 B/param = 511 MB streamed per step vs 126 MB L2 "
+                  "(no flush between steps)"}
 
 
 # ------------------------------------------------------ CPU oracle baseline
 
-def _oracle_sample(n_workers: int):
+def _oracle_inputs(n_workers: int):
+    """The full workload on the host: n_workers' ResNet-50 gradients, the
+    parameters, zero momentum (seeded synth/, like the GPU arm)."""
     import numpy as np
 
     import synth
     shapes, sizes = workload()
-    # sample: a prefix of the layer list holding ~2M params (every tensor kind)
-    take, acc = 0, 0
-    while take < len(shapes) and acc < 2_000_000:
-        acc += sizes[take]
-        take += 1
-    sub = shapes[:take]
-    g = synth.grads(sub, workers=n_workers)
-    w = synth.params(sub)
+    g = synth.grads(shapes, workers=n_workers)
+    w = synth.params(shapes)
     v = [np.zeros_like(x) for x in w]
-    return take, acc, sum(sizes), g, w, v
+    return sum(sizes), g, w, v
 
 
 def oracle_step_time(n_workers: int, dtype: str, budget_s: float = 0.0, steps: int = 0,
                      warmup: int = 0, threads: int = 1):
-    """Time the CPU oracle (single-threaded, as it stands) on a bounded
-    sample of the ResNet-50 workload: either for ~budget_s seconds, or for
-    `warmup` untimed + `steps` timed sample steps.  Returns (us per
-    full-workload step, sample description).  threads > 1 times the same
-    oracle under SURVEY §8(d) d.5 (ii)'s elementwise partition across host
-    threads (oracle.step_threaded, bit-identical output)."""
+    """Time the CPU oracle as it stands (oracle/cmn_oracle.c orc_step:
+    pack + tree reduce + average + momentum SGD) on the FULL workload:
+    `warmup` untimed + `steps` timed steps, or (steps = 0) steps for about
+    budget_s seconds, at least 3.  threads > 1 runs the same oracle under
+    SURVEY §8(d) d.5 (ii)'s elementwise partition across host threads
+    (oracle.step_threaded, bit-identical output).  Returns (mean us per
+    step, total timed seconds, timed steps, sample description)."""
     import oracle
-    take, acc, P, g, w, v = _oracle_sample(n_workers)
+    P, g, w, v = _oracle_inputs(n_workers)
     if threads > 1:
         def one():
             oracle.step_threaded(g, w, v, 0.1, 0.9, dtype, threads=threads)
@@ -215,19 +229,17 @@ def oracle_step_time(n_workers: int, dtype: str, budget_s: float = 0.0, steps: i
             oracle.step(g, w, v, 0.1, 0.9, dtype)
     for _ in range(warmup):
         one()
-    times = []
-    t_end = time.time() + budget_s
-    while (steps and len(times) < steps) or (not steps and (time.time() < t_end or len(times) < 2)):
-        t0 = time.perf_counter()
+    n = 0
+    t0 = time.perf_counter()
+    while (steps and n < steps) or (not steps and (time.perf_counter() - t0 < budget_s or n < 3)):
         one()
-        times.append(time.perf_counter() - t0)
-    per_param = statistics.median(times) / acc
+        n += 1
+    total = time.perf_counter() - t0
     how = "1 thread" if threads <= 1 else f"{threads} threads, elementwise partition"
-    desc = (f"oracle/cmn_oracle.c orc_step (pack+tree-reduce+momentum-SGD, {how}) on the first "
-            f"{take} of 161 ResNet-50 tensors ({acc:,} params), {n_workers} simulated worker(s), "
-            f"{dtype}, median of {len(times)} timed sample steps, scaled x{P / acc:.2f} to the "
-            f"full {P:,}-param set")
-    return per_param * P * 1e6, desc
+    desc = (f"oracle/cmn_oracle.c orc_step (pack+tree-reduce+average+momentum-SGD, {how}) on the full "
+            f"workload: all 161 ResNet-50 tensors ({P:,} params), {n_workers} simulated worker(s), {dtype}, "
+            f"mean of {n} timed full steps after {warmup} untimed")
+    return total / n * 1e6, total, n, desc
 
 
 def _cpu_model() -> str:
@@ -246,14 +258,16 @@ def run_reference(args):
     if rank != 0:
         return 0
     n = max(1, args.gpus)
-    us, desc = oracle_step_time(n, args.dtype, steps=args.steps, warmup=args.warmup)
+    us, total_s, k, desc = oracle_step_time(n, args.dtype, steps=args.steps, warmup=args.warmup)
     shapes, sizes = workload()
-    cfg = {"workload": workload_name(sum(sizes), args.dtype), "comm_dtype": args.dtype,
-           "parallelism": f"dp{n}", "workers": f"{n} worker(s) simulated on the host CPU"}
+    import oracle
+    L = oracle.layout(sizes)[1]
+    cfg = common_config(sum(sizes), len(sizes), L, args.dtype, n)
     line = {"impl": "reference", "metric": METRIC, "value": us, "unit": "us", "n_gpus": n,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": us / 1e3,
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded counter-hash, synth/)", "config": cfg,
+            "details": {"timed_region_s": total_s, "workers": f"{n} worker(s) simulated on the host CPU"},
             "cpu_baseline": {"value": us, "unit": "us", "cores": 1, "kind": "oracle", "sample": desc,
                              "cpu": _cpu_model()},
             "e2e": {"value": us, "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -278,6 +292,12 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        # NCCL (the measured comparison) reports its communicator (nranks,
+        # NVLS / ring choice); every NCCL call below runs with fd 1 routed to
+        # stderr, so those lines never reach the one-line stdout
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,ENV,TUNING")
     if args.gpus != world and world > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     # one process per GPU; on a box with fewer GPUs than ranks (tests), ranks
@@ -371,7 +391,15 @@ def main():
         # Runtime schedule choice: every rank times each candidate (max over
         # ranks, so all ranks pick the same one); switching schedules between
         # calls is safe (every buffer reuse is behind a start barrier).
-        cands = list(SCHEDULES) if args.schedule == "auto" else [args.schedule]
+        # fixed order, the library default (pipelined, 4 pieces) first: a
+        # zero budget runs the default deterministically
+        order = ["pipelined4"] + [n for n in SCHEDULES if n != "pipelined4"]
+        cands = order if args.schedule == "auto" else [args.schedule]
+        t_tune0 = time.time()
+
+        def budget_left():
+            return time.time() - t_tune0 < args.tune_budget_s
+
         def trial_us():
             for _ in range(3):
                 comm.step(g, args.dtype, 0.1, 0.9, stream)
@@ -419,14 +447,20 @@ def main():
             return float(t.item()) * 1e3
 
         trials = {}
-        for name in cands:
+        for i, name in enumerate(cands):
+            if i > 0 and not budget_left():
+                break                    # every rank decides from the same max-over-ranks clock below
             set_schedule(name)
             trials[name] = trial_us()
+            go = torch.tensor([1.0 if budget_left() else 0.0], dtype=torch.float64)
+            dist.all_reduce(go, op=dist.ReduceOp.MIN)   # all ranks stop at the same candidate
+            if go.item() == 0.0:
+                break
         # The same schedules replayed from a captured CUDA graph (no host
         # launch cost per step: the pipelined step is ~7 API calls per piece).
         for name in ("pipelined4", "pipelined8", "fused", "fused_push"):
-            if args.schedule != "auto":
-                break
+            if args.schedule != "auto" or name not in trials or not budget_left():
+                continue
             set_schedule(name)
             gr = capture_step()
             if gr is not None:
@@ -439,17 +473,48 @@ def main():
         # NVLS becomes a headline candidate only after its sums pass the
         # tolerance gate against the tree sums on this box.
         from paper_1908_00213_b200.cmn import CmnError
+        S_bus = 2 * (world - 1) / world * (4 if args.dtype == "fp32" else 2) * P
+
+        def allreduce_only_us():
+            """pack(+cast) + all-reduce alone (cmn_allreduce_grads, no
+            update), 10 calls, max over ranks: config 5's quantity at the
+            R50 size, for the hand-written kernels and NCCL alike."""
+            for _ in range(3):
+                comm.allreduce_grads(g, args.dtype, stream)
+            torch.cuda.synchronize()
+            barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(10):
+                comm.allreduce_grads(g, args.dtype, stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            t = torch.tensor([a.elapsed_time(b) / 10], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            comm.update_momentum_sgd(0.1, 0.9, stream)      # consume (state hygiene)
+            return float(t.item()) * 1e3
+
+        set_schedule("serial", "auto")
+        us_ar = allreduce_only_us()
+        comparisons["cmn"] = {"allreduce_incl_pack_us": us_ar,
+                              "allreduce_incl_pack_bus_gbs": S_bus / (us_ar * 1e-6) / 1e9}
         for alt in ("nccl", "nvls"):
-            try:
-                with stdout_to_stderr():
+            with stdout_to_stderr():        # NCCL INFO lines -> stderr
+                try:
                     comm.set_algo(alt)
-            except CmnError as e:
-                comparisons[alt] = {"unavailable": str(e)[:160]}
-                continue
-            comparisons[alt] = {}
-            for sched in ("serial", "pipelined4"):
-                set_schedule(sched, alt)
-                comparisons[alt][f"{sched}_step_us"] = trial_us()
+                except CmnError as e:
+                    comparisons[alt] = {"unavailable": str(e)[:160]}
+                    continue
+                comparisons[alt] = {}
+                set_schedule("serial", alt)
+                us_alt = allreduce_only_us()
+                comparisons[alt]["allreduce_incl_pack_us"] = us_alt
+                comparisons[alt]["allreduce_incl_pack_bus_gbs"] = S_bus / (us_alt * 1e-6) / 1e9
+                for sched in ("serial", "pipelined4"):
+                    set_schedule(sched, alt)
+                    t_alt = trial_us()
+                    comparisons[alt][f"{sched}_step_us"] = t_alt
+                    comparisons[alt][f"{sched}_step_bus_gbs"] = S_bus / (t_alt * 1e-6) / 1e9
             if alt == "nvls" and args.schedule == "auto":
                 ratio = nvls_check()
                 comparisons[alt]["tolerance_ratio_vs_tree"] = ratio
@@ -631,7 +696,8 @@ def main():
                                                          "schedule" if schedule.startswith("pipelined")
                                                          else "; copies around the step")}
 
-    comm.finalize()
+    with stdout_to_stderr():              # ncclCommDestroy may log
+        comm.finalize()
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -668,6 +734,10 @@ def main():
         # for every 2 it writes
         roof["nominal_peak"] = 7700.0
         roof["frac_of_nominal"] = roof["achieved"] / 7700.0
+        # The conservative figure: per-step median with events between steps
+        # (no overlap of one step's drain with the next one's launch)
+        roof["achieved_per_step_median"] = alg_bytes / (per_step["median_us"] * 1e-6) / 1e9
+        roof["frac_per_step_median"] = roof["achieved_per_step_median"] / peak
         bus = None
     else:
         S = csz * P
@@ -678,51 +748,59 @@ def main():
                   else "k_twoshot (reduce-scatter) + k_update_gather" if schedule.startswith("fused")
                   else "k_nvls (multimem.ld_reduce / multimem.st)" if schedule.startswith("nvls")
                   else "k_oneshot / k_twoshot all-reduce")
-        roof = {"bound": "nvlink", "kernel": kernel,
-                "achieved": bus_bytes / (kernel_ms_per_step * 1e-3) / 1e9,
-                "peak": 770.0, "unit": "GB/s",
-                "peak_source": "measured peer copy 770 GB/s/direction (B200_PROFILING.md); 900 nominal",
-                "algorithmic_bytes_per_launch": bus_bytes / max(kernel_launches_per_step, 1e-9),
-                "kernel_us_per_step": kernel_ms_per_step * 1e3,
-                "launches_per_step": kernel_launches_per_step, "timing": timing_note,
-                "step_achieved": bus, "traffic": None}
-        roof["frac"] = roof["achieved"] / 770.0
+        # The north-star quantity is the whole STEP against the bus roofline
+        # (<= 248.5 us at N = 8 = 80 % of 900 GB/s): achieved =
+        # bus bytes 2(N-1)/N S / ms_per_step, so exposed pack / update time
+        # counts against it.  The collective kernels' own device time is
+        # reported beside it (kernel_only).
+        k_ach = bus_bytes / (kernel_ms_per_step * 1e-3) / 1e9
+        roof = {"bound": "nvlink", "kernel": f"whole step, schedule {schedule}",
+                "achieved": bus, "peak": 770.0, "unit": "GB/s",
+                "peak_source": "measured peer copy 770 GB/s/direction (B200_PROFILING.md); "
+                               "900 nominal in frac_of_nominal",
+                "algorithmic_bytes_per_step": bus_bytes,
+                "frac": bus / 770.0, "nominal_peak": 900.0, "frac_of_nominal": bus / 900.0,
+                "timing": f"CUDA events around the timed region of {args.steps} steps, max over ranks",
+                "kernel_only": {"kernel": kernel, "achieved": k_ach, "frac": k_ach / 770.0,
+                                "us_per_step": kernel_ms_per_step * 1e3,
+                                "launches_per_step": kernel_launches_per_step,
+                                "algorithmic_bytes_per_launch":
+                                    bus_bytes / max(kernel_launches_per_step, 1e-9),
+                                "timing": timing_note},
+                "traffic": None}
         if schedule.startswith("nvls"):
             # bus bytes follow the all-reduce convention (2(N-1)/N S); the
             # bytes the in-switch reduction actually moves per rank and
             # direction are (N+1)/N S, reported beside it
             link = (world + 1) / world * S
             roof["nvls_link_bytes_per_rank_direction"] = link
-            roof["nvls_link_frac"] = link / (kernel_ms_per_step * 1e-3) / 1e9 / 770.0
+            roof["nvls_link_frac_of_step"] = link / (ms * 1e-3) / 1e9 / 770.0
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:      # the contract: rank 0 at N = 1 only
-        cus, desc = oracle_step_time(world, args.dtype, budget_s=args.cpu_budget_s)
+        cus, _, _, desc = oracle_step_time(world, args.dtype, budget_s=args.cpu_budget_s, warmup=1)
         cpu = {"value": cus, "unit": "us", "cores": 1, "kind": "oracle", "sample": desc,
                "cpu": _cpu_model()}
         nth = os.cpu_count() or 1
         if nth > 1:  # same oracle, elements partitioned over all cores
-            tus, tdesc = oracle_step_time(world, args.dtype, budget_s=args.cpu_budget_s / 2,
-                                          threads=nth)
+            tus, _, _, tdesc = oracle_step_time(world, args.dtype, budget_s=args.cpu_budget_s / 2,
+                                                warmup=1, threads=nth)
             cpu["threaded"] = {"value": tus, "unit": "us", "cores": nth, "sample": tdesc}
 
-    cfg = {"workload": workload_name(P, args.dtype),
-           "n_tensors": T, "n_params": P, "padded_len": L, "comm_dtype": args.dtype,
-           "algo": args.algo if world > 1 else "identity (N=1 fused direct update)",
-           "schedule": schedule, "schedule_trials_us": trials,
-           "comparisons": comparisons or None,
-           "lr": 0.1, "mu": 0.9,
-           "l2": "inputs larger than L2: 20 B/param = 511 MB streamed per step vs 126 MB L2, "
-                 "K steps back to back",
-           "step_us_after_l2_write_flush": cold_us,
-           "per_step_us": per_step,
-           "replicas_bitwise_equal": replicas_equal,
-           "warmup_steps_run": n_w,
-           "parallelism": f"dp{world}"}
+    cfg = common_config(P, T, L, args.dtype, world)
+    details = {"algo": args.algo if world > 1 else "identity (N=1 fused direct update)",
+               "schedule": schedule, "schedule_trials_us": trials,
+               "tune_budget_s": args.tune_budget_s if world > 1 else None,
+               "comparisons": comparisons or None,
+               "step_us_after_l2_write_flush": cold_us,
+               "per_step_us": per_step,
+               "replicas_bitwise_equal": replicas_equal,
+               "warmup_steps_run": n_w}
     line = {"metric": METRIC, "value": us, "unit": "us", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded counter-hash, synth/)",
-            "config": cfg, "bus_gbs": bus, "hbm_gbs": roof["achieved"] if world == 1 else None,
+            "config": cfg, "details": details, "bus_gbs": bus,
+            "hbm_gbs": roof["achieved"] if world == 1 else None,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks}
     print(json.dumps(line))

@@ -17,7 +17,7 @@
  *   a1  pack      b_r[off_t + k] = cast(g_t[k])      (cast: fp32 identity or fp16 RNE)
  *   a2  allreduce r[j] = tree_{i<N}(b_i[j])          (pairwise tree in rank order, fp32
  *                                                      accumulation, fp16 rounded once)
- *   a3  update    a = r * fl(1/N); v = fma(mu, v, a); w = fma(-lr, v, w)   (in place)
+ *   a3  update    a = r / N; v = fma(mu, v, a); w = fma(-lr, v, w)   (in place)
  * Layout: off_0 = 0, off_{t+1} = align64(off_t + n_t); pads are zero.
  * Results are bitwise identical on every rank and bitwise equal to the CPU
  * oracle (oracle/cmn_oracle.c) for the hand-written algorithms.
@@ -202,7 +202,8 @@ cmn_status cmn_allreduce_grads(cmn_comm *comm, const float *const *grads,
                                cmn_dtype dtype, void *stream);
 
 /* cmn_update_momentum_sgd -- step a3 on every registered tensor, in place:
- *   a = r[off_t+k] * fl(1/N);  v = fmaf(mu, v, a);  w = fmaf(-lr, v, w).
+ *   a = r[off_t+k] / N (one IEEE division, "dividing the sum by the number of
+ *   replicas");  v = fmaf(mu, v, a);  w = fmaf(-lr, v, w).
  * Consumes the reduced buffer of the last allreduce; calling it twice, or
  * before any allreduce, returns CMN_ERR_STATE. */
 cmn_status cmn_update_momentum_sgd(cmn_comm *comm, float lr, float mu, void *stream);
@@ -259,7 +260,7 @@ cmn_status cmn_step_host(cmn_comm *comm, const float *const *host_grads,
 cmn_status cmn_step_host_packed(cmn_comm *comm, const float *host_grads, float *host_params,
                                 cmn_dtype dtype, float lr, float mu, void *stream);
 
-/* cmn_unpack_avg_grads -- writes the averaged gradient a = r * fl(1/N)
+/* cmn_unpack_avg_grads -- writes the averaged gradient a = r / N
  * back into `out` (n_tensors device fp32 pointers; may alias the grads),
  * which is Chainer's own semantics of "updates its own replica ... with the
  * gradient obtained through the all-reduce".  Does not

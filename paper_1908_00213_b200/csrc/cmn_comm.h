@@ -143,6 +143,11 @@ struct cmn_comm {
     // pipelined N > 1 step: pack(p+1) and update(p-1) on the caller's stream
     // overlap all-reduce(p) on a high-priority communication stream.
     int pipe_pieces = 4;
+    // fault injection, tests only: CMN_TEST_ONESHOT_DELAY_US stalls this
+    // rank's one-shot CTAs after their start barrier; CMN_TEST_NO_END_BARRIER=1
+    // drops the pipelined step's one-shot end barrier (negative control)
+    uint32_t test_delay_ns = 0;
+    bool test_no_end_barrier = false;
     int fused_update = 0;         // N > 1 cmn_step: RS + fused all-gather/update (1 pull, 2 push)
     Nvls nvls;                    // NEXT-3 multicast resources (CMN_ALGO_NVLS)
     // NEXT-4 sharded update: items clipped to every rank's two-shot chunk

@@ -276,6 +276,7 @@ Barrier make_barrier(cmn_comm *c, int dtype, BarrierKind kind, int64_t e0, int64
     b.timeout_ns = static_cast<uint64_t>(c->timeout_ms) * 1000000ull;
     b.err = c->d_err;
     b.derr = c->d_errdev;
+    b.test_delay_ns = c->test_delay_ns;
     return b;
 }
 
@@ -342,6 +343,8 @@ cmn_status init_common(int rank, int world, int dev, bool sim, cmn_allgather_fn 
     c->nsm = prop.multiProcessorCount;
     c->oneshot_max = env_size("CMN_ONESHOT_MAX_BYTES", c->oneshot_max);
     c->pipe_pieces = static_cast<int>(env_size("CMN_PIECES", static_cast<size_t>(c->pipe_pieces)));
+    c->test_delay_ns = static_cast<uint32_t>(env_size("CMN_TEST_ONESHOT_DELAY_US", 0) * 1000u);
+    c->test_no_end_barrier = env_size("CMN_TEST_NO_END_BARRIER", 0) != 0;
     if (cudaHostAlloc(&c->h_err, sizeof(int), cudaHostAllocMapped) != cudaSuccess ||
         cudaHostGetDevicePointer(reinterpret_cast<void **>(&c->d_err), c->h_err, 0) != cudaSuccess) {
         delete c;

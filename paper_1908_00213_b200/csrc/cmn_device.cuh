@@ -78,6 +78,44 @@ __device__ __forceinline__ void st_cs_u2(void *p, const uint2 &v) {
 }
 #endif
 
+// 32-byte (256-bit, LDG/STG.E.ENL2.256 on sm_100a) streaming accesses; the
+// address must be 32-byte aligned.
+struct F8 {
+    float4 lo, hi;
+};
+__device__ __forceinline__ F8 ld_cs_f8(const float *p) {
+    F8 r;
+    asm volatile("ld.global.cs.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r.lo.x), "=f"(r.lo.y), "=f"(r.lo.z), "=f"(r.lo.w), "=f"(r.hi.x), "=f"(r.hi.y),
+                   "=f"(r.hi.z), "=f"(r.hi.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st_cs_f8(float *p, const F8 &v) {
+    asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v.lo.x),
+                 "f"(v.lo.y), "f"(v.lo.z), "f"(v.lo.w), "f"(v.hi.x), "f"(v.hi.y), "f"(v.hi.z),
+                 "f"(v.hi.w)
+                 : "memory");
+}
+
+__device__ __forceinline__ F8 ld_f8(const float *p) {
+    F8 r;
+    asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r.lo.x), "=f"(r.lo.y), "=f"(r.lo.z), "=f"(r.lo.w), "=f"(r.hi.x), "=f"(r.hi.y),
+                   "=f"(r.hi.z), "=f"(r.hi.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st_f8(float *p, const F8 &v) {
+    asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v.lo.x),
+                 "f"(v.lo.y), "f"(v.lo.z), "f"(v.lo.w), "f"(v.hi.x), "f"(v.hi.y), "f"(v.hi.z),
+                 "f"(v.hi.w)
+                 : "memory");
+}
+__device__ __forceinline__ bool aligned32(const void *p) {
+    return (reinterpret_cast<uintptr_t>(p) & 31u) == 0;
+}
+
 // 16-byte load that may target a peer GPU's memory (UVA / IPC mapping) and
 // data published by a peer during this kernel: weak load, no L1 allocation
 // (never the non-coherent .nc path).
@@ -119,6 +157,13 @@ __device__ __forceinline__ uint64_t global_timer_ns() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
+}
+
+// Fault injection for tests: stall the calling thread for `ns` nanoseconds.
+__device__ __forceinline__ void stall_ns(uint32_t ns) {
+    const uint64_t t0 = global_timer_ns();
+    while (global_timer_ns() - t0 < ns) {
+    }
 }
 
 // This call's barrier value for the calling CTA: reads and advances the

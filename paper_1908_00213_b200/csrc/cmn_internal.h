@@ -78,6 +78,8 @@ struct Barrier {
     int *err;           // host-mapped error word: 0 ok, 1 timeout, 2 mismatch
     int *derr;          // the same code in device memory, read by every later
                         // kernel of the communicator (comm_failed) to skip its stores
+    uint32_t test_delay_ns;   // fault injection (tests only, CMN_TEST_ONESHOT_DELAY_US):
+                              // one-shot CTAs stall this long after the start barrier
 };
 
 // Peer buffer table (packed or reduced) in 16-byte units.

@@ -18,6 +18,7 @@
 // 8 KB tiles for the packed-index kernels, streaming (.cs) cache hints where
 // they measured faster (profiles/r1_hints_ab.jsonl: not in the N = 1 direct
 // update, nor in the fp32 update-from-packed).
+#include <cmath>
 #include <cstdint>
 #include <cstdlib>
 #include <utility>
@@ -50,23 +51,37 @@ static_assert(kItemElems % (4 * kThreads) == 0, "item must be a whole number of 
 // a = r / N ("dividing the sum by the number of replicas", PAPER.md:453-454,
 // reading R3: one IEEE division, __fdiv_rn); v = fma(mu, v, a);
 // w = fma(-lr, v, w) (reading R6).
-__device__ __forceinline__ float average(float r, float n_rep) { return __fdiv_rn(r, n_rep); }
+// For N a power of two the division is exact-equal to the multiplication by
+// 1/N (both are the correctly rounded r / N), so those N take one FMUL and
+// the others __fdiv_rn (DIV, chosen per launch): the division measured +6 %
+// in the ALU-heavier Adam update at N = 1.
+struct Avg {
+    float n;     // N
+    float inv;   // 1/N (exact for N a power of two)
+};
+template <bool DIV>
+__device__ __forceinline__ float average(float r, const Avg &a) {
+    if constexpr (DIV) return __fdiv_rn(r, a.n);
+    else return __fmul_rn(r, a.inv);
+}
 
 __device__ __forceinline__ void sgd_core(float a, float lr, float mu, float &w, float &v) {
     v = __fmaf_rn(mu, v, a);
     w = __fmaf_rn(-lr, v, w);
 }
-__device__ __forceinline__ void sgd_elem(float r, float n_rep, float lr, float mu, float &w,
+template <bool DIV>
+__device__ __forceinline__ void sgd_elem(float r, const Avg &n_rep, float lr, float mu, float &w,
                                          float &v) {
-    sgd_core(average(r, n_rep), lr, mu, w, v);
+    sgd_core(average<DIV>(r, n_rep), lr, mu, w, v);
 }
 
-__device__ __forceinline__ void sgd_vec(const float4 &r, float n_rep, float lr, float mu,
+template <bool DIV>
+__device__ __forceinline__ void sgd_vec(const float4 &r, const Avg &n_rep, float lr, float mu,
                                         float4 &w, float4 &v) {
-    sgd_elem(r.x, n_rep, lr, mu, w.x, v.x);
-    sgd_elem(r.y, n_rep, lr, mu, w.y, v.y);
-    sgd_elem(r.z, n_rep, lr, mu, w.z, v.z);
-    sgd_elem(r.w, n_rep, lr, mu, w.w, v.w);
+    sgd_elem<DIV>(r.x, n_rep, lr, mu, w.x, v.x);
+    sgd_elem<DIV>(r.y, n_rep, lr, mu, w.y, v.y);
+    sgd_elem<DIV>(r.z, n_rep, lr, mu, w.z, v.z);
+    sgd_elem<DIV>(r.w, n_rep, lr, mu, w.w, v.w);
 }
 // N = 1: the average is the identity (r / 1 == r exactly), no division.
 __device__ __forceinline__ void sgd_vec1(const float4 &a, float lr, float mu, float4 &w, float4 &v) {
@@ -133,11 +148,72 @@ __device__ __forceinline__ void pack_store(void *packed, int64_t j, const float4
     }
 }
 
+#ifndef CMN_PACK_V8
+#define CMN_PACK_V8 1
+#endif
+// 256-bit variant (CMN_PACK_V8): each thread moves 8 consecutive elements
+// per access -- one LDG.256 of fp32 and one STG.256 (fp32 payload) or one
+// STG.128 of eight halves (fp16 payload) -- instead of 16-byte loads and
+// 16 / 8-byte stores.  Needs a 32-byte aligned gradient pointer (checked
+// per item, uniform per CTA; otherwise the 16-byte path runs).
+constexpr int kPackVec8 = kItemElems / 8 / kPackThreads;   // 8-element groups per thread per item
+
+template <int DT>
+__device__ __forceinline__ void pack_store8(void *packed, int64_t j, const F8 &x) {
+    if constexpr (DT == 0) {
+        st_cs_f8(static_cast<float *>(packed) + j, x);
+    } else {
+        const uint4 h = make_uint4(pack_half2(x.lo.x, x.lo.y), pack_half2(x.lo.z, x.lo.w),
+                                   pack_half2(x.hi.x, x.hi.y), pack_half2(x.hi.z, x.hi.w));
+        __stcs(reinterpret_cast<uint4 *>(static_cast<uint16_t *>(packed) + j), h);
+    }
+}
+
+// One item with 256-bit accesses (src 32-byte aligned, it.base multiple of 8).
+template <int DT>
+__device__ __forceinline__ void pack_item_v8(const float *__restrict__ src, const Item &it,
+                                             void *__restrict__ packed) {
+    const int n8 = it.len >> 3;
+    F8 x[kPackVec8];
+#pragma unroll
+    for (int u = 0; u < kPackVec8; ++u) {
+        const int q = threadIdx.x + u * kPackThreads;
+        if (q < n8) x[u] = ld_cs_f8(src + 8 * q);
+    }
+#pragma unroll
+    for (int u = 0; u < kPackVec8; ++u) {
+        const int q = threadIdx.x + u * kPackThreads;
+        if (q < n8) pack_store8<DT>(packed, it.base + 8 * q, x[u]);
+    }
+    for (int k = (n8 << 3) + threadIdx.x; k < it.len; k += kPackThreads) {
+        const float sv = src[k];
+        if constexpr (DT == 0)
+            static_cast<float *>(packed)[it.base + k] = sv;
+        else
+            static_cast<uint16_t *>(packed)[it.base + k] = __half_as_ushort(__float2half_rn(sv));
+    }
+}
+
 // One CTA's share of the pack: items its[0..kPackItems) starting at ib,
 // all loads issued before the first store.
 template <int DT, int CAP>
 __device__ __forceinline__ void pack_items(const GradTabN<CAP> &g, int t_lo, const Item (&its)[kPackItems],
                                            int ib, int i1, void *__restrict__ packed) {
+    if constexpr (CMN_PACK_V8 != 0 && kPackItems == 1) {
+        if (ib >= i1) return;
+        const Item it = its[0];
+        const float *__restrict__ src = g.p[it.t - t_lo] + it.k0;
+        if ((reinterpret_cast<uintptr_t>(src) & 31u) == 0) {
+            pack_item_v8<DT>(src, it, packed);
+            for (int k = threadIdx.x; k < it.pad; k += kPackThreads) {
+                if constexpr (DT == 0)
+                    static_cast<float *>(packed)[it.base + it.len + k] = 0.0f;
+                else
+                    static_cast<uint16_t *>(packed)[it.base + it.len + k] = 0;
+            }
+            return;
+        }
+    }
     float4 x[kPackItems][kPackVec];
 #pragma unroll
     for (int j = 0; j < kPackItems; ++j) {
@@ -213,9 +289,9 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const __grid_constant__ G
 // Streaming hints only for the fp16 payload: the .cs A/B
 // (profiles/r1_hints_ab.jsonl) measured plain accesses 1-4 % faster for the
 // fp32 payload and .cs ~4 % faster for fp16.
-template <int DT>
+template <int DT, bool DIV>
 __device__ __forceinline__ void update_sgd_item(const Item &it, const TensorDesc &d,
-                                                const void *__restrict__ reduced, float n_rep,
+                                                const void *__restrict__ reduced, const Avg n_rep,
                                                 float lr, float mu, const int *derr) {
     constexpr bool CS = DT == 1;
     float *__restrict__ w = d.w + it.k0;
@@ -239,24 +315,24 @@ __device__ __forceinline__ void update_sgd_item(const Item &it, const TensorDesc
     for (int u = 0; u < kVecPerThread; ++u) {
         const int v = threadIdx.x + u * kThreads;
         if (v < nv) {
-            sgd_vec(r[u], n_rep, lr, mu, wv[u], mv[u]);
+            sgd_vec<DIV>(r[u], n_rep, lr, mu, wv[u], mv[u]);
             st_f4<CS>(w + 4 * v, wv[u]);
             st_f4<CS>(m + 4 * v, mv[u]);
         }
     }
     for (int k = (nv << 2) + threadIdx.x; k < it.len; k += kThreads) {
         float wk = w[k], mk = m[k];
-        sgd_elem(load_r1<DT>(reduced, base + k), n_rep, lr, mu, wk, mk);
+        sgd_elem<DIV>(load_r1<DT>(reduced, base + k), n_rep, lr, mu, wk, mk);
         w[k] = wk;
         m[k] = mk;
     }
 }
 
-template <int DT, bool STRIDE>
+template <int DT, bool STRIDE, bool DIV>
 __global__ void __launch_bounds__(kThreads) k_update_sgd(const TensorDesc *__restrict__ td,
                                                          const Item *__restrict__ items, int i0,
                                                          int i1, const void *__restrict__ reduced,
-                                                         float n_rep, float lr, float mu,
+                                                         const Avg n_rep, float lr, float mu,
                                                          const int *derr) {
     // PDL (see launch_pdl): descriptors are static, read before the wait.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -265,10 +341,10 @@ __global__ void __launch_bounds__(kThreads) k_update_sgd(const TensorDesc *__res
     TensorDesc d = td[it.t];
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if constexpr (!STRIDE) {
-        update_sgd_item<DT>(it, d, reduced, n_rep, lr, mu, derr);
+        update_sgd_item<DT, DIV>(it, d, reduced, n_rep, lr, mu, derr);
     } else {
         for (;;) {
-            update_sgd_item<DT>(it, d, reduced, n_rep, lr, mu, derr);
+            update_sgd_item<DT, DIV>(it, d, reduced, n_rep, lr, mu, derr);
             ib += gridDim.x;
             if (ib >= i1) break;
             it = items[ib];
@@ -287,6 +363,55 @@ __global__ void __launch_bounds__(kThreads) k_update_sgd(const TensorDesc *__res
 // hints measured 1.6 % slower here (bench 79.3 vs 78.0 us; probe
 // scripts/update_variants.cu B vs A), so this kernel -- the whole N = 1
 // step -- uses plain LDG/STG.128.
+#ifndef CMN_DIRECT_V8
+#define CMN_DIRECT_V8 0
+#endif
+// 256-bit variant of the N = 1 step body (CMN_DIRECT_V8, measurement switch):
+// per thread 2 x 8 elements of g, w, v with LDG/STG.256.  g and w must be
+// 32-byte aligned (checked per item; the momentum is, at mom + base).
+[[maybe_unused]] constexpr int kVec8PerThread = kItemElems / 8 / kThreads;
+
+template <int DT>
+__device__ __forceinline__ void direct_item_v8(const float *__restrict__ gp, float *__restrict__ w,
+                                               float *__restrict__ m, int len, float lr, float mu) {
+    const int n8 = len >> 3;
+    F8 r[kVec8PerThread], wv[kVec8PerThread], mv[kVec8PerThread];
+#pragma unroll
+    for (int u = 0; u < kVec8PerThread; ++u) {
+        const int q = threadIdx.x + u * kThreads;
+        if (q < n8) {
+            r[u] = ld_f8(gp + 8 * q);
+            wv[u] = ld_f8(w + 8 * q);
+            mv[u] = ld_f8(m + 8 * q);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < kVec8PerThread; ++u) {
+        const int q = threadIdx.x + u * kThreads;
+        if (q < n8) {
+            F8 a = r[u];
+            if constexpr (DT == 1) {
+                a.lo.x = round_through_half(a.lo.x); a.lo.y = round_through_half(a.lo.y);
+                a.lo.z = round_through_half(a.lo.z); a.lo.w = round_through_half(a.lo.w);
+                a.hi.x = round_through_half(a.hi.x); a.hi.y = round_through_half(a.hi.y);
+                a.hi.z = round_through_half(a.hi.z); a.hi.w = round_through_half(a.hi.w);
+            }
+            sgd_vec1(a.lo, lr, mu, wv[u].lo, mv[u].lo);
+            sgd_vec1(a.hi, lr, mu, wv[u].hi, mv[u].hi);
+            st_f8(w + 8 * q, wv[u]);
+            st_f8(m + 8 * q, mv[u]);
+        }
+    }
+    for (int k = (n8 << 3) + threadIdx.x; k < len; k += kThreads) {
+        float a = gp[k];
+        if constexpr (DT == 1) a = round_through_half(a);
+        float wk = w[k], mk = m[k];
+        sgd_core(a, lr, mu, wk, mk);
+        w[k] = wk;
+        m[k] = mk;
+    }
+}
+
 template <int DT, int CAP>
 __global__ void __launch_bounds__(kThreads) k_update_direct(const __grid_constant__ GradTabN<CAP> g,
                                                             const __grid_constant__ GradTabN<CAP> wt,
@@ -304,6 +429,12 @@ __global__ void __launch_bounds__(kThreads) k_update_direct(const __grid_constan
     float *__restrict__ m = mom + it.base;
     const int nv = it.len >> 2;
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if constexpr (CMN_DIRECT_V8 != 0) {
+        if (aligned32(gp) && aligned32(w)) {
+            direct_item_v8<DT>(gp, w, m, it.len, lr, mu);
+            return;
+        }
+    }
     auto ld = [](const float *p) { return *reinterpret_cast<const float4 *>(p); };
     auto st = [](float *p, const float4 &x) { *reinterpret_cast<float4 *>(p) = x; };
 
@@ -343,18 +474,18 @@ __global__ void __launch_bounds__(kThreads) k_update_direct(const __grid_constan
     }
 }
 
-template <int DT, int CAP>
+template <int DT, int CAP, bool DIV>
 __global__ void __launch_bounds__(kThreads) k_unpack_avg(const __grid_constant__ GradTabN<CAP> out, int t_lo,
                                                          const TensorDesc *__restrict__ td,
                                                          const Item *__restrict__ items, int i0,
                                                          const void *__restrict__ reduced,
-                                                         float n_rep, const int *derr) {
+                                                         const Avg n_rep, const int *derr) {
     if (comm_failed(derr)) return;
     const Item it = items[i0 + blockIdx.x];
     const int64_t base = td[it.t].off + it.k0;
     float *dst = const_cast<float *>(out.p[it.t - t_lo]) + it.k0;
     for (int k = threadIdx.x; k < it.len; k += kThreads)
-        dst[k] = average(load_r1<DT>(reduced, base + k), n_rep);
+        dst[k] = average<DIV>(load_r1<DT>(reduced, base + k), n_rep);
 }
 
 #ifndef CMN_ADAM_DIRECT_CS
@@ -380,15 +511,16 @@ __device__ __forceinline__ void adam_core(float a, float alpha_t, float beta1, f
     const float den = __fadd_rn(__fsqrt_rn(v), eps);
     w = __fsub_rn(w, __fmul_rn(alpha_t, __fdiv_rn(m, den)));
 }
-__device__ __forceinline__ void adam_elem(float r, float n_rep, float alpha_t, float beta1,
+template <bool DIV>
+__device__ __forceinline__ void adam_elem(float r, const Avg &n_rep, float alpha_t, float beta1,
                                           float beta2, float c1, float c2, float eps, float &w,
                                           float &m, float &v) {
-    adam_core(average(r, n_rep), alpha_t, beta1, beta2, c1, c2, eps, w, m, v);
+    adam_core(average<DIV>(r, n_rep), alpha_t, beta1, beta2, c1, c2, eps, w, m, v);
 }
 
-template <int DT>
+template <int DT, bool DIV>
 __device__ __forceinline__ void update_adam_item(const Item &it, const TensorDesc &d,
-                                                 const void *__restrict__ reduced, float n_rep,
+                                                 const void *__restrict__ reduced, const Avg n_rep,
                                                  float alpha_t, float beta1, float beta2, float c1,
                                                  float c2, float eps, const int *derr) {
     float *__restrict__ w = d.w + it.k0;
@@ -417,10 +549,10 @@ __device__ __forceinline__ void update_adam_item(const Item &it, const TensorDes
         for (int u = 0; u < U; ++u) {
             const int q = threadIdx.x + (pass * U + u) * kThreads;
             if (q < nv) {
-                adam_elem(r[u].x, n_rep, alpha_t, beta1, beta2, c1, c2, eps, wv[u].x, mv[u].x, vv[u].x);
-                adam_elem(r[u].y, n_rep, alpha_t, beta1, beta2, c1, c2, eps, wv[u].y, mv[u].y, vv[u].y);
-                adam_elem(r[u].z, n_rep, alpha_t, beta1, beta2, c1, c2, eps, wv[u].z, mv[u].z, vv[u].z);
-                adam_elem(r[u].w, n_rep, alpha_t, beta1, beta2, c1, c2, eps, wv[u].w, mv[u].w, vv[u].w);
+                adam_elem<DIV>(r[u].x, n_rep, alpha_t, beta1, beta2, c1, c2, eps, wv[u].x, mv[u].x, vv[u].x);
+                adam_elem<DIV>(r[u].y, n_rep, alpha_t, beta1, beta2, c1, c2, eps, wv[u].y, mv[u].y, vv[u].y);
+                adam_elem<DIV>(r[u].z, n_rep, alpha_t, beta1, beta2, c1, c2, eps, wv[u].z, mv[u].z, vv[u].z);
+                adam_elem<DIV>(r[u].w, n_rep, alpha_t, beta1, beta2, c1, c2, eps, wv[u].w, mv[u].w, vv[u].w);
                 st_cs_f4(w + 4 * q, wv[u]);
                 st_cs_f4(m + 4 * q, mv[u]);
                 st_cs_f4(v + 4 * q, vv[u]);
@@ -429,7 +561,7 @@ __device__ __forceinline__ void update_adam_item(const Item &it, const TensorDes
     }
     for (int k = (nv << 2) + threadIdx.x; k < it.len; k += kThreads) {
         float wk = w[k], mk = m[k], vk = v[k];
-        adam_elem(load_r1<DT>(reduced, it.base + k), n_rep, alpha_t, beta1, beta2, c1, c2, eps,
+        adam_elem<DIV>(load_r1<DT>(reduced, it.base + k), n_rep, alpha_t, beta1, beta2, c1, c2, eps,
                   wk, mk, vk);
         w[k] = wk;
         m[k] = mk;
@@ -437,11 +569,11 @@ __device__ __forceinline__ void update_adam_item(const Item &it, const TensorDes
     }
 }
 
-template <int DT, bool STRIDE>
+template <int DT, bool STRIDE, bool DIV>
 __global__ void __launch_bounds__(kThreads) k_update_adam(const TensorDesc *__restrict__ td,
                                                           const Item *__restrict__ items, int i0,
                                                           int i1, const void *__restrict__ reduced,
-                                                          float n_rep, float alpha_t, float beta1,
+                                                          const Avg n_rep, float alpha_t, float beta1,
                                                           float beta2, float c1, float c2,
                                                           float eps, const int *derr) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // PDL, see launch_pdl
@@ -450,10 +582,10 @@ __global__ void __launch_bounds__(kThreads) k_update_adam(const TensorDesc *__re
     TensorDesc d = td[it.t];
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if constexpr (!STRIDE) {
-        update_adam_item<DT>(it, d, reduced, n_rep, alpha_t, beta1, beta2, c1, c2, eps, derr);
+        update_adam_item<DT, DIV>(it, d, reduced, n_rep, alpha_t, beta1, beta2, c1, c2, eps, derr);
     } else {
         for (;;) {
-            update_adam_item<DT>(it, d, reduced, n_rep, alpha_t, beta1, beta2, c1, c2, eps, derr);
+            update_adam_item<DT, DIV>(it, d, reduced, n_rep, alpha_t, beta1, beta2, c1, c2, eps, derr);
             ib += gridDim.x;
             if (ib >= i1) break;
             it = items[ib];
@@ -581,6 +713,7 @@ __global__ void __launch_bounds__(kThreads) k_oneshot(const __grid_constant__ Pe
                                                       const __grid_constant__ Barrier bar) {
     const uint32_t bv = barrier_value(bar);
     if (!cross_rank_barrier(bar, bv, N, 0)) return;
+    if (bar.test_delay_ns) stall_ns(bar.test_delay_ns);   // tests: a slow peer
     for (int64_t tile = v0 + static_cast<int64_t>(blockIdx.x) * kTileVecs; tile < v1;
          tile += static_cast<int64_t>(gridDim.x) * kTileVecs) {
         uint4 x[kARVec][N];
@@ -675,11 +808,11 @@ __global__ void __launch_bounds__(kThreads) k_twoshot(const __grid_constant__ Pe
 // reading the reduce-scatter output (own reduced buffer, packed layout) and
 // publishing the new parameters into the fp32 exchange buffer at the same
 // packed indices.
-template <int DT>
+template <int DT, bool DIV>
 __global__ void __launch_bounds__(kThreads) k_update_chunk(const TensorDesc *__restrict__ td,
                                                            const Item *__restrict__ items, int i0,
                                                            const void *__restrict__ reduced,
-                                                           float *__restrict__ exch, float n_rep,
+                                                           float *__restrict__ exch, const Avg n_rep,
                                                            float lr, float mu, const int *derr) {
     const Item it = items[i0 + blockIdx.x];
     const TensorDesc d = td[it.t];
@@ -702,7 +835,7 @@ __global__ void __launch_bounds__(kThreads) k_update_chunk(const TensorDesc *__r
     for (int u = 0; u < kVecPerThread; ++u) {
         const int v = threadIdx.x + u * kThreads;
         if (v < nv) {
-            sgd_vec(r[u], n_rep, lr, mu, wv[u], mv[u]);
+            sgd_vec<DIV>(r[u], n_rep, lr, mu, wv[u], mv[u]);
             st_cs_f4(w + 4 * v, wv[u]);
             st_cs_f4(m + 4 * v, mv[u]);
             st_u4(x + 4 * v, make_uint4(__float_as_uint(wv[u].x), __float_as_uint(wv[u].y),
@@ -711,7 +844,7 @@ __global__ void __launch_bounds__(kThreads) k_update_chunk(const TensorDesc *__r
     }
     for (int k = (nv << 2) + threadIdx.x; k < it.len; k += kThreads) {
         float wk = w[k], mk = m[k];
-        sgd_elem(load_r1<DT>(reduced, it.base + k), n_rep, lr, mu, wk, mk);
+        sgd_elem<DIV>(load_r1<DT>(reduced, it.base + k), n_rep, lr, mu, wk, mk);
         w[k] = wk;
         m[k] = mk;
         x[k] = wk;
@@ -758,12 +891,12 @@ __global__ void __launch_bounds__(kThreads) k_gather_params(const TensorDesc *__
 // copy: saves writing and re-reading (N-1)/N of the reduced buffer in HBM).
 // Start barrier: every peer has arrived, so its reduce-scatter completed.
 // Grid-stride over the chunk-clipped items (Item.reserved = owner).
-template <int DT>
+template <int DT, bool DIV>
 __global__ void __launch_bounds__(kThreads) k_update_gather(const TensorDesc *__restrict__ td,
                                                             const Item *__restrict__ items, int i0,
                                                             int i1,
                                                             const __grid_constant__ PeerBufs red,
-                                                            int world, float n_rep, float lr,
+                                                            int world, const Avg n_rep, float lr,
                                                             float mu,
                                                             const __grid_constant__ Barrier bar) {
     const uint32_t bv = barrier_value(bar);
@@ -796,14 +929,14 @@ __global__ void __launch_bounds__(kThreads) k_update_gather(const TensorDesc *__
         for (int u = 0; u < kVecPerThread; ++u) {
             const int v = threadIdx.x + u * kThreads;
             if (v < nv) {
-                sgd_vec(r[u], n_rep, lr, mu, wv[u], mv[u]);
+                sgd_vec<DIV>(r[u], n_rep, lr, mu, wv[u], mv[u]);
                 st_cs_f4(w + 4 * v, wv[u]);
                 st_cs_f4(m + 4 * v, mv[u]);
             }
         }
         for (int k = (nv << 2) + threadIdx.x; k < it.len; k += kThreads) {
             float wk = w[k], mk = m[k];
-            sgd_elem(load_r1<DT>(src, it.base + k), n_rep, lr, mu, wk, mk);
+            sgd_elem<DIV>(load_r1<DT>(src, it.base + k), n_rep, lr, mu, wk, mk);
             w[k] = wk;
             m[k] = mk;
         }
@@ -932,6 +1065,13 @@ __global__ void __launch_bounds__(kThreads) k_nvls(const char *mc_packed, char *
 
 inline int grid_of(int i0, int i1) { return i1 > i0 ? i1 - i0 : 0; }
 
+// The average's constants: DIV (an IEEE division) unless N is a power of two.
+inline Avg make_avg(float n) { return Avg{n, 1.0f / n}; }
+inline bool needs_div(float n) {
+    int e = 0;
+    return std::frexp(n, &e) != 0.5f;   // n = 0.5 * 2^e exactly <=> power of two
+}
+
 }  // namespace
 
 bool pdl_enabled() {
@@ -1010,13 +1150,23 @@ cudaError_t launch_update_sgd(const TensorDesc *td, const Item *items, int i0, i
     if (n == 0) return cudaSuccess;
     const int grid = capped(n, max_ctas);
     (void)cudaGetLastError();  // report this launch's error, not a stale one
+    const Avg a = make_avg(n_rep);
     cudaError_t e;
-    if (grid < n)
-        e = dtype == 0 ? launch_pdl(k_update_sgd<0, true>, grid, kThreads, s, td, items, i0, i1, reduced, n_rep, lr, mu, derr)
-                       : launch_pdl(k_update_sgd<1, true>, grid, kThreads, s, td, items, i0, i1, reduced, n_rep, lr, mu, derr);
-    else
-        e = dtype == 0 ? launch_pdl(k_update_sgd<0, false>, grid, kThreads, s, td, items, i0, i1, reduced, n_rep, lr, mu, derr)
-                       : launch_pdl(k_update_sgd<1, false>, grid, kThreads, s, td, items, i0, i1, reduced, n_rep, lr, mu, derr);
+    if (needs_div(n_rep)) {
+        if (grid < n)
+            e = dtype == 0 ? launch_pdl(k_update_sgd<0, true, true>, grid, kThreads, s, td, items, i0, i1, reduced, a, lr, mu, derr)
+                           : launch_pdl(k_update_sgd<1, true, true>, grid, kThreads, s, td, items, i0, i1, reduced, a, lr, mu, derr);
+        else
+            e = dtype == 0 ? launch_pdl(k_update_sgd<0, false, true>, grid, kThreads, s, td, items, i0, i1, reduced, a, lr, mu, derr)
+                           : launch_pdl(k_update_sgd<1, false, true>, grid, kThreads, s, td, items, i0, i1, reduced, a, lr, mu, derr);
+    } else {
+        if (grid < n)
+            e = dtype == 0 ? launch_pdl(k_update_sgd<0, true, false>, grid, kThreads, s, td, items, i0, i1, reduced, a, lr, mu, derr)
+                           : launch_pdl(k_update_sgd<1, true, false>, grid, kThreads, s, td, items, i0, i1, reduced, a, lr, mu, derr);
+        else
+            e = dtype == 0 ? launch_pdl(k_update_sgd<0, false, false>, grid, kThreads, s, td, items, i0, i1, reduced, a, lr, mu, derr)
+                           : launch_pdl(k_update_sgd<1, false, false>, grid, kThreads, s, td, items, i0, i1, reduced, a, lr, mu, derr);
+    }
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
@@ -1054,10 +1204,14 @@ cudaError_t launch_unpack_avg(const GradTab &out, int t_lo, const TensorDesc *td
     if (grid == 0) return cudaSuccess;
     (void)cudaGetLastError();  // report this launch's error, not a stale one
     const auto t = shrink<kGradCap>(out);
+    const Avg a = make_avg(n_rep);
+    const bool div = needs_div(n_rep);
     if (dtype == 0)
-        k_unpack_avg<0, kGradCap><<<grid, kThreads, 0, s>>>(t, t_lo, td, items, i0, reduced, n_rep, derr);
+        (div ? k_unpack_avg<0, kGradCap, true> : k_unpack_avg<0, kGradCap, false>)<<<grid, kThreads, 0, s>>>(
+            t, t_lo, td, items, i0, reduced, a, derr);
     else
-        k_unpack_avg<1, kGradCap><<<grid, kThreads, 0, s>>>(t, t_lo, td, items, i0, reduced, n_rep, derr);
+        (div ? k_unpack_avg<1, kGradCap, true> : k_unpack_avg<1, kGradCap, false>)<<<grid, kThreads, 0, s>>>(
+            t, t_lo, td, items, i0, reduced, a, derr);
     return cudaGetLastError();
 }
 
@@ -1070,16 +1224,18 @@ cudaError_t launch_update_adam(const TensorDesc *td, const Item *items, int i0, 
     const int grid = capped(n, max_ctas);
     (void)cudaGetLastError();  // report this launch's error, not a stale one
     cudaError_t e;
+    const Avg a = make_avg(n_rep);
+    const bool div = needs_div(n_rep);
+    auto go = [&](auto kernel) {
+        return launch_pdl(kernel, grid, kThreads, s, td, items, i0, i1, reduced, a, alpha_t, beta1, beta2,
+                          c1, c2, eps, derr);
+    };
     if (grid < n)
-        e = dtype == 0 ? launch_pdl(k_update_adam<0, true>, grid, kThreads, s, td, items, i0, i1, reduced,
-                                    n_rep, alpha_t, beta1, beta2, c1, c2, eps, derr)
-                       : launch_pdl(k_update_adam<1, true>, grid, kThreads, s, td, items, i0, i1, reduced,
-                                    n_rep, alpha_t, beta1, beta2, c1, c2, eps, derr);
+        e = dtype == 0 ? (div ? go(k_update_adam<0, true, true>) : go(k_update_adam<0, true, false>))
+                       : (div ? go(k_update_adam<1, true, true>) : go(k_update_adam<1, true, false>));
     else
-        e = dtype == 0 ? launch_pdl(k_update_adam<0, false>, grid, kThreads, s, td, items, i0, i1, reduced,
-                                    n_rep, alpha_t, beta1, beta2, c1, c2, eps, derr)
-                       : launch_pdl(k_update_adam<1, false>, grid, kThreads, s, td, items, i0, i1, reduced,
-                                    n_rep, alpha_t, beta1, beta2, c1, c2, eps, derr);
+        e = dtype == 0 ? (div ? go(k_update_adam<0, false, true>) : go(k_update_adam<0, false, false>))
+                       : (div ? go(k_update_adam<1, false, true>) : go(k_update_adam<1, false, false>));
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
@@ -1194,10 +1350,14 @@ cudaError_t launch_update_chunk(const TensorDesc *td, const Item *items, int i0,
     const int grid = grid_of(i0, i1);
     if (grid == 0) return cudaSuccess;
     (void)cudaGetLastError();
+    const Avg a = make_avg(n_rep);
+    const bool div = needs_div(n_rep);
     if (dtype == 0)
-        k_update_chunk<0><<<grid, kThreads, 0, s>>>(td, items, i0, reduced, exch, n_rep, lr, mu, derr);
+        (div ? k_update_chunk<0, true> : k_update_chunk<0, false>)<<<grid, kThreads, 0, s>>>(
+            td, items, i0, reduced, exch, a, lr, mu, derr);
     else
-        k_update_chunk<1><<<grid, kThreads, 0, s>>>(td, items, i0, reduced, exch, n_rep, lr, mu, derr);
+        (div ? k_update_chunk<1, true> : k_update_chunk<1, false>)<<<grid, kThreads, 0, s>>>(
+            td, items, i0, reduced, exch, a, lr, mu, derr);
     return cudaGetLastError();
 }
 
@@ -1215,12 +1375,14 @@ cudaError_t launch_update_gather(const TensorDesc *td, const Item *items, int i0
                                  float mu, const Barrier &bar, int blocks, cudaStream_t s) {
     if (blocks <= 0 || blocks > kMaxBarrierBlocks) return cudaErrorInvalidValue;
     (void)cudaGetLastError();
+    const Avg a = make_avg(n_rep);
+    const bool div = needs_div(n_rep);
     if (dtype == 0)
-        k_update_gather<0><<<blocks, kThreads, 0, s>>>(td, items, i0, i1, red, world, n_rep, lr, mu,
-                                                       bar);
+        (div ? k_update_gather<0, true> : k_update_gather<0, false>)<<<blocks, kThreads, 0, s>>>(
+            td, items, i0, i1, red, world, a, lr, mu, bar);
     else
-        k_update_gather<1><<<blocks, kThreads, 0, s>>>(td, items, i0, i1, red, world, n_rep, lr, mu,
-                                                       bar);
+        (div ? k_update_gather<1, true> : k_update_gather<1, false>)<<<blocks, kThreads, 0, s>>>(
+            td, items, i0, i1, red, world, a, lr, mu, bar);
     return cudaGetLastError();
 }
 

@@ -395,7 +395,7 @@ cmn_status step_pipelined(cmn_comm *c, const float *const *grads, int dtype, flo
         CMN_CUDA(cudaEventRecord(c->pev[2 * p], s));
         CMN_CUDA(cudaStreamWaitEvent(c->sc, c->pev[2 * p], 0));
         if (cmn_status st = reduce_phase(c, pieces[p].first, pieces[p].second, dtype, seq, algo[p],
-                                         c->sc, p + 1 == P);
+                                         c->sc, p + 1 == P && !c->test_no_end_barrier);
             st != CMN_OK)
             return st;
         CMN_CUDA(cudaEventRecord(c->pev[2 * p + 1], c->sc));

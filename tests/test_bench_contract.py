@@ -34,8 +34,11 @@ def test_reference_arm_one_json_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] == 1
     import bench
     assert d["metric"] == bench.METRIC
-    P = 25557032
-    assert d["config"]["workload"] == bench.workload_name(P, "fp32")
+    P, T, L = 25557032, 161, 25557056
+    # the config object is identical to the GPU arm's (bench.common_config)
+    assert d["config"] == bench.common_config(P, T, L, "fp32", 1)
+    assert "full workload" in d["cpu_baseline"]["sample"]       # no extrapolated sample
+    assert d["details"]["timed_region_s"] > 0
     blj = json.load(open(os.path.join(ROOT, "BASELINE.json")))
     assert d["metric"] == blj["metric"]
 

@@ -68,5 +68,55 @@ def test_bench_n2_torchrun_contract():
     lines = [x for x in p.stdout.splitlines() if x.strip()]
     assert len(lines) == 1, p.stdout
     d = _check(lines[0], 2)
-    assert d["config"]["replicas_bitwise_equal"] is True
+    _check_n_gt_1(d, 2)
+
+
+def _check_n_gt_1(d, n):
+    import bench
+    assert d["details"]["replicas_bitwise_equal"] is True
     assert d["cpu_baseline"] is None           # rank 0 at N = 1 only
+    assert d["config"] == bench.common_config(25557032, 161, 25557056, "fp32", n)
+    r = d["roofline"]
+    # the north-star quantity: the whole step's bus bytes over ms_per_step
+    bus_bytes = 2 * (n - 1) / n * 4 * 25557032
+    assert abs(r["achieved"] - bus_bytes / (d["ms_per_step"] * 1e-3) / 1e9) <= 1e-6 * r["achieved"]
+    assert abs(r["frac"] - r["achieved"] / 770.0) < 1e-9
+    assert abs(r["frac_of_nominal"] - r["achieved"] / 900.0) < 1e-9
+    k = r["kernel_only"]
+    assert k["achieved"] >= r["achieved"] * 0.999 and k["frac"] > 0   # kernels are a part of the step
+    c = d["details"]["comparisons"]
+    assert c["cmn"]["allreduce_incl_pack_us"] > 0 and c["cmn"]["allreduce_incl_pack_bus_gbs"] > 0
+    for alt in ("nccl", "nvls"):          # measured, or why not (one GPU: NCCL refuses 2 ranks)
+        assert "unavailable" in c[alt] or c[alt]["allreduce_incl_pack_us"] > 0
+    assert d["details"]["schedule_trials_us"]
+    assert d["details"]["tune_budget_s"] is not None
+
+
+def test_bench_n8_timesliced_contract():
+    """8 ranks time-sliced on the one test GPU (what a SCALE run at N = 8
+    executes, minus the NVLink): the line carries the same N > 1 fields; a
+    2 s autotune budget keeps it bounded."""
+    p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "8", "--master-addr", "127.0.0.1", "--master-port",
+                        str(_free_port()), "bench.py", "--gpus", "8", "--steps", "4", "--warmup", "3",
+                        "--min-warmup-s", "0", "--tune-budget-s", "2", "--no-e2e"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=1800)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [x for x in p.stdout.splitlines() if x.strip()]
+    assert len(lines) == 1, p.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 8 and d["e2e"] is None
+    _check_n_gt_1(d, 8)
+
+
+def test_reference_arm_same_config_as_gpu_arm():
+    """The driver compares the two arms' config objects: identical."""
+    outs = []
+    for impl in ("cmn", "reference"):
+        p = subprocess.run([sys.executable, "bench.py", "--impl", impl, "--steps", "4", "--warmup", "3",
+                            "--min-warmup-s", "0", "--no-cpu-baseline", "--no-e2e"],
+                           cwd=ROOT, capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        outs.append(json.loads(p.stdout.strip().splitlines()[-1]))
+    assert outs[0]["config"] == outs[1]["config"]
+    assert outs[1]["steps"] == 4 and outs[1]["details"]["timed_region_s"] > 0

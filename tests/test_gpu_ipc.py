@@ -32,6 +32,10 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode, pieces=0):
     from paper_1908_00213_b200 import cmn
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    if mode.startswith("slow_peer") and rank == 1:
+        # fault injection: this rank's one-shot CTAs stall 20 ms after their
+        # start barrier, so rank 0 races ahead into its next step
+        os.environ["CMN_TEST_ONESHOT_DELAY_US"] = "20000"
     try:
         torch.cuda.set_device(0)
         dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -61,7 +65,7 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode, pieces=0):
             comm.finalize()
             return
         comm.set_algo(algo)
-        comm.set_pipeline(pieces)
+        comm.set_pipeline(pieces + (rank if mode == "piece_mismatch" else 0))
         comm.set_fused_update(2 if mode in ("push", "graph_push") else mode in ("fused", "graph_fused"))
         if mode == "capture_unpipelined":
             g0 = [torch.from_numpy(x).cuda() for x in synth.grads(shapes, workers=world)[rank]]
@@ -77,7 +81,7 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode, pieces=0):
                 q.put((rank, "error", e.status_name))
             dist.barrier()
             return
-        if mode in ("graph", "graph_sharded", "graph_fused", "graph_push"):
+        if mode in ("graph", "graph_sharded", "graph_fused", "graph_push", "slow_peer_graph"):
             # step 0 eagerly (creates internal streams), then capture ONE step
             # into a CUDA graph and replay it for steps 1.. with fresh grads
             # copied into the captured buffers.
@@ -93,8 +97,13 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode, pieces=0):
                     dst.copy_(torch.from_numpy(x))
                 graph.replay()
             steps = 0
+        snap = None
         for s in range(steps):
             g = [torch.from_numpy(x).cuda() for x in synth.grads(shapes, workers=world, step=s)[rank]]
+            if mode in ("skip", "piece_mismatch"):
+                torch.cuda.synchronize()
+                snap = [np.concatenate([x.cpu().numpy().reshape(-1) for x in w]),
+                        np.concatenate([comm.momentum(t).cpu().numpy().reshape(-1) for t in range(len(w))])]
             if mode == "skip" and rank == 1 and s == 1:
                 continue                              # fault injection: rank 1 skips a collective
             if mode == "reregister" and s == 1:
@@ -164,7 +173,14 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode, pieces=0):
             else:
                 q.put((rank, "ok", wb.tobytes(), vb.tobytes()))
         except cmn.CmnError as e:
-            q.put((rank, "error", e.status_name))
+            if snap is not None:
+                # the failed call must leave w and v exactly as they were
+                wb = np.concatenate([x.cpu().numpy().reshape(-1) for x in w])
+                vb = np.concatenate([comm.momentum(t).cpu().numpy().reshape(-1) for t in range(len(w))])
+                same = wb.tobytes() == snap[0].tobytes() and vb.tobytes() == snap[1].tobytes()
+                q.put((rank, "error", e.status_name, same))
+            else:
+                q.put((rank, "error", e.status_name))
         dist.barrier()            # no rank frees its IPC-exported buffers while a peer may read them
         comm.finalize()
     except Exception as e:  # noqa: BLE001
@@ -417,14 +433,53 @@ def test_ipc_reregistration(orc):
         assert np.array_equal(np.frombuffer(r[3], np.uint32), np.concatenate(v).view(np.uint32))
 
 
-def test_ipc_skipped_collective_times_out():
-    """Fault injection: rank 1 skips one step's all-reduce.  Rank 0's
-    kernel must not hang: its spin-wait times out (3 s) and the error
-    surfaces as CMN_ERR_TIMEOUT -- or, if rank 1's next
-    call pairs with it, the sequence numbers still let both finish."""
-    res = _run(2, "fp32", "oneshot", steps=3, mode="skip")
+@pytest.mark.parametrize("algo,pieces", [("oneshot", 0), ("twoshot", 0), ("oneshot", 2), ("twoshot", 3)])
+def test_ipc_skipped_collective_times_out(algo, pieces):
+    """Fault injection: rank 1 skips one step (every collective of it).
+    Rank 0's call 2 pairs with rank 1's call 3 (same layout, same kinds: a
+    skipped whole step is indistinguishable by design), and rank 0's last
+    call then finds no peer: its spin-wait times out (3 s), the error
+    surfaces as CMN_ERR_TIMEOUT, and -- every later kernel
+    checks the device error word -- that failed call leaves rank 0's w and v
+    bit-identical to what they were before it (serial and pipelined
+    schedules, one-shot and two-shot)."""
+    res = _run(2, "fp32", algo, steps=3, mode="skip", pieces=pieces)
     statuses = {r[0]: r[1:] for r in res}
     assert statuses[0][0] == "error" and statuses[0][1] == "CMN_ERR_TIMEOUT", res
+    assert statuses[0][2] is True, "the timed-out call modified rank 0's w / v"
+
+
+def test_ipc_piece_mismatch_detected_outputs_untouched():
+    """Ranks that cut the step into different pieces (rank 0 one collective
+    over the whole model, rank 1 the pipelined schedule's first piece) issue
+    all-reduces over different packed ranges at the same epoch: the
+    barrier's call tag (range hash) turns that into CMN_ERR_MISMATCH instead
+    of reducing unrelated ranges, and neither rank's w or v changes."""
+    res = _run(2, "fp32", "twoshot", steps=1, mode="piece_mismatch", pieces=1)
+    assert all(r[1] == "error" for r in res), res
+    assert any(r[2] == "CMN_ERR_MISMATCH" for r in res), res
+    assert all(r[2] in ("CMN_ERR_MISMATCH", "CMN_ERR_TIMEOUT") for r in res), res
+    assert all(r[3] is True for r in res), res
+
+
+@pytest.mark.parametrize("mode,dtype", [("slow_peer", "fp32"), ("slow_peer_graph", "fp16")])
+def test_ipc_oneshot_pipelined_slow_peer(orc, mode, dtype):
+    """Advisor finding (pipelined step, one-shot all-reduce): rank 1's
+    one-shot CTAs stall 20 ms after the start barrier, so rank 0 finishes
+    its all-reduce of the last piece and, with an even piece count, packs
+    the next step's gradients into the very region rank 1 has not read yet.
+    The last piece's end barrier must hold rank 0 back: w and v stay
+    bit-exact with the oracle on both ranks, eagerly and replayed from a
+    captured CUDA graph (same buffers every replay)."""
+    res = _run(2, dtype, "oneshot", steps=3, mode=mode, pieces=4)
+    assert all(r[1] == "ok" for r in res), res
+    shapes = synth.mlp_shapes()
+    w = synth.params(shapes)
+    v = [np.zeros_like(x) for x in w]
+    for s in range(3):
+        orc.step(synth.grads(shapes, workers=2, step=s), w, v, 0.1, 0.9, dtype)
+    for r in res:
+        assert np.array_equal(np.frombuffer(r[2], np.uint32), np.concatenate(w).view(np.uint32)), r[0]
 
 
 def test_ipc_structure_mismatch_detected():
