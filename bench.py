@@ -398,7 +398,14 @@ def main():
         t_tune0 = time.time()
 
         def budget_left():
-            return time.time() - t_tune0 < args.tune_budget_s
+            """Collective: every rank gets the same answer (each rank's own
+            clock decides, MIN over ranks), so all ranks try the same
+            candidates -- a divergent choice would pair different
+            collectives across ranks."""
+            ok = torch.tensor([1.0 if time.time() - t_tune0 < args.tune_budget_s else 0.0],
+                              dtype=torch.float64)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            return ok.item() == 1.0
 
         def trial_us():
             for _ in range(3):
@@ -447,20 +454,18 @@ def main():
             return float(t.item()) * 1e3
 
         trials = {}
-        for i, name in enumerate(cands):
-            if i > 0 and not budget_left():
-                break                    # every rank decides from the same max-over-ranks clock below
+        for name in cands:
             set_schedule(name)
             trials[name] = trial_us()
-            go = torch.tensor([1.0 if budget_left() else 0.0], dtype=torch.float64)
-            dist.all_reduce(go, op=dist.ReduceOp.MIN)   # all ranks stop at the same candidate
-            if go.item() == 0.0:
+            if not budget_left():        # collective: all ranks stop at the same candidate
                 break
         # The same schedules replayed from a captured CUDA graph (no host
         # launch cost per step: the pipelined step is ~7 API calls per piece).
         for name in ("pipelined4", "pipelined8", "fused", "fused_push"):
-            if args.schedule != "auto" or name not in trials or not budget_left():
+            if args.schedule != "auto" or name not in trials:
                 continue
+            if not budget_left():
+                break
             set_schedule(name)
             gr = capture_step()
             if gr is not None:

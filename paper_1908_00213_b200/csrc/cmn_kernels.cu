@@ -169,28 +169,50 @@ __device__ __forceinline__ void pack_store8(void *packed, int64_t j, const F8 &x
     }
 }
 
-// One item with 256-bit accesses (src 32-byte aligned, it.base multiple of 8).
-template <int DT>
-__device__ __forceinline__ void pack_item_v8(const float *__restrict__ src, const Item &it,
-                                             void *__restrict__ packed) {
-    const int n8 = it.len >> 3;
-    F8 x[kPackVec8];
+// A CTA's items with 256-bit accesses (every src 32-byte aligned, bases
+// multiples of 8): all loads of all items before the first store.
+template <int DT, int CAP>
+__device__ __forceinline__ void pack_items_v8(const GradTabN<CAP> &g, int t_lo,
+                                              const Item (&its)[kPackItems], int ib, int i1,
+                                              void *__restrict__ packed) {
+    F8 x[kPackItems][kPackVec8];
 #pragma unroll
-    for (int u = 0; u < kPackVec8; ++u) {
-        const int q = threadIdx.x + u * kPackThreads;
-        if (q < n8) x[u] = ld_cs_f8(src + 8 * q);
+    for (int j = 0; j < kPackItems; ++j) {
+        if (ib + j < i1) {
+            const Item it = its[j];
+            const float *__restrict__ src = g.p[it.t - t_lo] + it.k0;
+            const int n8 = it.len >> 3;
+#pragma unroll
+            for (int u = 0; u < kPackVec8; ++u) {
+                const int q = threadIdx.x + u * kPackThreads;
+                if (q < n8) x[j][u] = ld_cs_f8(src + 8 * q);
+            }
+        }
     }
 #pragma unroll
-    for (int u = 0; u < kPackVec8; ++u) {
-        const int q = threadIdx.x + u * kPackThreads;
-        if (q < n8) pack_store8<DT>(packed, it.base + 8 * q, x[u]);
-    }
-    for (int k = (n8 << 3) + threadIdx.x; k < it.len; k += kPackThreads) {
-        const float sv = src[k];
-        if constexpr (DT == 0)
-            static_cast<float *>(packed)[it.base + k] = sv;
-        else
-            static_cast<uint16_t *>(packed)[it.base + k] = __half_as_ushort(__float2half_rn(sv));
+    for (int j = 0; j < kPackItems; ++j) {
+        if (ib + j >= i1) break;
+        const Item it = its[j];
+        const float *__restrict__ src = g.p[it.t - t_lo] + it.k0;
+        const int n8 = it.len >> 3;
+#pragma unroll
+        for (int u = 0; u < kPackVec8; ++u) {
+            const int q = threadIdx.x + u * kPackThreads;
+            if (q < n8) pack_store8<DT>(packed, it.base + 8 * q, x[j][u]);
+        }
+        for (int k = (n8 << 3) + threadIdx.x; k < it.len; k += kPackThreads) {
+            const float sv = src[k];
+            if constexpr (DT == 0)
+                static_cast<float *>(packed)[it.base + k] = sv;
+            else
+                static_cast<uint16_t *>(packed)[it.base + k] = __half_as_ushort(__float2half_rn(sv));
+        }
+        for (int k = threadIdx.x; k < it.pad; k += kPackThreads) {
+            if constexpr (DT == 0)
+                static_cast<float *>(packed)[it.base + it.len + k] = 0.0f;
+            else
+                static_cast<uint16_t *>(packed)[it.base + it.len + k] = 0;
+        }
     }
 }
 
@@ -199,18 +221,13 @@ __device__ __forceinline__ void pack_item_v8(const float *__restrict__ src, cons
 template <int DT, int CAP>
 __device__ __forceinline__ void pack_items(const GradTabN<CAP> &g, int t_lo, const Item (&its)[kPackItems],
                                            int ib, int i1, void *__restrict__ packed) {
-    if constexpr (CMN_PACK_V8 != 0 && kPackItems == 1) {
-        if (ib >= i1) return;
-        const Item it = its[0];
-        const float *__restrict__ src = g.p[it.t - t_lo] + it.k0;
-        if ((reinterpret_cast<uintptr_t>(src) & 31u) == 0) {
-            pack_item_v8<DT>(src, it, packed);
-            for (int k = threadIdx.x; k < it.pad; k += kPackThreads) {
-                if constexpr (DT == 0)
-                    static_cast<float *>(packed)[it.base + it.len + k] = 0.0f;
-                else
-                    static_cast<uint16_t *>(packed)[it.base + it.len + k] = 0;
-            }
+    if constexpr (CMN_PACK_V8 != 0) {
+        bool al = true;
+#pragma unroll
+        for (int j = 0; j < kPackItems; ++j)
+            if (ib + j < i1) al = al && aligned32(g.p[its[j].t - t_lo] + its[j].k0);
+        if (al) {
+            pack_items_v8<DT, CAP>(g, t_lo, its, ib, i1, packed);
             return;
         }
     }

@@ -101,7 +101,8 @@ def test_bench_n8_timesliced_contract():
                         str(_free_port()), "bench.py", "--gpus", "8", "--steps", "4", "--warmup", "3",
                         "--min-warmup-s", "0", "--tune-budget-s", "2", "--no-e2e"],
                        cwd=ROOT, capture_output=True, text=True, timeout=1800)
-    assert p.returncode == 0, p.stderr[-2000:]
+    tb = p.stderr.find("Traceback")
+    assert p.returncode == 0, p.stderr[tb: tb + 3000] if tb >= 0 else p.stderr[-3000:]
     lines = [x for x in p.stdout.splitlines() if x.strip()]
     assert len(lines) == 1, p.stdout
     d = json.loads(lines[0])
