@@ -32,8 +32,17 @@
  *     enqueued).  CUDA / NCCL failures map to CMN_ERR_CUDA / CMN_ERR_NCCL.
  *     A device-side timeout or call-sequence mismatch detected by a kernel
  *     surfaces as CMN_ERR_TIMEOUT / CMN_ERR_MISMATCH on the NEXT call on that
- *     communicator (or from cmn_poll_error).  cmn_last_error() returns a
- *     thread-local text for the last non-OK status.
+ *     communicator (or from cmn_poll_error).  The failed call itself leaves
+ *     the parameters, the momentum / Adam state and its other outputs
+ *     untouched: the detecting kernel and every later kernel of the
+ *     communicator skip their stores (device error word).  One partial case:
+ *     a peer slower than the timeout, arriving after some of a kernel's CTAs
+ *     gave up -- the CTAs that met it apply their (correct) part.  A failed
+ *     communicator stays failed; finalize it.  Call-sequence mismatches are
+ *     detected by a per-call tag (payload dtype, kernel kind, packed range);
+ *     a rank skipping a WHOLE step pairs its next step with the peers' current
+ *     one undetected and the last call then times out.  cmn_last_error()
+ *     returns a thread-local text for the last non-OK status.
  *   - Handles are not thread-safe; one thread drives one communicator.
  *   - Every rank must issue the same sequence of collective calls
  *     (cmn_register_params, cmn_allreduce_*, cmn_step*) with the same layout

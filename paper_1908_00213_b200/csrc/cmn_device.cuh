@@ -204,18 +204,21 @@ __device__ __forceinline__ void record_failure(const Barrier &bar, int code) {
 // also proves every peer finished all its earlier collective kernels.
 //
 // Returns false when the CTA must not touch data: an earlier collective of
-// this communicator already failed (the barrier is not even entered), or
-// this wait timed out / saw a mismatch.  Callers return immediately, so a
-// failed call leaves its outputs (and, through comm_failed, the parameters
-// and optimizer state the update kernels would write) untouched.
+// this communicator already failed, or this wait timed out / saw a
+// mismatch, or another CTA of this rank recorded a failure while we spun.
+// Callers return immediately, so a failed call leaves its outputs (and,
+// through comm_failed, the parameters and optimizer state the update
+// kernels would write) untouched.  The error-word load is issued before the
+// flag round trip and consumed after it, so it adds no latency to a healthy
+// barrier; a rank that already failed still posts its flag once (its peers
+// may pass this barrier with this call's valid inputs and then fail at the
+// next one), but never touches data again.
 __device__ __forceinline__ bool cross_rank_barrier(const Barrier &bar, uint32_t value, int world,
                                                    int slot) {
     if (!bar.enabled) return true;
-    __shared__ int s_dead;
-    if (threadIdx.x == 0) s_dead = comm_failed(bar.derr) ? 1 : 0;
-    __syncthreads();
-    if (s_dead) return false;
     const int tid = threadIdx.x;
+    const int dead0 = tid == 0 && comm_failed(bar.derr) ? 1 : 0;   // consumed at the end
+    __syncthreads();
     int bad = 0;
     if (tid < world) {
         const size_t cell = (static_cast<size_t>(slot) * kMaxBarrierBlocks + blockIdx.x) * kMaxWorld;
@@ -231,6 +234,10 @@ __device__ __forceinline__ bool cross_rank_barrier(const Barrier &bar, uint32_t 
                 break;
             }
             if (static_cast<int32_t>(v - value) >= 0) break;
+            if ((spin & 63u) == 0 && comm_failed(bar.derr)) {   // failed elsewhere: stop waiting
+                bad = 1;
+                break;
+            }
             if ((spin & 1023u) == 0) {
                 const uint64_t t = global_timer_ns();
                 if (t0 == 0) {
@@ -243,7 +250,7 @@ __device__ __forceinline__ bool cross_rank_barrier(const Barrier &bar, uint32_t 
             }
         }
     }
-    return __syncthreads_or(bad) == 0;
+    return __syncthreads_or(bad | dead0) == 0;
 }
 
 }  // namespace cmn
