@@ -1038,3 +1038,71 @@ def test_step_host_packed_param_staging(cmn, orc, monkeypatch, per_tensor):
                     assert_bitwise(hw.numpy()[off[t]: off[t] + sizes[t]].copy(), w_o[t], f"host w[{t}] step {s}")
     finally:
         comm.finalize()
+
+
+@pytest.mark.parametrize("N,dtype", [(3, "fp32"), (5, "fp16"), (6, "fp32"), (7, "fp32")])
+def test_average_by_division_every_kernel(cmn, orc, N, dtype):
+    """Reading R3 ("dividing the sum by the number of
+    replicas") at N that are not powers of two -- where r * fl(1/N) and r / N
+    differ -- through every kernel that averages: cmn_unpack_avg_grads (the
+    averaged gradient itself, vs the oracle's `avg` output), the update from
+    the reduced buffer, the fused all-gather + update, the sharded update and
+    Adam, each bitwise vs the oracle."""
+    shapes = RAGGED + [(1000,)]
+    grads = synth.grads(shapes, workers=N, seed=11)
+    params0 = synth.params(shapes, seed=11)
+    w_o = [p.copy() for p in params0]
+    v_o = [np.zeros_like(p) for p in params0]
+    res = orc.step(grads, w_o, v_o, 0.1, 0.9, dtype, want_avg=True)
+    # the oracle's average differs from the reciprocal product somewhere (the
+    # case this test exists for)
+    r = orc.f16_to_f32(res["reduced"]) if dtype == "fp16" else res["reduced"]
+    recip = (r * np.float32(1.0 / N)).astype(np.float32)
+    avg_flat = np.concatenate(res["avg"])
+    off = res["off"]
+    recip_flat = np.concatenate([recip[off[t]: off[t] + p.size] for t, p in enumerate(params0)])
+    assert np.count_nonzero(avg_flat.view(np.uint32) != recip_flat.view(np.uint32)) > 0
+    for mode in ("unpack", "serial", "fused", "sharded"):
+        comm = cmn.Comm.simulated_world(N)
+        try:
+            w = to_dev(params0)
+            comm.register_params(w)
+            gd = comm.prepare([to_dev(gw) for gw in grads])
+            if mode == "unpack":
+                comm.allreduce_grads(gd, dtype)
+                out = [torch.empty_like(x) for x in w]
+                comm.unpack_avg_grads(out)
+                torch.cuda.synchronize()
+                for t in range(len(w)):
+                    assert_bitwise(out[t].cpu().numpy().reshape(-1), res["avg"][t], f"avg[{t}]")
+                continue
+            if mode == "serial":
+                comm.allreduce_grads(gd, dtype)
+                comm.update_momentum_sgd(0.1, 0.9)
+            elif mode == "fused":
+                comm.set_fused_update(1)
+                comm.step(gd, dtype, 0.1, 0.9)
+            else:
+                comm.step_sharded(gd, dtype, 0.1, 0.9)
+            torch.cuda.synchronize()
+            for t in range(len(w)):
+                assert_bitwise(w[t].cpu().numpy().reshape(-1), w_o[t], f"{mode} w[{t}]")
+        finally:
+            comm.finalize()
+    # Adam from the reduced buffer
+    sizes = [synth.numel(s) for s in shapes]
+    w_a = [p.copy() for p in params0]
+    m_a = [np.zeros_like(p) for p in params0]
+    v_a = [np.zeros_like(p) for p in params0]
+    orc.update_adam(res["reduced"], dtype, N, 1e-3, 0.9, 0.999, 1e-8, 1, orc.layout(sizes)[0], w_a, m_a, v_a)
+    comm = cmn.Comm.simulated_world(N)
+    try:
+        w = to_dev(params0)
+        comm.register_params(w)
+        comm.allreduce_grads([to_dev(gw) for gw in grads], dtype)
+        comm.update_adam(1e-3, 0.9, 0.999, 1e-8, 1)
+        torch.cuda.synchronize()
+        for t in range(len(w)):
+            assert_bitwise(w[t].cpu().numpy().reshape(-1), w_a[t], f"adam w[{t}]")
+    finally:
+        comm.finalize()
