@@ -63,7 +63,10 @@ cmn_status check_async_error(cmn_comm *c) {
     if (!c->h_err) return CMN_OK;
     const int e = *reinterpret_cast<volatile int *>(c->h_err);
     if (e == 1) return fail(CMN_ERR_TIMEOUT, "device spin-wait on a peer timed out");
-    if (e == 2) return fail(CMN_ERR_MISMATCH, "peer issued a different collective (dtype/algo)");
+    if (e == 2) return fail(CMN_ERR_MISMATCH, "peer issued a different collective (dtype/algo/kind/range)");
+    if (e == 3)
+        return fail(CMN_ERR_TIMEOUT, "a peer rank's communicator failed earlier (timeout or call "
+                                     "mismatch there); this rank stopped waiting for it");
     return CMN_OK;
 }
 

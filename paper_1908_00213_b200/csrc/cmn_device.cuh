@@ -159,28 +159,6 @@ __device__ __forceinline__ uint64_t global_timer_ns() {
     return t;
 }
 
-// Fault injection for tests: stall the calling thread for `ns` nanoseconds.
-__device__ __forceinline__ void stall_ns(uint32_t ns) {
-    const uint64_t t0 = global_timer_ns();
-    while (global_timer_ns() - t0 < ns) {
-    }
-}
-
-// This call's barrier value for the calling CTA: reads and advances the
-// CTA's epoch counter (one increment per collective kernel; the next kernel
-// on the stream starts after this one completes, so reads see the update).
-__device__ __forceinline__ uint32_t barrier_value(const Barrier &bar) {
-    __shared__ uint32_t s_val;
-    if (!bar.enabled) return 0;
-    if (threadIdx.x == 0) {
-        const uint32_t e = bar.epoch[blockIdx.x] + 1u;
-        bar.epoch[blockIdx.x] = e;
-        s_val = (e << kTagBits) | (bar.tag & kTagMask);
-    }
-    __syncthreads();
-    return s_val;
-}
-
 // Has a collective of this communicator failed (timeout or mismatch)?  The
 // device-memory error word is set by the barrier that detected it; every
 // later kernel of the step checks it and leaves its outputs untouched.
@@ -194,6 +172,40 @@ __device__ __forceinline__ void record_failure(const Barrier &bar, int code) {
     *reinterpret_cast<volatile int *>(bar.err) = code;
 }
 
+// Fault injection for tests: stall the calling thread for `ns` nanoseconds.
+__device__ __forceinline__ void stall_ns(uint32_t ns) {
+    const uint64_t t0 = global_timer_ns();
+    while (global_timer_ns() - t0 < ns) {
+    }
+}
+
+// This call's barrier value for the calling CTA: reads and advances the
+// CTA's epoch counter (one increment per collective kernel; the next kernel
+// on the stream starts after this one completes, so reads see the update).
+//
+// When an earlier kernel of this communicator already failed (device error
+// word) the value carries the reserved tag kDeadTag instead of the call tag:
+// cross_rank_barrier then posts it as a poison flag and returns false.  A
+// failed rank that posted a normal value would overwrite its cell with a
+// later epoch, which a peer still waiting on an earlier barrier reads as
+// "passed" (flags only grow) -- pairing it with a collective that never
+// happened (scripts/diag_piece_mismatch.py saw a TIMEOUT at the next
+// barrier instead of the MISMATCH); the poison instead makes every waiting
+// peer fail at once.  The error word is loaded together with the epoch
+// counter, so the check costs no latency.
+__device__ __forceinline__ uint32_t barrier_value(const Barrier &bar) {
+    __shared__ uint32_t s_val;
+    if (!bar.enabled) return 0;
+    if (threadIdx.x == 0) {
+        const bool dead = comm_failed(bar.derr);
+        const uint32_t e = bar.epoch[blockIdx.x] + 1u;
+        bar.epoch[blockIdx.x] = e;
+        s_val = (e << kTagBits) | (dead ? kDeadTag : (bar.tag & kTagMask));
+    }
+    __syncthreads();
+    return s_val;
+}
+
 // Pairwise per-CTA barrier across ranks: CTA b of rank r tells CTA b of
 // every rank "my inputs for this phase are published" and waits for the
 // same from all of them.  Flag values only grow, so no reset is needed; a
@@ -203,21 +215,31 @@ __device__ __forceinline__ void record_failure(const Barrier &bar, int code) {
 // after the previous kernel on its stream completed, passing the barrier
 // also proves every peer finished all its earlier collective kernels.
 //
-// Returns false when the CTA must not touch data: an earlier collective of
-// this communicator already failed, or this wait timed out / saw a
-// mismatch, or another CTA of this rank recorded a failure while we spun.
-// Callers return immediately, so a failed call leaves its outputs (and,
-// through comm_failed, the parameters and optimizer state the update
-// kernels would write) untouched.  The error-word load is issued before the
-// flag round trip and consumed after it, so it adds no latency to a healthy
-// barrier; a rank that already failed still posts its flag once (its peers
-// may pass this barrier with this call's valid inputs and then fail at the
-// next one), but never touches data again.
+// Returns false when the CTA must not touch data: an earlier kernel of this
+// communicator already failed (barrier_value carried kDeadTag: the poison
+// is posted to every peer's cells of both slots, nothing else happens), a
+// peer posted the poison, this wait timed out or saw a mismatch, or another
+// CTA of this rank recorded a failure while we spun (polled every 64 spins,
+// so one CTA's timeout stops the others at once).  Callers return immediately, so a
+// failed call leaves its outputs (and, through comm_failed, the parameters
+// and optimizer state the update kernels would write) untouched.  Within one
+// kernel a CTA that passed its start barrier still posts its later barrier
+// (mid / end) even if another CTA failed meanwhile: its peer CTA passed the
+// same start barrier, so the pair stays consistent.
 __device__ __forceinline__ bool cross_rank_barrier(const Barrier &bar, uint32_t value, int world,
                                                    int slot) {
     if (!bar.enabled) return true;
     const int tid = threadIdx.x;
-    const int dead0 = tid == 0 && comm_failed(bar.derr) ? 1 : 0;   // consumed at the end
+    if ((value & kTagMask) == kDeadTag) {  // uniform across the CTA (shared value)
+        if (tid < world) {
+            for (int sl = 0; sl < kBarrierSlots; ++sl)
+                st_release_sys(bar.flags[tid] +
+                                   (static_cast<size_t>(sl) * kMaxBarrierBlocks + blockIdx.x) * kMaxWorld +
+                                   bar.rank,
+                               value);
+        }
+        return false;
+    }
     __syncthreads();
     int bad = 0;
     if (tid < world) {
@@ -228,6 +250,11 @@ __device__ __forceinline__ bool cross_rank_barrier(const Barrier &bar, uint32_t 
         uint64_t t0 = 0;
         for (uint32_t spin = 1;; ++spin) {
             const uint32_t v = ld_acquire_sys(mine);
+            if ((v & kTagMask) == kDeadTag) {   // the peer's communicator failed earlier
+                record_failure(bar, 3);
+                bad = 1;
+                break;
+            }
             if ((v >> kTagBits) == (value >> kTagBits) && v != value) {
                 record_failure(bar, 2);
                 bad = 1;
@@ -250,7 +277,7 @@ __device__ __forceinline__ bool cross_rank_barrier(const Barrier &bar, uint32_t 
             }
         }
     }
-    return __syncthreads_or(bad | dead0) == 0;
+    return __syncthreads_or(bad) == 0;
 }
 
 }  // namespace cmn

@@ -29,6 +29,9 @@ constexpr int kGradCap = 256;         // grad pointers carried per launch (kerne
 // epoch is reported as CMN_ERR_MISMATCH instead of being paired with it.
 constexpr uint32_t kTagBits = 8;
 constexpr uint32_t kTagMask = (1u << kTagBits) - 1u;
+// Poison tag a failed rank posts instead of a call tag (kind bits 7: no real
+// kernel kind), so waiting peers fail at once instead of timing out.
+constexpr uint32_t kDeadTag = 0xFFu;
 
 // One registered tensor (device-resident table built at registration).
 struct TensorDesc {
@@ -75,7 +78,7 @@ struct Barrier {
     uint32_t tag;       // kTagBits bits (dtype, kernel kind, range hash); a
                         // same-epoch different-tag peer is a call-sequence mismatch
     uint64_t timeout_ns;
-    int *err;           // host-mapped error word: 0 ok, 1 timeout, 2 mismatch
+    int *err;           // host-mapped error word: 0 ok, 1 timeout, 2 mismatch, 3 peer failed
     int *derr;          // the same code in device memory, read by every later
                         // kernel of the communicator (comm_failed) to skip its stores
     uint32_t test_delay_ns;   // fault injection (tests only, CMN_TEST_ONESHOT_DELAY_US):
