@@ -38,7 +38,10 @@
  *     communicator skip their stores (device error word).  One partial case:
  *     a peer slower than the timeout, arriving after some of a kernel's CTAs
  *     gave up -- the CTAs that met it apply their (correct) part.  A failed
- *     communicator stays failed; finalize it.  Call-sequence mismatches are
+ *     communicator stays failed (finalize it) and posts a poison flag in
+ *     its later collectives, so its peers fail at once with CMN_ERR_TIMEOUT
+ *     ("a peer rank's communicator failed") instead of waiting out the
+ *     timeout.  Call-sequence mismatches are
  *     detected by a per-call tag (payload dtype, kernel kind, packed range);
  *     a rank skipping a WHOLE step pairs its next step with the peers' current
  *     one undetected and the last call then times out.  cmn_last_error()
