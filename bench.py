@@ -67,6 +67,11 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=10.0,
                     help="cpu_baseline: time full-workload oracle steps for about this long (>= 3 steps)")
+    ap.add_argument("--nvls", action="store_true",
+                    help="N > 1: also time the NVLS (multimem) all-reduce as a comparison and, if it passes "
+                         "the runtime tolerance gate, as a headline candidate.  Off by default: the kernel "
+                         "has never executed on hardware (the one-GPU boxes refuse multicast objects), and "
+                         "a fault there would poison the CUDA context of the whole N > 1 run")
     ap.add_argument("--tune-budget-s", type=float, default=30.0,
                     help="N > 1 schedule autotune: stop trying candidates after this long "
                          "(candidates in a fixed order, the default schedule first)")
@@ -503,7 +508,10 @@ def main():
         us_ar = allreduce_only_us()
         comparisons["cmn"] = {"allreduce_incl_pack_us": us_ar,
                               "allreduce_incl_pack_bus_gbs": S_bus / (us_ar * 1e-6) / 1e9}
-        for alt in ("nccl", "nvls"):
+        if not args.nvls:
+            comparisons["nvls"] = {"unavailable": "not requested (bench.py --nvls): never executed on "
+                                                  "hardware yet, kept out of the default run"}
+        for alt in ("nccl", "nvls") if args.nvls else ("nccl",):
             with stdout_to_stderr():        # NCCL INFO lines -> stderr
                 try:
                     comm.set_algo(alt)
