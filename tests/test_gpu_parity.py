@@ -1046,8 +1046,9 @@ def test_average_by_division_every_kernel(cmn, orc, N, dtype):
     replicas") at N that are not powers of two -- where r * fl(1/N) and r / N
     differ -- through every kernel that averages: cmn_unpack_avg_grads (the
     averaged gradient itself, vs the oracle's `avg` output), the update from
-    the reduced buffer, the fused all-gather + update, the sharded update and
-    Adam, each bitwise vs the oracle."""
+    the reduced buffer (serial and pipelined), the fused all-gather + update
+    (pull and push), the sharded update and Adam, each bitwise vs the
+    oracle."""
     shapes = RAGGED + [(1000,)]
     grads = synth.grads(shapes, workers=N, seed=11)
     params0 = synth.params(shapes, seed=11)
@@ -1062,7 +1063,7 @@ def test_average_by_division_every_kernel(cmn, orc, N, dtype):
     off = res["off"]
     recip_flat = np.concatenate([recip[off[t]: off[t] + p.size] for t, p in enumerate(params0)])
     assert np.count_nonzero(avg_flat.view(np.uint32) != recip_flat.view(np.uint32)) > 0
-    for mode in ("unpack", "serial", "fused", "sharded"):
+    for mode in ("unpack", "serial", "pipelined", "fused", "push", "sharded"):
         comm = cmn.Comm.simulated_world(N)
         try:
             w = to_dev(params0)
@@ -1079,8 +1080,11 @@ def test_average_by_division_every_kernel(cmn, orc, N, dtype):
             if mode == "serial":
                 comm.allreduce_grads(gd, dtype)
                 comm.update_momentum_sgd(0.1, 0.9)
-            elif mode == "fused":
-                comm.set_fused_update(1)
+            elif mode == "pipelined":
+                comm.set_pipeline(3)
+                comm.step(gd, dtype, 0.1, 0.9)
+            elif mode in ("fused", "push"):
+                comm.set_fused_update(1 if mode == "fused" else 2)
                 comm.step(gd, dtype, 0.1, 0.9)
             else:
                 comm.step_sharded(gd, dtype, 0.1, 0.9)
@@ -1104,5 +1108,50 @@ def test_average_by_division_every_kernel(cmn, orc, N, dtype):
         torch.cuda.synchronize()
         for t in range(len(w)):
             assert_bitwise(w[t].cpu().numpy().reshape(-1), w_a[t], f"adam w[{t}]")
+    finally:
+        comm.finalize()
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "fp16"])
+def test_pack_16b_aligned_gradients_fallback(cmn, orc, dtype):
+    """The pack's 256-bit path needs 32-byte aligned gradient pointers; the
+    C ABI only requires 16 bytes.  Gradients placed at 16-byte (not 32-byte)
+    offsets inside one allocation take the 128-bit path for those items:
+    packed buffers, reduced buffers and w, v still bit-exact (N = 3)."""
+    shapes = RAGGED + [(8192,), (64, 65)]
+    N = 3
+    grads = [synth.grads(shapes, workers=N, step=s, seed=13) for s in range(2)]
+    params0 = synth.params(shapes, seed=13)
+    ora, _, _ = run_oracle(orc, shapes, N, dtype, grads, params0, 0.1, 0.9)
+    comm = cmn.Comm.simulated_world(N)
+    try:
+        w = to_dev(params0)
+        comm.register_params(w)
+        off, L = comm.layout()
+        tdt = torch.float32 if dtype == "fp32" else torch.int16
+        for s, g in enumerate(grads):
+            gd = []
+            for gw in g:
+                views = []
+                for t, x in enumerate(gw):
+                    # every tensor 16 B past a 32-B boundary of its own buffer
+                    buf = torch.empty(x.size + 8, dtype=torch.float32, device=DEV)
+                    assert buf.data_ptr() % 32 == 0
+                    v = buf[4: 4 + x.size]
+                    assert v.data_ptr() % 32 == 16
+                    v.copy_(torch.from_numpy(x.reshape(-1)))
+                    views.append(v)
+                gd.append(views)
+            comm.allreduce_grads(gd, dtype)
+            for r in range(N):
+                p = torch.empty(L, dtype=tdt, device=DEV)
+                comm.copy_packed(r, p)
+                got = p.cpu().numpy()
+                got = got.view(np.uint16) if dtype == "fp16" else got
+                assert_bitwise(got, ora[s]["packed"][r], f"step {s} packed rank {r}")
+            comm.update_momentum_sgd(0.1, 0.9)
+            torch.cuda.synchronize()
+            for t in range(len(w)):
+                assert_bitwise(w[t].cpu().numpy().reshape(-1), ora[s]["w"][t], f"step {s} w[{t}]")
     finally:
         comm.finalize()
