@@ -72,6 +72,10 @@ def parse():
                          "the runtime tolerance gate, as a headline candidate.  Off by default: the kernel "
                          "has never executed on hardware (the one-GPU boxes refuse multicast objects), and "
                          "a fault there would poison the CUDA context of the whole N > 1 run")
+    ap.add_argument("--sweep-budget-s", type=float, default=20.0,
+                    help="N > 1: BASELINE config 5 -- packed-buffer sweep 64 KB .. 1 GB (fp32), the "
+                         "hand-written all-reduce vs NCCL, bus GB/s; stops when this budget is spent "
+                         "(0 = off)")
     ap.add_argument("--tune-budget-s", type=float, default=30.0,
                     help="N > 1 schedule autotune: stop trying candidates after this long "
                          "(candidates in a fixed order, the default schedule first)")
@@ -278,6 +282,86 @@ def run_reference(args):
             "e2e": {"value": us, "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
+
+
+# ------------------------------------------------- config 5 (N > 1 only)
+
+SWEEP_BYTES = [64 << 10, 1 << 20, 16 << 20, 256 << 20, 1 << 30]
+
+
+def config5_sweep(args, rank, world, local, group, dev, stream):
+    """BASELINE config 5 at this N: one flat fp32 "tensor" of S bytes, S from
+    64 KB to 1 GB; pack + all-reduce alone (cmn_allreduce_grads, no update)
+    with the hand-written kernels (algo auto: one-shot <= 1 MB, else
+    two-shot) and with NCCL, 10 calls after 3 warm-up, max over ranks; bus
+    GB/s = 2(N-1)/N S / t.  A separate communicator (one re-registration per
+    size, a collective); the inputs are device-generated (timing only, no
+    parity claim).  Stops when --sweep-budget-s is spent (decided
+    collectively, so every rank runs the same sizes)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1908_00213_b200 import Comm
+    from paper_1908_00213_b200.cmn import CmnError
+    t0 = time.time()
+    out = []
+    c2 = Comm.init(rank, world, local, group)
+
+    def agree(flag: bool) -> bool:
+        t = torch.tensor([1.0 if flag else 0.0], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return t.item() == 1.0
+
+    def time_ar(table):
+        for _ in range(3):
+            c2.allreduce_grads(table, "fp32", stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(10):
+            c2.allreduce_grads(table, "fp32", stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b) / 10 * 1e3], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        c2.update_momentum_sgd(0.0, 0.0, stream)      # consume (state hygiene)
+        return float(t.item())
+
+    nccl_ok = None
+    try:
+        for S in SWEEP_BYTES:
+            if not agree(time.time() - t0 < args.sweep_budget_s):
+                break
+            n = S // 4
+            w = torch.zeros(n, dtype=torch.float32, device=dev)
+            gen = torch.Generator(device=dev).manual_seed(190800213 + rank)
+            g = torch.empty(n, dtype=torch.float32, device=dev).uniform_(-1e-2, 1e-2, generator=gen)
+            c2.register_params([w])
+            c2.set_algo("auto")
+            table = c2.prepare([g])
+            bus = 2 * (world - 1) / world * S
+            rec = {"bytes": S, "dtype": "fp32"}
+            us = time_ar(table)
+            rec.update(cmn_us=us, cmn_bus_gbs=bus / (us * 1e-6) / 1e9)
+            if nccl_ok is not False:
+                with stdout_to_stderr():
+                    try:
+                        c2.set_algo("nccl")
+                        nccl_ok = True
+                    except CmnError as e:
+                        nccl_ok = False
+                        rec["nccl"] = f"unavailable: {str(e)[:120]}"
+                    if nccl_ok:
+                        un = time_ar(table)
+                        rec.update(nccl_us=un, nccl_bus_gbs=bus / (un * 1e-6) / 1e9)
+            out.append(rec)
+            del table, g, w
+    finally:
+        with stdout_to_stderr():
+            c2.finalize()
+    torch.cuda.empty_cache()
+    return out
 
 
 # ---------------------------------------------------------------- the bench
@@ -711,6 +795,10 @@ def main():
 
     with stdout_to_stderr():              # ncclCommDestroy may log
         comm.finalize()
+
+    sweep = None
+    if world > 1 and args.sweep_budget_s > 0:
+        sweep = config5_sweep(args, rank, world, local, group, dev, stream)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -808,7 +896,8 @@ def main():
                "step_us_after_l2_write_flush": cold_us,
                "per_step_us": per_step,
                "replicas_bitwise_equal": replicas_equal,
-               "warmup_steps_run": n_w}
+               "warmup_steps_run": n_w,
+               "config5_sweep": sweep}
     line = {"metric": METRIC, "value": us, "unit": "us", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded counter-hash, synth/)",

@@ -90,6 +90,9 @@ def _check_n_gt_1(d, n):
         assert "unavailable" in c[alt] or c[alt]["allreduce_incl_pack_us"] > 0
     assert d["details"]["schedule_trials_us"]
     assert d["details"]["tune_budget_s"] is not None
+    sw = d["details"]["config5_sweep"]          # BASELINE config 5, budget-bounded
+    assert sw and sw[0]["bytes"] == 64 << 10 and all(x["cmn_us"] > 0 and x["cmn_bus_gbs"] > 0 for x in sw)
+    assert all("nccl_us" in x or "nccl" in x for x in sw)
 
 
 def test_bench_n8_timesliced_contract():
