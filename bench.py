@@ -344,7 +344,9 @@ def config5_sweep(args, rank, world, local, group, dev, stream):
             rec = {"bytes": S, "dtype": "fp32"}
             us = time_ar(table)
             rec.update(cmn_us=us, cmn_bus_gbs=bus / (us * 1e-6) / 1e9)
-            if nccl_ok is not False:
+            if nccl_ok is False:
+                rec["nccl"] = "unavailable (see the first size)"
+            else:
                 with stdout_to_stderr():
                     try:
                         c2.set_algo("nccl")
