@@ -284,6 +284,18 @@ def run_reference(args):
     return 0
 
 
+def all_ranks_agree(flag: bool) -> bool:
+    """Collective over the default (gloo) group: True only if every rank
+    passes True (MIN over ranks).  Every decision that selects which
+    collectives run next (autotune budget, sweep budget) goes through it, so
+    ranks whose clocks disagree never issue different collectives."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([1.0 if flag else 0.0], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return t.item() == 1.0
+
+
 # ------------------------------------------------- config 5 (N > 1 only)
 
 SWEEP_BYTES = [64 << 10, 1 << 20, 16 << 20, 256 << 20, 1 << 30]
@@ -307,11 +319,6 @@ def config5_sweep(args, rank, world, local, group, dev, stream):
     out = []
     c2 = Comm.init(rank, world, local, group)
 
-    def agree(flag: bool) -> bool:
-        t = torch.tensor([1.0 if flag else 0.0], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MIN)
-        return t.item() == 1.0
-
     def time_ar(table):
         for _ in range(3):
             c2.allreduce_grads(table, "fp32", stream)
@@ -331,7 +338,7 @@ def config5_sweep(args, rank, world, local, group, dev, stream):
     nccl_ok = None
     try:
         for S in SWEEP_BYTES:
-            if not agree(time.time() - t0 < args.sweep_budget_s):
+            if not all_ranks_agree(time.time() - t0 < args.sweep_budget_s):
                 break
             n = S // 4
             w = torch.zeros(n, dtype=torch.float32, device=dev)
@@ -493,10 +500,7 @@ def main():
             clock decides, MIN over ranks), so all ranks try the same
             candidates -- a divergent choice would pair different
             collectives across ranks."""
-            ok = torch.tensor([1.0 if time.time() - t_tune0 < args.tune_budget_s else 0.0],
-                              dtype=torch.float64)
-            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-            return ok.item() == 1.0
+            return all_ranks_agree(time.time() - t_tune0 < args.tune_budget_s)
 
         def trial_us():
             for _ in range(3):

@@ -105,3 +105,37 @@ def test_bootstrap_agrees(world):
 def test_bootstrap_mismatch_on_every_rank(mode):
     res = _run(mode)
     assert [r[1] for r in res] == [5, 5]      # CMN_ERR_MISMATCH on both ranks
+
+
+def _agree_worker(rank, world, port, q):
+    import sys
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import bench
+        # rank 1's budget ran out, the others' did not: nobody continues
+        out = [bench.all_ranks_agree(rank != 1), bench.all_ranks_agree(True), bench.all_ranks_agree(False)]
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_bench_budget_decisions_are_collective(world):
+    """bench.py's autotune / sweep budget stop is decided collectively (MIN
+    over ranks): with one rank out of budget every rank stops, so no rank
+    issues a collective its peers skip (the divergence that hung the
+    time-sliced N = 8 run once)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_agree_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(world)])
+    for p in ps:
+        p.join(timeout=60)
+    assert all(r[1] == [False, True, False] for r in res), res
