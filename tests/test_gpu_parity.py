@@ -1155,3 +1155,91 @@ def test_pack_16b_aligned_gradients_fallback(cmn, orc, dtype):
                 assert_bitwise(w[t].cpu().numpy().reshape(-1), ora[s]["w"][t], f"step {s} w[{t}]")
     finally:
         comm.finalize()
+
+
+@pytest.mark.parametrize("N", [1, 3])
+def test_checkpoint_resume_bitwise(cmn, orc, N):
+    """SURVEY §5 checkpoint / resume: 2 steps, snapshot w and the library-
+    owned momentum (cmn_get_momentum, read/write) to the host, finalize;
+    a fresh communicator registers the restored w, writes the momentum back
+    and takes 2 more steps -- bitwise equal to 4 uninterrupted oracle steps.
+    The same for Adam's m and v (cmn_get_adam_state) with the step count
+    continued by the caller."""
+    shapes = synth.mlp_shapes() + [(4097,)]
+    grads = [synth.grads(shapes, workers=N, step=s, seed=17) for s in range(4)]
+    params0 = synth.params(shapes, seed=17)
+    w_o = [p.copy() for p in params0]
+    v_o = [np.zeros_like(p) for p in params0]
+    for g in grads:
+        orc.step(g, w_o, v_o, 0.1, 0.9, "fp32")
+
+    def new_comm():
+        return cmn.Comm.simulated_world(N) if N > 1 else cmn.Comm.init(0, 1, 0)
+
+    def feed(g):
+        return [to_dev(gw) for gw in g] if N > 1 else to_dev(g[0])
+
+    comm = new_comm()
+    try:
+        w = to_dev(params0)
+        comm.register_params(w)
+        for g in grads[:2]:
+            comm.step(feed(g), "fp32", 0.1, 0.9)
+        torch.cuda.synchronize()
+        ck_w = [x.cpu().clone() for x in w]
+        ck_v = [comm.momentum(t).cpu().clone() for t in range(len(w))]
+    finally:
+        comm.finalize()
+    comm = new_comm()
+    try:
+        w = [x.to(DEV) for x in ck_w]
+        comm.register_params(w)                       # momentum starts at zero ...
+        for t in range(len(w)):
+            comm.momentum(t).copy_(ck_v[t].to(DEV))   # ... and is restored
+        for g in grads[2:]:
+            comm.step(feed(g), "fp32", 0.1, 0.9)
+        torch.cuda.synchronize()
+        for t in range(len(w)):
+            assert_bitwise(w[t].cpu().numpy().reshape(-1), w_o[t].reshape(-1), f"resumed w[{t}]")
+            assert_bitwise(comm.momentum(t).cpu().numpy().reshape(-1), v_o[t].reshape(-1), f"resumed v[{t}]")
+    finally:
+        comm.finalize()
+    # Adam: m, v restored through cmn_get_adam_state, step count continued
+    sizes = [synth.numel(s) for s in shapes]
+    off = orc.layout(sizes)[0]
+    wa = [p.copy() for p in params0]
+    ma = [np.zeros_like(p) for p in params0]
+    va = [np.zeros_like(p) for p in params0]
+    for k, g in enumerate(grads):
+        red = orc.reduce_tree([orc.pack(gw, off, orc.layout(sizes)[1], "fp32") for gw in g], "fp32")
+        orc.update_adam(red, "fp32", N, 1e-3, 0.9, 0.999, 1e-8, k + 1, off, wa, ma, va)
+    comm = new_comm()
+    try:
+        w = to_dev(params0)
+        comm.register_params(w)
+        for k, g in enumerate(grads[:2]):
+            comm.step_adam(feed(g), "fp32", 1e-3, 0.9, 0.999, 1e-8, k + 1)
+        torch.cuda.synchronize()
+        ck_w = [x.cpu().clone() for x in w]
+        ck = [tuple(s.cpu().clone() for s in comm.adam_state(t)) for t in range(len(w))]
+    finally:
+        comm.finalize()
+    comm = new_comm()
+    try:
+        w = [x.to(DEV) for x in ck_w]
+        comm.register_params(w)
+        comm.step_adam(feed([[np.zeros_like(p) for p in params0] for _ in range(N)]), "fp32",
+                       0.0, 0.9, 0.999, 1e-8, 1)        # allocates the state (alpha = 0: w unchanged)
+        for t in range(len(w)):
+            m_t, v_t = comm.adam_state(t)
+            m_t.copy_(ck[t][0].to(DEV))
+            v_t.copy_(ck[t][1].to(DEV))
+        for t in range(len(w)):
+            assert_bitwise(w[t].cpu().numpy().reshape(-1), ck_w[t].numpy().reshape(-1), "alpha=0 step")
+        for k, g in enumerate(grads[2:]):
+            comm.step_adam(feed(g), "fp32", 1e-3, 0.9, 0.999, 1e-8, k + 3)
+        torch.cuda.synchronize()
+        for t in range(len(w)):
+            assert_bitwise(w[t].cpu().numpy().reshape(-1), wa[t].reshape(-1), f"resumed adam w[{t}]")
+    finally:
+        comm.finalize()
