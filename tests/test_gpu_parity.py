@@ -13,7 +13,6 @@ import numpy as np
 import pytest
 import torch
 
-import oracle as orc_mod
 import synth
 
 pytestmark = pytest.mark.gpu
