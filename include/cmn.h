@@ -160,6 +160,21 @@ cmn_status cmn_init(int rank, int world_size, int cuda_device,
  * construction; cmn_copy_reduced exposes every rank's reduced buffer). */
 cmn_status cmn_init_simulated(int world_size, int cuda_device, cmn_comm **out);
 
+/* cmn_init_emulated -- a simulated world (as cmn_init_simulated: one process,
+ * every rank's buffers, rank-major grads) whose one-shot and two-shot
+ * all-reduces run as ONE cooperative launch over
+ * all ranks -- CTA b of rank r is block r * G + b, every block co-resident
+ * -- with the cross-rank barriers LIVE: the same flag pads, per-rank per-CTA
+ * epochs, call tags, timeouts and poison flags as cmn_init mode, exercised
+ * on one GPU without separate launches that wait on one another.  G is the
+ * collective grid (cmn_set_ctas) capped at the co-resident capacity / N.
+ * The other collectives (fused pull / push, sharded, NVLS, NCCL) behave as in
+ * cmn_init_simulated.  Test mode; fault injection through the environment:
+ * CMN_TEST_EMUL_ABSENT_RANK=r (rank r's blocks never arrive: the others time
+ * out), CMN_TEST_EMUL_MISMATCH_RANK=r (rank r posts another call tag).
+ * Errors: as cmn_init_simulated. */
+cmn_status cmn_init_emulated(int world_size, int cuda_device, cmn_comm **out);
+
 /* cmn_finalize -- synchronise the device, unmap peers, free everything the
  * library owns.  NULL is a no-op.  With world_size > 1 peers read this
  * rank's exported buffers during collectives, so call it only after every

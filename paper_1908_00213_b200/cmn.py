@@ -31,6 +31,7 @@ AllgatherFn = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_
 SIGNATURES = [
     ("cmn_init", C.c_int, [C.c_int, C.c_int, C.c_int, AllgatherFn, _P, _PP]),
     ("cmn_init_simulated", C.c_int, [C.c_int, C.c_int, _PP]),
+    ("cmn_init_emulated", C.c_int, [C.c_int, C.c_int, _PP]),
     ("cmn_finalize", C.c_int, [_P]),
     ("cmn_register_params", C.c_int, [_P, C.c_int, C.POINTER(C.c_int), _I64P, _PP]),
     ("cmn_get_layout", C.c_int, [_P, _I64P, _I64P]),
@@ -271,6 +272,15 @@ class Comm:
     def simulated_world(cls, world: int, device: int = 0) -> "Comm":
         h = C.c_void_p()
         _check(lib().cmn_init_simulated(world, device, C.byref(h)), "cmn_init_simulated")
+        return cls(h.value, world, 0, True, device)
+
+    @classmethod
+    def emulated_world(cls, world: int, device: int = 0) -> "Comm":
+        """cmn_init_emulated: the simulated world with its one-/two-shot
+        all-reduces run as ONE cooperative launch over every rank, the
+        cross-rank barriers live (include/cmn.h)."""
+        h = C.c_void_p()
+        _check(lib().cmn_init_emulated(world, device, C.byref(h)), "cmn_init_emulated")
         return cls(h.value, world, 0, True, device)
 
     @classmethod

@@ -31,6 +31,24 @@ cmn_status cmn_init_simulated(int world_size, int cuda_device, cmn_comm **out) {
     }
 }
 
+cmn_status cmn_init_emulated(int world_size, int cuda_device, cmn_comm **out) {
+    try {
+        const cmn_status st = init_common(0, world_size, cuda_device, true, nullptr, nullptr, out);
+        if (st != CMN_OK) return st;
+        cmn_comm *c = *out;
+        c->emulated = true;
+        const auto env_rank = [](const char *name) {
+            const char *v = std::getenv(name);
+            return v && *v ? std::atoi(v) : -1;
+        };
+        c->test_absent_rank = env_rank("CMN_TEST_EMUL_ABSENT_RANK");
+        c->test_mismatch_rank = env_rank("CMN_TEST_EMUL_MISMATCH_RANK");
+        return CMN_OK;
+    } catch (...) {
+        return fail(CMN_ERR_OOM, "host allocation failed");
+    }
+}
+
 cmn_status cmn_finalize(cmn_comm *c) {
     if (!c) return CMN_OK;
     cudaSetDevice(c->device);

@@ -92,6 +92,12 @@ struct ArResult {
 struct cmn_comm {
     int rank = 0, world = 1, device = 0;
     bool simulated = false;
+    // cmn_init_emulated: a simulated world (every rank's buffers in this
+    // process) whose one-shot / two-shot all-reduces run as ONE cooperative
+    // launch over all ranks with the cross-rank barriers live
+    bool emulated = false;
+    int test_absent_rank = -1;     // CMN_TEST_EMUL_ABSENT_RANK (emulation fault injection)
+    int test_mismatch_rank = -1;   // CMN_TEST_EMUL_MISMATCH_RANK
     cmn_allgather_fn ag = nullptr;
     void *user = nullptr;
     int nsm = 148;

@@ -280,6 +280,10 @@ Barrier make_barrier(cmn_comm *c, int dtype, BarrierKind kind, int64_t e0, int64
     b.err = c->d_err;
     b.derr = c->d_errdev;
     b.test_delay_ns = c->test_delay_ns;
+    b.emul_g = 0;                  // set by the emulated launchers
+    for (int r = 0; r < c->world; ++r) b.epochs[r] = c->rb[r].epoch;
+    b.test_absent_rank = c->emulated ? c->test_absent_rank : -1;
+    b.test_mismatch_rank = c->emulated ? c->test_mismatch_rank : -1;
     return b;
 }
 

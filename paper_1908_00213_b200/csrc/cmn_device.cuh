@@ -193,17 +193,41 @@ __device__ __forceinline__ void stall_ns(uint32_t ns) {
 // barrier instead of the MISMATCH); the poison instead makes every waiting
 // peer fail at once.  The error word is loaded together with the epoch
 // counter, so the check costs no latency.
+// Which rank and which of its CTAs this block plays: itself on a real rank;
+// under emulation (bar.emul_g > 0, one cooperative launch for the whole
+// world) block r * emul_g + b plays CTA b of rank r.
+struct CtaRank {
+    int b;      // CTA index within the rank's grid
+    int n;      // the rank's grid size
+    int rank;
+};
+__device__ __forceinline__ CtaRank cta_rank(const Barrier &bar) {
+    if (bar.emul_g > 0)
+        return CtaRank{static_cast<int>(blockIdx.x) % bar.emul_g, bar.emul_g,
+                       static_cast<int>(blockIdx.x) / bar.emul_g};
+    return CtaRank{static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), bar.rank};
+}
+
 __device__ __forceinline__ uint32_t barrier_value(const Barrier &bar) {
     __shared__ uint32_t s_val;
     if (!bar.enabled) return 0;
     if (threadIdx.x == 0) {
+        const CtaRank cr = cta_rank(bar);
+        uint32_t *epoch = bar.emul_g > 0 ? bar.epochs[cr.rank] : bar.epoch;
         const bool dead = comm_failed(bar.derr);
-        const uint32_t e = bar.epoch[blockIdx.x] + 1u;
-        bar.epoch[blockIdx.x] = e;
-        s_val = (e << kTagBits) | (dead ? kDeadTag : (bar.tag & kTagMask));
+        const uint32_t e = epoch[cr.b] + 1u;
+        epoch[cr.b] = e;
+        const uint32_t tag = cr.rank == bar.test_mismatch_rank ? (bar.tag ^ 0x2u) : bar.tag;
+        s_val = (e << kTagBits) | (dead ? kDeadTag : (tag & kTagMask));
     }
     __syncthreads();
     return s_val;
+}
+
+// Emulation fault injection: the CTAs of bar.test_absent_rank never arrive
+// (they return before touching anything), so their peers' barriers time out.
+__device__ __forceinline__ bool emulated_absent(const Barrier &bar) {
+    return bar.emul_g > 0 && static_cast<int>(blockIdx.x) / bar.emul_g == bar.test_absent_rank;
 }
 
 // Pairwise per-CTA barrier across ranks: CTA b of rank r tells CTA b of
@@ -230,12 +254,13 @@ __device__ __forceinline__ bool cross_rank_barrier(const Barrier &bar, uint32_t 
                                                    int slot) {
     if (!bar.enabled) return true;
     const int tid = threadIdx.x;
+    const CtaRank cr = cta_rank(bar);
     if ((value & kTagMask) == kDeadTag) {  // uniform across the CTA (shared value)
         if (tid < world) {
             for (int sl = 0; sl < kBarrierSlots; ++sl)
                 st_release_sys(bar.flags[tid] +
-                                   (static_cast<size_t>(sl) * kMaxBarrierBlocks + blockIdx.x) * kMaxWorld +
-                                   bar.rank,
+                                   (static_cast<size_t>(sl) * kMaxBarrierBlocks + cr.b) * kMaxWorld +
+                                   cr.rank,
                                value);
         }
         return false;
@@ -243,10 +268,10 @@ __device__ __forceinline__ bool cross_rank_barrier(const Barrier &bar, uint32_t 
     __syncthreads();
     int bad = 0;
     if (tid < world) {
-        const size_t cell = (static_cast<size_t>(slot) * kMaxBarrierBlocks + blockIdx.x) * kMaxWorld;
+        const size_t cell = (static_cast<size_t>(slot) * kMaxBarrierBlocks + cr.b) * kMaxWorld;
         __threadfence_system();
-        st_release_sys(bar.flags[tid] + cell + bar.rank, value);
-        const uint32_t *mine = bar.flags[bar.rank] + cell + tid;
+        st_release_sys(bar.flags[tid] + cell + cr.rank, value);
+        const uint32_t *mine = bar.flags[cr.rank] + cell + tid;
         uint64_t t0 = 0;
         for (uint32_t spin = 1;; ++spin) {
             const uint32_t v = ld_acquire_sys(mine);

@@ -83,6 +83,14 @@ struct Barrier {
                         // kernel of the communicator (comm_failed) to skip its stores
     uint32_t test_delay_ns;   // fault injection (tests only, CMN_TEST_ONESHOT_DELAY_US):
                               // one-shot CTAs stall this long after the start barrier
+    // Emulated world (cmn_init_emulated): one COOPERATIVE launch plays every
+    // rank -- CTA b of rank r is blockIdx.x = r * emul_g + b, all co-resident
+    // by construction -- so the cross-rank barrier runs for real on one GPU
+    // without separate launches that wait on one another.  0 = off.
+    int emul_g;
+    uint32_t *epochs[kMaxWorld];   // emulation: every rank's per-CTA epoch counters
+    int test_absent_rank;     // emulation fault injection: this rank's CTAs never arrive (-1: none)
+    int test_mismatch_rank;   // emulation fault injection: this rank posts another call tag (-1: none)
 };
 
 // Peer buffer table (packed or reduced) in 16-byte units.
@@ -136,19 +144,24 @@ cudaError_t launch_adam_direct(const GradTab &g, const GradTab &wt, int ntab, in
 // a2 one-shot: out[j] = tree_i(in_i[j]) for j in [e0, e1) (elements; e0, e1
 // multiples of kAlign).  Barrier slot 0 at entry when enabled; with
 // end_barrier also slot 1 at exit (every peer finished reading `in`).
+// Emulated world (bar.enabled, emulate = true): ONE cooperative launch of
+// world x G CTAs plays every rank (G = min(blocks, co-resident capacity /
+// world)), rank r writing outs.p[r]; `out` is then unused.
 cudaError_t launch_allreduce_oneshot(const PeerBufs &in, int world, void *out, int64_t e0,
                                      int64_t e1, int dtype, bool end_barrier, const Barrier &bar,
-                                     int blocks, cudaStream_t s);
+                                     int blocks, cudaStream_t s, bool emulate = false,
+                                     const PeerBufs *outs = nullptr);
 
 // a2 two-shot.  phase bit 1: reduce-scatter of rank `rank`'s chunk from all
 // `in` buffers into red[rank]; phase bit 2: all-gather of every other
 // rank's chunk from red[p] into red[rank].  With the barrier enabled and
 // both phases: start barrier, RS, mid barrier, AG in one kernel.
 // chunk_start/chunk_end give every rank's element range (within [e0, e1)).
+// emulate = true: one cooperative launch plays every rank (`rank` unused).
 cudaError_t launch_allreduce_twoshot(const PeerBufs &in, const PeerBufs &red, int world, int rank,
                                      const int64_t *chunk_start, const int64_t *chunk_end,
                                      int dtype, int phases, const Barrier &bar, int blocks,
-                                     cudaStream_t s);
+                                     cudaStream_t s, bool emulate = false);
 
 // NEXT-4 sharded update: momentum SGD on the items of the own chunk, also
 // writing w' into the fp32 exchange buffer (packed layout).

@@ -723,16 +723,23 @@ constexpr int kTileVecs = kThreads * kARVec;    // 8 KB tile
 // peer finished reading this call's packed buffers (the pipelined step's
 // last piece needs it: its next pack into the same region is ordered only
 // after this kernel, see step_pipelined).
+// Under emulation (bar.emul_g > 0) the block plays CTA cr.b of rank cr.rank
+// and writes outs.p[cr.rank]; otherwise cr is (blockIdx.x, gridDim.x) and
+// the output is `out`.
 template <int N, int DT>
 __global__ void __launch_bounds__(kThreads) k_oneshot(const __grid_constant__ PeerBufs in,
-                                                      void *__restrict__ out, int64_t v0,
-                                                      int64_t v1, int end_barrier,
+                                                      void *__restrict__ out,
+                                                      const __grid_constant__ PeerBufs outs,
+                                                      int64_t v0, int64_t v1, int end_barrier,
                                                       const __grid_constant__ Barrier bar) {
+    if (emulated_absent(bar)) return;                  // tests: a rank that never arrives
+    const CtaRank cr = cta_rank(bar);
+    if (bar.emul_g > 0) out = const_cast<void *>(outs.p[cr.rank]);
     const uint32_t bv = barrier_value(bar);
     if (!cross_rank_barrier(bar, bv, N, 0)) return;
     if (bar.test_delay_ns) stall_ns(bar.test_delay_ns);   // tests: a slow peer
-    for (int64_t tile = v0 + static_cast<int64_t>(blockIdx.x) * kTileVecs; tile < v1;
-         tile += static_cast<int64_t>(gridDim.x) * kTileVecs) {
+    for (int64_t tile = v0 + static_cast<int64_t>(cr.b) * kTileVecs; tile < v1;
+         tile += static_cast<int64_t>(cr.n) * kTileVecs) {
         uint4 x[kARVec][N];
 #pragma unroll
         for (int u = 0; u < kARVec; ++u) {
@@ -766,13 +773,16 @@ __global__ void __launch_bounds__(kThreads) k_twoshot(const __grid_constant__ Pe
                                                       const __grid_constant__ Chunks ch,
                                                       int phases,
                                                       const __grid_constant__ Barrier bar) {
+    if (emulated_absent(bar)) return;                  // tests: a rank that never arrives
+    const CtaRank cr = cta_rank(bar);
+    if (bar.emul_g > 0) rank = cr.rank;
     const uint32_t bv = barrier_value(bar);
     if (phases & 1) {
         if (!cross_rank_barrier(bar, bv, N, 0)) return;
         const int64_t s = ch.s[rank], e = ch.e[rank];
         uint4 *dst = static_cast<uint4 *>(const_cast<void *>(red.p[rank]));
-        for (int64_t tile = s + static_cast<int64_t>(blockIdx.x) * kTileVecs; tile < e;
-             tile += static_cast<int64_t>(gridDim.x) * kTileVecs) {
+        for (int64_t tile = s + static_cast<int64_t>(cr.b) * kTileVecs; tile < e;
+             tile += static_cast<int64_t>(cr.n) * kTileVecs) {
             uint4 x[kARVec][N];
 #pragma unroll
             for (int u = 0; u < kARVec; ++u) {
@@ -795,8 +805,8 @@ __global__ void __launch_bounds__(kThreads) k_twoshot(const __grid_constant__ Pe
         int64_t maxlen = 0;
 #pragma unroll
         for (int p = 0; p < N; ++p) maxlen = max(maxlen, ch.e[p] - ch.s[p]);
-        for (int64_t tile = static_cast<int64_t>(blockIdx.x) * kTileVecs; tile < maxlen;
-             tile += static_cast<int64_t>(gridDim.x) * kTileVecs) {
+        for (int64_t tile = static_cast<int64_t>(cr.b) * kTileVecs; tile < maxlen;
+             tile += static_cast<int64_t>(cr.n) * kTileVecs) {
             uint4 x[kARVec][N];
 #pragma unroll
             for (int u = 0; u < kARVec; ++u) {
@@ -1287,45 +1297,76 @@ cudaError_t launch_adam_direct(const GradTab &g, const GradTab &wt, int ntab, in
 }
 
 namespace {
+// A barrier kernel's launch: plain (one rank), or -- emulated world, bar
+// enabled with emulate = true -- ONE cooperative launch of world x G blocks
+// playing every rank, G = min(blocks, co-resident capacity / world), so the
+// spinning blocks of different "ranks" are guaranteed to run together.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_barrier_kernel(void (*kernel)(KArgs...), int world, int blocks, bool emulate,
+                                  Barrier bar, cudaStream_t s, Args &&...args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.blockDim = dim3(static_cast<unsigned>(kThreads));
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    if (emulate) {
+        int dev = 0, per_sm = 0, nsm = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0);
+        if (e != cudaSuccess) return e;
+        int g = per_sm * nsm / world;
+        if (g > blocks) g = blocks;
+        if (g < 1) return cudaErrorCooperativeLaunchTooLarge;
+        bar.emul_g = g;
+        cfg.gridDim = dim3(static_cast<unsigned>(world * g));
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    } else {
+        bar.emul_g = 0;
+        cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+        cfg.numAttrs = 0;
+    }
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)..., bar);
+}
+
 template <int N, int DT>
-void oneshot_n(const PeerBufs &in, void *out, int64_t v0, int64_t v1, int end_bar, const Barrier &bar,
-               int blocks, cudaStream_t s) {
-    k_oneshot<N, DT><<<blocks, kThreads, 0, s>>>(in, out, v0, v1, end_bar, bar);
+cudaError_t oneshot_n(const PeerBufs &in, void *out, const PeerBufs &outs, int64_t v0, int64_t v1,
+                      int end_bar, const Barrier &bar, int blocks, bool emulate, cudaStream_t s) {
+    return launch_barrier_kernel(k_oneshot<N, DT>, N, blocks, emulate, bar, s, in, out, outs, v0, v1,
+                                 end_bar);
 }
 template <int N, int DT>
-void twoshot_n(const PeerBufs &in, const PeerBufs &red, int rank, const Chunks &ch, int phases,
-               const Barrier &bar, int blocks, cudaStream_t s) {
-    k_twoshot<N, DT><<<blocks, kThreads, 0, s>>>(in, red, rank, ch, phases, bar);
+cudaError_t twoshot_n(const PeerBufs &in, const PeerBufs &red, int rank, const Chunks &ch, int phases,
+                      const Barrier &bar, int blocks, bool emulate, cudaStream_t s) {
+    return launch_barrier_kernel(k_twoshot<N, DT>, N, blocks, emulate, bar, s, in, red, rank, ch, phases);
 }
 template <int DT>
-bool oneshot_dispatch(int world, const PeerBufs &in, void *out, int64_t v0, int64_t v1,
-                      int end_bar, const Barrier &bar, int blocks, cudaStream_t s) {
+cudaError_t oneshot_dispatch(int world, const PeerBufs &in, void *out, const PeerBufs &outs, int64_t v0,
+                             int64_t v1, int end_bar, const Barrier &bar, int blocks, bool emulate,
+                             cudaStream_t s) {
     switch (world) {
-        case 1: oneshot_n<1, DT>(in, out, v0, v1, end_bar, bar, blocks, s); return true;
-        case 2: oneshot_n<2, DT>(in, out, v0, v1, end_bar, bar, blocks, s); return true;
-        case 3: oneshot_n<3, DT>(in, out, v0, v1, end_bar, bar, blocks, s); return true;
-        case 4: oneshot_n<4, DT>(in, out, v0, v1, end_bar, bar, blocks, s); return true;
-        case 5: oneshot_n<5, DT>(in, out, v0, v1, end_bar, bar, blocks, s); return true;
-        case 6: oneshot_n<6, DT>(in, out, v0, v1, end_bar, bar, blocks, s); return true;
-        case 7: oneshot_n<7, DT>(in, out, v0, v1, end_bar, bar, blocks, s); return true;
-        case 8: oneshot_n<8, DT>(in, out, v0, v1, end_bar, bar, blocks, s); return true;
-        default: return false;
+#define CMN_ONESHOT_CASE(n) \
+        case n: return oneshot_n<n, DT>(in, out, outs, v0, v1, end_bar, bar, blocks, emulate, s);
+        CMN_ONESHOT_CASE(1) CMN_ONESHOT_CASE(2) CMN_ONESHOT_CASE(3) CMN_ONESHOT_CASE(4)
+        CMN_ONESHOT_CASE(5) CMN_ONESHOT_CASE(6) CMN_ONESHOT_CASE(7) CMN_ONESHOT_CASE(8)
+#undef CMN_ONESHOT_CASE
+        default: return cudaErrorInvalidValue;
     }
 }
 template <int DT>
-bool twoshot_dispatch(int world, const PeerBufs &in, const PeerBufs &red, int rank,
-                      const Chunks &ch, int phases, const Barrier &bar, int blocks,
-                      cudaStream_t s) {
+cudaError_t twoshot_dispatch(int world, const PeerBufs &in, const PeerBufs &red, int rank,
+                             const Chunks &ch, int phases, const Barrier &bar, int blocks, bool emulate,
+                             cudaStream_t s) {
     switch (world) {
-        case 1: twoshot_n<1, DT>(in, red, rank, ch, phases, bar, blocks, s); return true;
-        case 2: twoshot_n<2, DT>(in, red, rank, ch, phases, bar, blocks, s); return true;
-        case 3: twoshot_n<3, DT>(in, red, rank, ch, phases, bar, blocks, s); return true;
-        case 4: twoshot_n<4, DT>(in, red, rank, ch, phases, bar, blocks, s); return true;
-        case 5: twoshot_n<5, DT>(in, red, rank, ch, phases, bar, blocks, s); return true;
-        case 6: twoshot_n<6, DT>(in, red, rank, ch, phases, bar, blocks, s); return true;
-        case 7: twoshot_n<7, DT>(in, red, rank, ch, phases, bar, blocks, s); return true;
-        case 8: twoshot_n<8, DT>(in, red, rank, ch, phases, bar, blocks, s); return true;
-        default: return false;
+#define CMN_TWOSHOT_CASE(n) \
+        case n: return twoshot_n<n, DT>(in, red, rank, ch, phases, bar, blocks, emulate, s);
+        CMN_TWOSHOT_CASE(1) CMN_TWOSHOT_CASE(2) CMN_TWOSHOT_CASE(3) CMN_TWOSHOT_CASE(4)
+        CMN_TWOSHOT_CASE(5) CMN_TWOSHOT_CASE(6) CMN_TWOSHOT_CASE(7) CMN_TWOSHOT_CASE(8)
+#undef CMN_TWOSHOT_CASE
+        default: return cudaErrorInvalidValue;
     }
 }
 // elements -> 16-byte units
@@ -1334,31 +1375,35 @@ inline int64_t to_vec(int64_t elems, int dtype) { return dtype == 0 ? elems / 4 
 
 cudaError_t launch_allreduce_oneshot(const PeerBufs &in, int world, void *out, int64_t e0,
                                      int64_t e1, int dtype, bool end_barrier, const Barrier &bar,
-                                     int blocks, cudaStream_t s) {
+                                     int blocks, cudaStream_t s, bool emulate, const PeerBufs *outs) {
     if (blocks <= 0 || blocks > kMaxBarrierBlocks) return cudaErrorInvalidValue;
+    if (emulate && (!outs || !bar.enabled)) return cudaErrorInvalidValue;
     (void)cudaGetLastError();
     const int64_t v0 = to_vec(e0, dtype), v1 = to_vec(e1, dtype);
     const int eb = end_barrier ? 1 : 0;
-    const bool ok = dtype == 0 ? oneshot_dispatch<0>(world, in, out, v0, v1, eb, bar, blocks, s)
-                               : oneshot_dispatch<1>(world, in, out, v0, v1, eb, bar, blocks, s);
-    return ok ? cudaGetLastError() : cudaErrorInvalidValue;
+    const PeerBufs none{};
+    const PeerBufs &o = outs ? *outs : none;
+    const cudaError_t e = dtype == 0 ? oneshot_dispatch<0>(world, in, out, o, v0, v1, eb, bar, blocks, emulate, s)
+                                     : oneshot_dispatch<1>(world, in, out, o, v0, v1, eb, bar, blocks, emulate, s);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_allreduce_twoshot(const PeerBufs &in, const PeerBufs &red, int world, int rank,
                                      const int64_t *chunk_start, const int64_t *chunk_end,
                                      int dtype, int phases, const Barrier &bar, int blocks,
-                                     cudaStream_t s) {
+                                     cudaStream_t s, bool emulate) {
     if (blocks <= 0 || blocks > kMaxBarrierBlocks) return cudaErrorInvalidValue;
+    if (emulate && (!bar.enabled || phases != 3)) return cudaErrorInvalidValue;
     (void)cudaGetLastError();
     Chunks ch{};
     for (int p = 0; p < world; ++p) {
         ch.s[p] = to_vec(chunk_start[p], dtype);
         ch.e[p] = to_vec(chunk_end[p], dtype);
     }
-    const bool ok = dtype == 0
-                        ? twoshot_dispatch<0>(world, in, red, rank, ch, phases, bar, blocks, s)
-                        : twoshot_dispatch<1>(world, in, red, rank, ch, phases, bar, blocks, s);
-    return ok ? cudaGetLastError() : cudaErrorInvalidValue;
+    const cudaError_t e =
+        dtype == 0 ? twoshot_dispatch<0>(world, in, red, rank, ch, phases, bar, blocks, emulate, s)
+                   : twoshot_dispatch<1>(world, in, red, rank, ch, phases, bar, blocks, emulate, s);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_update_chunk(const TensorDesc *td, const Item *items, int i0, int i1,

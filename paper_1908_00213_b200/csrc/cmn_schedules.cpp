@@ -70,7 +70,22 @@ cmn_status reduce_phase_launch(cmn_comm *c, int ta, int tb, int dtype, uint32_t 
         red.p[r] = c->rb[r].reduced[par];
     }
     const int blocks = ar_blocks_for(c);
-    const Barrier bar = make_barrier(c, dtype, algo == CMN_ALGO_TWOSHOT ? kBarTwoshot : kBarOneshot, e0, e1);
+    Barrier bar = make_barrier(c, dtype, algo == CMN_ALGO_TWOSHOT ? kBarTwoshot : kBarOneshot, e0, e1);
+    int64_t cs[kMaxWorld], ce[kMaxWorld];
+    chunk_plan(e0, e1, c->world, cs, ce);
+    if (c->emulated) {
+        // one cooperative launch plays every rank, barriers live
+        bar.enabled = 1;
+        if (algo == CMN_ALGO_ONESHOT)
+            return launched(c,
+                            launch_allreduce_oneshot(in, c->world, nullptr, e0, e1, dtype, end_barrier, bar,
+                                                     blocks, s, true, &red),
+                            "allreduce_oneshot (emulated world)");
+        return launched(c,
+                        launch_allreduce_twoshot(in, red, c->world, 0, cs, ce, dtype, 3, bar, blocks, s,
+                                                 true),
+                        "allreduce_twoshot (emulated world)");
+    }
     if (algo == CMN_ALGO_ONESHOT) {
         for (int i = 0; i < nsim; ++i) {
             const int r = c->simulated ? i : c->rank;
@@ -82,8 +97,6 @@ cmn_status reduce_phase_launch(cmn_comm *c, int ta, int tb, int dtype, uint32_t 
         }
         return CMN_OK;
     }
-    int64_t cs[kMaxWorld], ce[kMaxWorld];
-    chunk_plan(e0, e1, c->world, cs, ce);
     if (c->simulated) {
         for (int phase = 1; phase <= 2; ++phase)
             for (int r = 0; r < c->world; ++r) {

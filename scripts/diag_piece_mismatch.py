@@ -1,8 +1,13 @@
 #!/usr/bin/env python
-"""Diagnostic: two processes on one GPU issue mismatched collectives (rank 0
-one whole-model all-reduce, rank 1 the pipelined step's first piece).
-Prints per-rank timestamps of the call, the synchronize and the status, to
-see which wait (if any) runs into the device timeout."""
+"""Diagnostic: two processes, one GPU each, issue mismatched collectives
+(rank 0 one whole-model all-reduce, rank 1 the pipelined step's first
+piece).  Prints per-rank timestamps of the call, the synchronize and the
+status, to see which wait (if any) runs into the device timeout.
+
+Round 2 ran this with both ranks on one GPU (profiles/r2_diag_piece_mismatch.txt);
+since then ranks whose kernels wait on one another are never time-sliced on
+one GPU (B200_PROFILING.md), so it needs two GPUs.  The same fault is covered
+on one GPU by tests/test_gpu_emulated.py (CMN_TEST_EMUL_MISMATCH_RANK)."""
 import os
 import socket
 import sys
@@ -20,10 +25,10 @@ def worker(rank, port, timeout_ms):
     from paper_1908_00213_b200 import cmn
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    torch.cuda.set_device(0)
+    torch.cuda.set_device(rank)
     dist.init_process_group("gloo", rank=rank, world_size=2)
     shapes = synth.mlp_shapes()
-    comm = cmn.Comm.init(rank, 2, 0, dist.group.WORLD)
+    comm = cmn.Comm.init(rank, 2, rank, dist.group.WORLD)
     comm.set_timeout(timeout_ms)
     w = [torch.from_numpy(p).cuda() for p in synth.params(shapes)]
     comm.register_params(w)
@@ -49,7 +54,10 @@ def worker(rank, port, timeout_ms):
 
 
 if __name__ == "__main__":
+    import torch
     import torch.multiprocessing as mp
+    if torch.cuda.device_count() < 2:
+        raise SystemExit("needs 2 GPUs (ranks are never time-sliced on one GPU)")
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]

@@ -82,7 +82,9 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > torch.cuda.device_count():   # never time-slice barrier ranks on one GPU
+        raise SystemExit(f"{world} ranks need {world} GPUs (B200_PROFILING.md)")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("gloo", rank=rank, world_size=world)

@@ -13,6 +13,21 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: takes more than a few seconds")
 
 
+def require_gpus_for_ranks(world: int):
+    """Ranks whose kernels wait on one another (cross-rank barriers) need a
+    GPU each: run as separate launches on one GPU nothing guarantees they run
+    at the same time (B200_PROFILING.md; 2 and 4 such processes on one B200
+    raised Xid 109).  On a box with fewer GPUs the test is skipped; the same
+    barrier protocol runs on one GPU in tests/test_gpu_emulated.py (one
+    cooperative launch over all ranks), the kernels' arithmetic in the
+    simulated-world parity tests, and the host logic on CPU (gloo)."""
+    import torch
+    n = torch.cuda.device_count()
+    if n < world:
+        pytest.skip(f"{world} ranks with cross-rank barriers need {world} GPUs (this box has {n}); "
+                    "never time-sliced on one GPU")
+
+
 @pytest.fixture(scope="session")
 def orc():
     import oracle

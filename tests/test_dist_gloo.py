@@ -139,3 +139,39 @@ def test_bench_budget_decisions_are_collective(world):
     for p in ps:
         p.join(timeout=60)
     assert all(r[1] == [False, True, False] for r in res), res
+
+
+def _probe_worker(rank, world, port, q):
+    import sys
+    import types
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import bench
+        args = types.SimpleNamespace(dtype="fp32")
+        res, adopted = bench.nvls_probe(args, rank, world, 0, timeout_s=240)
+        q.put((rank, res, adopted))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_nvls_probe_failure_is_contained_and_collective():
+    """bench.py's isolated NVLS probe on a host without a GPU: every rank's
+    child process fails (no CUDA device), the parent ranks survive, report
+    why, and agree collectively not to adopt NVLS (the host side of the
+    probe that shields an N > 1 run from a fault in the multimem kernel)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_probe_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(2)], key=lambda r: r[0])
+    for p in ps:
+        p.join(timeout=60)
+    for rank, r, adopted in res:
+        assert adopted is False
+        assert r["probe"].startswith("child process") and "unavailable" in r and r["probe_s"] > 0

@@ -269,10 +269,13 @@ def _mno_worker(rank, world, port, q, depths, bucket_bytes, dtype):
     from paper_1908_00213_b200.optim import MultiNodeOptimizer
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    global DEV
     try:
-        torch.cuda.set_device(0)
+        dev = rank % torch.cuda.device_count()          # one GPU per rank
+        DEV = f"cuda:{dev}"
+        torch.cuda.set_device(dev)
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        comm = cm.Comm.init(rank, world, 0, dist.group.WORLD)
+        comm = cm.Comm.init(rank, world, dev, dist.group.WORLD)
         comm.set_timeout(60000)
         models = {d: mlp(d, seed=40 + d) for d in sorted(set(depths))}   # same init on every rank
         opt = None
@@ -307,7 +310,7 @@ def _mno_worker(rank, world, port, q, depths, bucket_bytes, dtype):
 @pytest.mark.parametrize("world,bucket_bytes,dtype", [(2, None, "fp32"), (3, None, "fp16"),
                                                       (2, 64 << 10, "fp32")])
 def test_multi_node_optimizer_processes_oracle_parity(cmn, orc, world, bucket_bytes, dtype):
-    """MultiNodeOptimizer across 2-3 real processes (CUDA-IPC barriers live),
+    """MultiNodeOptimizer across 2-3 real processes, one per GPU (CUDA-IPC barriers live),
     each rank backpropagating its own batch, the model's depth changing
     3 -> 3 -> 4 -> 4 -> 3 on every rank in the same iterations (PAPER.md:
     493-501, Define-by-Run; each change is a collective re-registration
@@ -316,11 +319,14 @@ def test_multi_node_optimizer_processes_oracle_parity(cmn, orc, world, bucket_by
     produced: per iteration oracle.step over the N ranks' gradients of the
     registered model, v zeroed at each re-registration.  Every rank's final
     parameters of both models and its momentum must equal the oracle's
-    bitwise."""
+    bitwise.  One GPU per rank (conftest.require_gpus_for_ranks)."""
     import socket
 
     import numpy as np
     import torch.multiprocessing as mp
+
+    from conftest import require_gpus_for_ranks
+    require_gpus_for_ranks(world)
     depths = [3, 3, 4, 4, 3]
     s = socket.socket()
     s.bind(("127.0.0.1", 0))

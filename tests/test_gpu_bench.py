@@ -1,8 +1,10 @@
-"""bench.py's driver contract on the GPU: N = 1 directly and N = 2 under
-torchrun (both ranks on the one test GPU): exactly one JSON line on stdout
-with the contract's keys, a positive kernel count, a roofline of the
-dominant kernel, the e2e number with its byte counts, clocks, and at N = 2
-the replicas bitwise equal after the timed steps."""
+"""bench.py's driver contract on the GPU: N = 1 directly, and N = 2 / 8
+under torchrun with one GPU per rank (skipped on a box with fewer GPUs:
+ranks whose kernels spin on each other's flags are never time-sliced on one
+GPU, B200_PROFILING.md): exactly one JSON line on stdout with the
+contract's keys, a positive kernel count, a roofline of the dominant
+kernel, the e2e number with its byte counts, clocks, and at N > 1 the
+replicas bitwise equal after the timed steps."""
 import json
 import os
 import socket
@@ -10,6 +12,7 @@ import subprocess
 import sys
 
 import pytest
+from conftest import require_gpus_for_ranks
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
@@ -59,6 +62,7 @@ def test_bench_n1_contract():
 
 
 def test_bench_n2_torchrun_contract():
+    require_gpus_for_ranks(2)
     p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                         "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
                         str(_free_port()), "bench.py", "--gpus", "2", "--steps", "4", "--warmup", "3",
@@ -90,6 +94,10 @@ def _check_n_gt_1(d, n):
     assert c["cmn"]["allreduce_incl_pack_us"] > 0 and c["cmn"]["allreduce_incl_pack_bus_gbs"] > 0
     for alt in ("nccl", "nvls"):          # measured, or why not (one GPU: NCCL refuses 2 ranks)
         assert "unavailable" in c[alt] or c[alt]["allreduce_incl_pack_us"] > 0
+    # NVLS was first tried in isolated child processes (one GPU: multicast refused)
+    pr = c["nvls"]["probe"]
+    assert pr["probe"].startswith("child process") and pr["probe_s"] > 0
+    assert "unavailable" in pr or pr.get("passed") is not None
     assert d["details"]["schedule_trials_us"]
     assert d["details"]["tune_budget_s"] is not None
     sw = d["details"]["config5_sweep"]          # BASELINE config 5, budget-bounded
@@ -97,10 +105,67 @@ def _check_n_gt_1(d, n):
     assert all("nccl_us" in x or "nccl" in x for x in sw)
 
 
-def test_bench_n8_timesliced_contract():
-    """8 ranks time-sliced on the one test GPU (what a SCALE run at N = 8
-    executes, minus the NVLink): the line carries the same N > 1 fields; a
-    2 s autotune budget keeps it bounded."""
+def test_bench_nvls_probe_plumbing():
+    """The isolated NVLS probe's machinery (child processes with their own
+    process group and CUDA context, the tolerance gate against the tree sums,
+    the timings, the replica check, the collective verdict), driven with the
+    two-shot P2P all-reduce standing in for the multimem kernel: every child
+    passes, and because the algorithm was not NVLS the parent does not
+    adopt it."""
+    require_gpus_for_ranks(2)
+    env = dict(os.environ, CMN_TEST_NVLS_PROBE_ALGO="twoshot")
+    p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
+                        str(_free_port()), "bench.py", "--gpus", "2", "--steps", "4", "--warmup", "3",
+                        "--min-warmup-s", "0", "--tune-budget-s", "1", "--sweep-budget-s", "0",
+                        "--no-e2e"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=1200, env=env)
+    tb = p.stderr.find("Traceback")
+    assert p.returncode == 0, p.stderr[tb: tb + 3000] if tb >= 0 else p.stderr[-3000:]
+    d = json.loads(p.stdout.strip().splitlines()[-1])
+    nv = d["details"]["comparisons"]["nvls"]
+    pr = nv["probe"]
+    assert pr["algo"] == "twoshot" and pr["passed"] is True, pr
+    assert pr["tolerance_ratio_vs_tree"] == 0.0          # the same algorithm: identical sums
+    assert pr["replicas_bitwise_equal"] is True
+    for k in ("allreduce_incl_pack_us", "serial_step_us", "pipelined4_step_us"):
+        assert pr[k] > 0
+    assert "unavailable" in nv                            # not adopted: not the NVLS algorithm
+    assert not d["details"]["schedule"].startswith("nvls")
+
+
+@pytest.mark.parametrize("algo", ["twoshot", "nvls"])
+def test_bench_nvls_child_single_rank(algo):
+    """The NVLS probe's child process (bench.py --nvls-child) on its own, one
+    rank on the one GPU (no cross-rank waiting): with the two-shot kernel
+    standing in it sets up, passes the tolerance gate (identical sums),
+    times the all-reduce and both step schedules and checks the replica;
+    with the real NVLS algorithm it reports why multicast is unavailable
+    (the one-GPU boxes refuse multicast objects) -- either way exactly one
+    JSON object on stdout and exit code 0."""
+    env = dict(os.environ, RANK="0", WORLD_SIZE="1", LOCAL_RANK="0",
+               CMN_NVLS_CHILD_INIT=f"tcp://127.0.0.1:{_free_port()}")
+    if algo != "nvls":
+        env["CMN_TEST_NVLS_PROBE_ALGO"] = algo
+    p = subprocess.run([sys.executable, "bench.py", "--nvls-child", "--dtype", "fp32", "--gpus", "1"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600, env=env)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [x for x in p.stdout.splitlines() if x.strip()]
+    assert len(lines) == 1, p.stdout
+    r = json.loads(lines[0])
+    assert r["probe"].startswith("child process") and r["algo"] == algo
+    if algo == "nvls":
+        assert "unavailable" in r or r.get("passed") is True, r
+    else:
+        assert r["passed"] is True and r["tolerance_ratio_vs_tree"] == 0.0, r
+        assert r["replicas_bitwise_equal"] is True
+        assert all(r[k] > 0 for k in ("allreduce_incl_pack_us", "serial_step_us", "pipelined4_step_us"))
+
+
+def test_bench_n8_contract():
+    """8 ranks, one GPU each (what a SCALE run at N = 8 executes): the line
+    carries the same N > 1 fields; a 2 s autotune budget keeps it bounded."""
+    require_gpus_for_ranks(8)
     p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                         "--nproc-per-node", "8", "--master-addr", "127.0.0.1", "--master-port",
                         str(_free_port()), "bench.py", "--gpus", "8", "--steps", "4", "--warmup", "3",

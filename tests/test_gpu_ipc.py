@@ -1,10 +1,15 @@
 """The real multi-process path (cmn_init: CUDA-IPC peer mapping, per-CTA
-release/acquire barriers across processes) with 2 and 3 ranks sharing one
-GPU (the only configuration gpurun offers): each process owns its buffers,
-peers read them through IPC mappings exactly as over NVSwitch.  Results are
-compared bit-exact with the oracle and across ranks (replica consistency,
-SPEC.md:608).  Contexts time-slice on one device, so barriers are slow but
-correct; every spin is bounded by the device timeout."""
+release/acquire barriers across processes), one process per GPU: rank r on
+device r.  Each process owns its buffers, peers read them through IPC
+mappings over NVSwitch.  Results are compared bit-exact with the oracle and
+across ranks (replica consistency); every spin is bounded by the
+device timeout.
+
+These tests need one GPU per rank (conftest.require_gpus_for_ranks): ranks
+whose kernels spin on each other's flags must never be separate launches on
+one GPU (B200_PROFILING.md).  On a one-GPU box they skip; the barrier
+protocol is then covered by tests/test_gpu_emulated.py (all ranks in one
+cooperative launch, barriers live)."""
 import os
 import socket
 
@@ -37,7 +42,8 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode, pieces=0):
         # start barrier, so rank 0 races ahead into its next step
         os.environ["CMN_TEST_ONESHOT_DELAY_US"] = "20000"
     try:
-        torch.cuda.set_device(0)
+        dev = rank % torch.cuda.device_count()          # one GPU per rank
+        torch.cuda.set_device(dev)
         dist.init_process_group("gloo", rank=rank, world_size=world)
         shapes = synth.mlp_shapes()
         digest = mode.startswith("r50:")          # full ResNet-50 set: return hashes
@@ -45,7 +51,7 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode, pieces=0):
             shapes, mode = synth.resnet50_shapes(), mode[4:]
         if mode == "mismatch" and rank == 1:
             shapes = shapes[:-1] + [(11,)]
-        comm = cmn.Comm.init(rank, world, 0, dist.group.WORLD)
+        comm = cmn.Comm.init(rank, world, dev, dist.group.WORLD)
         comm.set_timeout(3000 if mode == "skip" else 60000)
         w = [torch.from_numpy(p).cuda() for p in synth.params(shapes)]
         try:
@@ -191,6 +197,8 @@ def _worker(rank, world, port, dtype, algo, steps, q, mode, pieces=0):
 
 
 def _run(world, dtype, algo, steps=2, mode="same", pieces=0):
+    from conftest import require_gpus_for_ranks
+    require_gpus_for_ranks(world)
     from paper_1908_00213_b200 import build
     build.build()
     ctx = mp.get_context("spawn")
