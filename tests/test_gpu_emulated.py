@@ -228,3 +228,45 @@ def test_emulated_fault_leaves_state_untouched(cmn, monkeypatch, fault, code, al
             comm.poll_error()
     finally:
         comm.finalize()
+
+
+def test_emulated_reregistration_structure_changes(cmn, orc):
+    """Define-by-Run at N > 1 ("model structure can be
+    changed at any iteration dynamically"): the registered structure changes
+    between iterations (MLP depth 3 -> 3 -> 4 -> 4 -> 3, each model keeping
+    its own parameters), every change a re-registration that re-plans the
+    layout and resets momentum (reading R7); 4 emulated ranks with the
+    barriers live across re-registrations.  Each model's parameters and the
+    final momentum bit-exact vs the oracle replaying the same sequence."""
+    def shapes_of(depth):
+        dims = [784] + [100] * (depth - 1) + [10]
+        out = []
+        for i in range(depth):
+            out += [(dims[i + 1], dims[i]), (dims[i + 1],)]
+        return out
+
+    N, lr, mu, depths = 4, 0.05, 0.9, [3, 3, 4, 4, 3]
+    models = {d: synth.params(shapes_of(d), seed=40 + d) for d in sorted(set(depths))}
+    dev_w = {d: [torch.from_numpy(p.copy()).to(DEV) for p in models[d]] for d in models}
+    w_o = {d: [p.copy() for p in models[d]] for d in models}
+    comm = cmn.Comm.emulated_world(N)
+    try:
+        comm.set_algo("twoshot")
+        cur, v_o = None, None
+        for it, d in enumerate(depths):
+            shapes = shapes_of(d)
+            if d != cur:
+                comm.register_params(dev_w[d])
+                v_o = [np.zeros_like(x) for x in w_o[d]]
+                cur = d
+            comm.step(_dev_grads(shapes, N, it), "fp32", lr, mu)
+            orc.step(synth.grads(shapes, workers=N, step=it), w_o[d], v_o, lr, mu, "fp32")
+        torch.cuda.synchronize()
+        comm.poll_error()
+        for d in models:
+            for t in range(len(models[d])):
+                _same(dev_w[d][t].cpu().numpy().reshape(-1), w_o[d][t], f"depth {d} w[{t}]")
+        for t in range(len(v_o)):
+            _same(comm.momentum(t).cpu().numpy().reshape(-1), v_o[t], f"v[{t}]")
+    finally:
+        comm.finalize()
