@@ -28,6 +28,28 @@ def require_gpus_for_ranks(world: int):
                     "never time-sliced on one GPU")
 
 
+@pytest.fixture(scope="module", params=["simulated", "emulated"])
+def cmn_worlds(request):
+    """The binding module, once per single-GPU world kind.  In the
+    "emulated" pass Comm.simulated_world builds cmn_init_emulated worlds, so
+    every simulated-N test runs a second time with the one-/two-shot
+    all-reduces as ONE cooperative launch over all ranks and the cross-rank
+    barriers live (the schedules that have no emulated form -- fused pull /
+    push, sharded -- behave as in the simulated world)."""
+    from paper_1908_00213_b200 import build
+    build.build()
+    from paper_1908_00213_b200 import cmn as m
+    if request.param == "simulated":
+        yield m
+        return
+    saved = m.Comm.__dict__["simulated_world"]
+    m.Comm.simulated_world = m.Comm.__dict__["emulated_world"]
+    try:
+        yield m
+    finally:
+        m.Comm.simulated_world = saved
+
+
 @pytest.fixture(scope="session")
 def orc():
     import oracle

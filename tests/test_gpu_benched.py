@@ -27,11 +27,10 @@ DEV = "cuda:0"
 
 
 @pytest.fixture(scope="module")
-def cmn():
-    from paper_1908_00213_b200 import build
-    build.build()
-    from paper_1908_00213_b200 import cmn as m
-    return m
+def cmn(cmn_worlds):
+    """Every test here runs in the simulated and in the emulated world
+    (conftest.cmn_worlds: barriers live in one cooperative launch)."""
+    return cmn_worlds
 
 
 def _nan_aware_equal(got: np.ndarray, want: np.ndarray, what: str):
