@@ -36,7 +36,12 @@ def main():
     ap.add_argument("--worlds", default="2,4,8")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--algos", default="twoshot,oneshot")
+    ap.add_argument("--sweep", action="store_true",
+                    help="config-5 sizes instead of R50: one flat fp32 tensor of 64 KB .. 256 MB, "
+                         "pack + all-reduce per call (latency floor of the barrier kernels)")
     args = ap.parse_args()
+    if args.sweep:
+        return sweep(args)
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
     shapes = synth.resnet50_shapes()
     params0 = synth.params(shapes)
@@ -74,6 +79,44 @@ def main():
                     comm.finalize()
         del g
         torch.cuda.empty_cache()
+
+
+def sweep(args):
+    """Per-call device time of cmn_allreduce_grads (all ranks' packs + the
+    one cooperative all-reduce launch) on one flat fp32 tensor per rank, S
+    from 64 KB to 256 MB: at small S this is the latency floor of the
+    barrier kernels without NVLink (launches + flag round trips through the
+    one L2)."""
+    dev = "cuda:0"
+    stream = torch.cuda.current_stream()
+    for N in [int(x) for x in args.worlds.split(",")]:
+        for S in (64 << 10, 1 << 20, 16 << 20, 256 << 20):
+            n = S // 4
+            g = [torch.empty(n, device=dev).uniform_(-1e-2, 1e-2) for _ in range(N)]
+            for algo in args.algos.split(","):
+                comm = Comm.emulated_world(N)
+                try:
+                    w = torch.zeros(n, device=dev)
+                    comm.register_params([w])
+                    comm.set_algo(algo)
+                    table = comm.prepare(g)
+                    for _ in range(5):
+                        comm.allreduce_grads(table, "fp32")
+                    torch.cuda.synchronize()
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    for _ in range(args.iters):
+                        comm.allreduce_grads(table, "fp32")
+                    b.record(stream)
+                    torch.cuda.synchronize()
+                    comm.poll_error()
+                    print(json.dumps({"what": "emulated pack + all-reduce per call (barriers live), flat fp32",
+                                      "N": N, "bytes": S, "algo": algo,
+                                      "us_per_call": a.elapsed_time(b) / args.iters * 1e3}), flush=True)
+                finally:
+                    comm.finalize()
+            del g
+    torch.cuda.empty_cache()
 
 
 if __name__ == "__main__":
