@@ -171,7 +171,10 @@ cmn_status cmn_init_simulated(int world_size, int cuda_device, cmn_comm **out);
  * The other collectives (fused pull / push, sharded, NVLS, NCCL) behave as in
  * cmn_init_simulated.  Test mode; fault injection through the environment:
  * CMN_TEST_EMUL_ABSENT_RANK=r (rank r's blocks never arrive: the others time
- * out), CMN_TEST_EMUL_MISMATCH_RANK=r (rank r posts another call tag).
+ * out), CMN_TEST_EMUL_MISMATCH_RANK=r (rank r posts another call tag),
+ * CMN_TEST_EMUL_SLOW_RANK=r with CMN_TEST_ONESHOT_DELAY_US=t (rank r's blocks
+ * stall t us after the start barrier), CMN_TEST_EMUL_SKIP_MID=1 (negative
+ * control: the two-shot skips its mid barrier).
  * Errors: as cmn_init_simulated. */
 cmn_status cmn_init_emulated(int world_size, int cuda_device, cmn_comm **out);
 

@@ -43,6 +43,8 @@ cmn_status cmn_init_emulated(int world_size, int cuda_device, cmn_comm **out) {
         };
         c->test_absent_rank = env_rank("CMN_TEST_EMUL_ABSENT_RANK");
         c->test_mismatch_rank = env_rank("CMN_TEST_EMUL_MISMATCH_RANK");
+        c->test_slow_rank = env_rank("CMN_TEST_EMUL_SLOW_RANK");
+        c->test_skip_mid = env_size("CMN_TEST_EMUL_SKIP_MID", 0) != 0 ? 1 : 0;
         return CMN_OK;
     } catch (...) {
         return fail(CMN_ERR_OOM, "host allocation failed");

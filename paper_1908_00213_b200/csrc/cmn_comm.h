@@ -98,6 +98,8 @@ struct cmn_comm {
     bool emulated = false;
     int test_absent_rank = -1;     // CMN_TEST_EMUL_ABSENT_RANK (emulation fault injection)
     int test_mismatch_rank = -1;   // CMN_TEST_EMUL_MISMATCH_RANK
+    int test_slow_rank = -1;       // CMN_TEST_EMUL_SLOW_RANK (with CMN_TEST_ONESHOT_DELAY_US)
+    int test_skip_mid = 0;         // CMN_TEST_EMUL_SKIP_MID (negative control)
     cmn_allgather_fn ag = nullptr;
     void *user = nullptr;
     int nsm = 148;

@@ -284,6 +284,8 @@ Barrier make_barrier(cmn_comm *c, int dtype, BarrierKind kind, int64_t e0, int64
     for (int r = 0; r < c->world; ++r) b.epochs[r] = c->rb[r].epoch;
     b.test_absent_rank = c->emulated ? c->test_absent_rank : -1;
     b.test_mismatch_rank = c->emulated ? c->test_mismatch_rank : -1;
+    b.test_slow_rank = c->emulated ? c->test_slow_rank : -1;
+    b.test_skip_mid = c->emulated ? c->test_skip_mid : 0;
     return b;
 }
 

@@ -153,6 +153,21 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ uint32_t ld_relaxed_sys(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+
+// Barrier memory-ordering variant (measurement switch CMN_BARRIER_VARIANT):
+//   0: __threadfence_system, st.release.sys, spin on ld.acquire.sys
+//   1: st.release.sys, spin on ld.acquire.sys
+//   2: st.release.sys, spin on ld.relaxed.sys, one fence.acq_rel.sys after
+#ifndef CMN_BARRIER_VARIANT
+#define CMN_BARRIER_VARIANT 0
+#endif
+
 __device__ __forceinline__ uint64_t global_timer_ns() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -224,6 +239,14 @@ __device__ __forceinline__ uint32_t barrier_value(const Barrier &bar) {
     return s_val;
 }
 
+// Fault injection (tests only): a slow peer.  Every CTA of this rank on a
+// real rank; under emulation only the blocks of bar.test_slow_rank (or all
+// of them when it is -1).
+__device__ __forceinline__ void test_stall(const Barrier &bar, const CtaRank &cr) {
+    if (bar.test_delay_ns && (bar.emul_g == 0 || bar.test_slow_rank < 0 || cr.rank == bar.test_slow_rank))
+        stall_ns(bar.test_delay_ns);
+}
+
 // Emulation fault injection: the CTAs of bar.test_absent_rank never arrive
 // (they return before touching anything), so their peers' barriers time out.
 __device__ __forceinline__ bool emulated_absent(const Barrier &bar) {
@@ -269,12 +292,18 @@ __device__ __forceinline__ bool cross_rank_barrier(const Barrier &bar, uint32_t 
     int bad = 0;
     if (tid < world) {
         const size_t cell = (static_cast<size_t>(slot) * kMaxBarrierBlocks + cr.b) * kMaxWorld;
+#if CMN_BARRIER_VARIANT == 0
         __threadfence_system();
+#endif
         st_release_sys(bar.flags[tid] + cell + cr.rank, value);
         const uint32_t *mine = bar.flags[cr.rank] + cell + tid;
         uint64_t t0 = 0;
         for (uint32_t spin = 1;; ++spin) {
+#if CMN_BARRIER_VARIANT == 2
+            const uint32_t v = ld_relaxed_sys(mine);
+#else
             const uint32_t v = ld_acquire_sys(mine);
+#endif
             if ((v & kTagMask) == kDeadTag) {   // the peer's communicator failed earlier
                 record_failure(bar, 3);
                 bad = 1;
@@ -285,7 +314,12 @@ __device__ __forceinline__ bool cross_rank_barrier(const Barrier &bar, uint32_t 
                 bad = 1;
                 break;
             }
-            if (static_cast<int32_t>(v - value) >= 0) break;
+            if (static_cast<int32_t>(v - value) >= 0) {
+#if CMN_BARRIER_VARIANT == 2
+                fence_acq_rel_sys();   // acquire: the peer's release store was observed
+#endif
+                break;
+            }
             if ((spin & 63u) == 0 && comm_failed(bar.derr)) {   // failed elsewhere: stop waiting
                 bad = 1;
                 break;

@@ -82,7 +82,7 @@ struct Barrier {
     int *derr;          // the same code in device memory, read by every later
                         // kernel of the communicator (comm_failed) to skip its stores
     uint32_t test_delay_ns;   // fault injection (tests only, CMN_TEST_ONESHOT_DELAY_US):
-                              // one-shot CTAs stall this long after the start barrier
+                              // one-shot / two-shot CTAs stall this long after the start barrier
     // Emulated world (cmn_init_emulated): one COOPERATIVE launch plays every
     // rank -- CTA b of rank r is blockIdx.x = r * emul_g + b, all co-resident
     // by construction -- so the cross-rank barrier runs for real on one GPU
@@ -91,6 +91,8 @@ struct Barrier {
     uint32_t *epochs[kMaxWorld];   // emulation: every rank's per-CTA epoch counters
     int test_absent_rank;     // emulation fault injection: this rank's CTAs never arrive (-1: none)
     int test_mismatch_rank;   // emulation fault injection: this rank posts another call tag (-1: none)
+    int test_slow_rank;       // emulation: only this rank's blocks take test_delay_ns (-1: every block)
+    int test_skip_mid;        // emulation negative control: two-shot skips its mid barrier
 };
 
 // Peer buffer table (packed or reduced) in 16-byte units.

@@ -737,7 +737,7 @@ __global__ void __launch_bounds__(kThreads) k_oneshot(const __grid_constant__ Pe
     if (bar.emul_g > 0) out = const_cast<void *>(outs.p[cr.rank]);
     const uint32_t bv = barrier_value(bar);
     if (!cross_rank_barrier(bar, bv, N, 0)) return;
-    if (bar.test_delay_ns) stall_ns(bar.test_delay_ns);   // tests: a slow peer
+    test_stall(bar, cr);                                   // tests: a slow peer
     for (int64_t tile = v0 + static_cast<int64_t>(cr.b) * kTileVecs; tile < v1;
          tile += static_cast<int64_t>(cr.n) * kTileVecs) {
         uint4 x[kARVec][N];
@@ -779,6 +779,7 @@ __global__ void __launch_bounds__(kThreads) k_twoshot(const __grid_constant__ Pe
     const uint32_t bv = barrier_value(bar);
     if (phases & 1) {
         if (!cross_rank_barrier(bar, bv, N, 0)) return;
+        test_stall(bar, cr);                               // tests: a slow peer
         const int64_t s = ch.s[rank], e = ch.e[rank];
         uint4 *dst = static_cast<uint4 *>(const_cast<void *>(red.p[rank]));
         for (int64_t tile = s + static_cast<int64_t>(cr.b) * kTileVecs; tile < e;
@@ -800,7 +801,9 @@ __global__ void __launch_bounds__(kThreads) k_twoshot(const __grid_constant__ Pe
         }
     }
     if (phases & 2) {
-        if (!cross_rank_barrier(bar, bv, N, 1)) return;
+        // the mid barrier: every rank's chunk is reduced before any rank
+        // gathers it (skipped only by the emulated negative-control test)
+        if (!(bar.emul_g > 0 && bar.test_skip_mid) && !cross_rank_barrier(bar, bv, N, 1)) return;
         uint4 *dst = static_cast<uint4 *>(const_cast<void *>(red.p[rank]));
         int64_t maxlen = 0;
 #pragma unroll

@@ -109,10 +109,27 @@ def sweep(args):
                         comm.allreduce_grads(table, "fp32")
                     b.record(stream)
                     torch.cuda.synchronize()
+                    eager_us = a.elapsed_time(b) / args.iters * 1e3
+                    # the same call captured once into a CUDA graph and
+                    # replayed: no host submission cost between calls, so
+                    # small sizes show the device-side floor
+                    graph = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(graph):
+                        comm.allreduce_grads(table, "fp32")
+                    for _ in range(3):
+                        graph.replay()
+                    torch.cuda.synchronize()
+                    a.record(stream)
+                    for _ in range(args.iters):
+                        graph.replay()
+                    b.record(stream)
+                    torch.cuda.synchronize()
                     comm.poll_error()
                     print(json.dumps({"what": "emulated pack + all-reduce per call (barriers live), flat fp32",
-                                      "N": N, "bytes": S, "algo": algo,
-                                      "us_per_call": a.elapsed_time(b) / args.iters * 1e3}), flush=True)
+                                      "N": N, "bytes": S, "algo": algo, "us_per_call": eager_us,
+                                      "us_per_call_graph": a.elapsed_time(b) / args.iters * 1e3}),
+                          flush=True)
+                    del graph
                 finally:
                     comm.finalize()
             del g

@@ -270,3 +270,60 @@ def test_emulated_reregistration_structure_changes(cmn, orc):
             _same(comm.momentum(t).cpu().numpy().reshape(-1), v_o[t], f"v[{t}]")
     finally:
         comm.finalize()
+
+
+def _run_twoshot_steps(cmn, shapes, N, steps):
+    """Every rank's reduced buffer (float32 values) after each of `steps`
+    two-shot all-reduces in the emulated world; w, v after the last step."""
+    comm = _emulated(cmn, N, "twoshot")
+    try:
+        w = [torch.from_numpy(p).to(DEV) for p in synth.params(shapes)]
+        comm.register_params(w)
+        L = comm.layout()[1]
+        red = []
+        for k in range(steps):
+            comm.allreduce_grads(_dev_grads(shapes, N, k), "fp32")
+            per = []
+            for r in range(N):
+                q = torch.empty(L, dtype=torch.float32, device=DEV)
+                comm.copy_reduced(r, q)
+                per.append(q)
+            comm.update_momentum_sgd(0.1, 0.9)
+            torch.cuda.synchronize()
+            red.append([q.cpu().numpy() for q in per])
+        comm.poll_error()
+        return red
+    finally:
+        comm.finalize()
+
+
+def test_emulated_slow_rank_mid_barrier(cmn, orc, monkeypatch):
+    """Rank 3's blocks stall 2 ms after the start barrier, before reducing
+    their chunk: every other rank finishes its reduce-scatter and must wait
+    at the two-shot mid barrier for rank 3's chunk before gathering it.
+    Every rank's reduced buffer stays bit-exact over 3 steps."""
+    monkeypatch.setenv("CMN_TEST_EMUL_SLOW_RANK", "3")
+    monkeypatch.setenv("CMN_TEST_ONESHOT_DELAY_US", "2000")
+    shapes, N = RAGGED, 4
+    want, _ = _oracle_steps(orc, shapes, N, "fp32", 3, 0.1, 0.9)
+    got = _run_twoshot_steps(cmn, shapes, N, 3)
+    for k in range(3):
+        for r in range(N):
+            _same(got[k][r], want[k]["reduced"], f"step {k} rank {r}")
+
+
+def test_emulated_negative_control_without_mid_barrier(cmn, orc, monkeypatch):
+    """The same slow rank with the mid barrier compiled out of the call
+    (CMN_TEST_EMUL_SKIP_MID): the other ranks gather rank 3's chunk before
+    rank 3 has reduced it and end up with a wrong sum -- the emulated world
+    does expose a missing cross-rank ordering (the test above is not
+    vacuous)."""
+    monkeypatch.setenv("CMN_TEST_EMUL_SLOW_RANK", "3")
+    monkeypatch.setenv("CMN_TEST_ONESHOT_DELAY_US", "2000")
+    monkeypatch.setenv("CMN_TEST_EMUL_SKIP_MID", "1")
+    shapes, N = RAGGED, 4
+    want, _ = _oracle_steps(orc, shapes, N, "fp32", 3, 0.1, 0.9)
+    got = _run_twoshot_steps(cmn, shapes, N, 3)
+    bad = sum(int(np.count_nonzero(_u32(got[k][r]) != _u32(want[k]["reduced"])))
+              for k in range(3) for r in range(N))
+    assert bad > 0, "without the mid barrier the gathered chunks should be stale"
