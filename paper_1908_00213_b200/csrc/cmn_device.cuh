@@ -159,13 +159,28 @@ __device__ __forceinline__ uint32_t ld_relaxed_sys(const uint32_t *p) {
     return v;
 }
 __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ void st_relaxed_sys(uint32_t *p, uint32_t v) {
+    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
-// Barrier memory-ordering variant (measurement switch CMN_BARRIER_VARIANT):
-//   0: __threadfence_system, st.release.sys, spin on ld.acquire.sys
-//   1: st.release.sys, spin on ld.acquire.sys
-//   2: st.release.sys, spin on ld.relaxed.sys, one fence.acq_rel.sys after
+// Barrier memory ordering (CMN_BARRIER_VARIANT; 3 is the default since
+// round 2, session 3, the others stay as measurement switches):
+//   0: every polling thread: __threadfence_system, st.release.sys, spin on
+//      ld.acquire.sys (the round-1/2 form: TWO MEMBAR.SYS per flag)
+//   1: every polling thread: st.release.sys, spin on ld.acquire.sys
+//   3: thread 0: ONE fence.acq_rel.sys for the CTA, then every peer's flag
+//      as st.relaxed.sys (release pattern: fence + strong store, same
+//      thread; bar.sync before it ordered every thread's writes); the
+//      polling threads spin on ld.acquire.sys
+//   4: as 3, but spin on ld.relaxed.sys and take one ld.acquire.sys of the
+//      cell once it is satisfied
+// Measured in the emulated world (profiles/r2s3_barrier_ab*.jsonl, tiny
+// all-reduce, graph replay): a system-scope fence costs ~6-8 us here; 0 ->
+// 3 takes the N = 2 two-shot from 36 to 20.5 us per call (7.8 us with
+// gpu-scope fences, which are not valid across GPUs), the R50 N = 8 fp32
+// two-shot from 385 to 370 us.  1, 3 and 4 are within 0.5 us of each other.
 #ifndef CMN_BARRIER_VARIANT
-#define CMN_BARRIER_VARIANT 0
+#define CMN_BARRIER_VARIANT 3
 #endif
 
 __device__ __forceinline__ uint64_t global_timer_ns() {
@@ -290,19 +305,29 @@ __device__ __forceinline__ bool cross_rank_barrier(const Barrier &bar, uint32_t 
     }
     __syncthreads();
     int bad = 0;
+    const size_t cell = (static_cast<size_t>(slot) * kMaxBarrierBlocks + cr.b) * kMaxWorld;
+#if CMN_BARRIER_VARIANT >= 3
+    if (tid == 0) {
+        // release: one fence for the whole CTA (bar.sync above ordered every
+        // thread's writes before it), then the flags as plain strong stores
+        fence_acq_rel_sys();
+        for (int p = 0; p < world; ++p) st_relaxed_sys(bar.flags[p] + cell + cr.rank, value);
+    }
+#endif
     if (tid < world) {
-        const size_t cell = (static_cast<size_t>(slot) * kMaxBarrierBlocks + cr.b) * kMaxWorld;
 #if CMN_BARRIER_VARIANT == 0
         __threadfence_system();
 #endif
+#if CMN_BARRIER_VARIANT < 3
         st_release_sys(bar.flags[tid] + cell + cr.rank, value);
+#endif
         const uint32_t *mine = bar.flags[cr.rank] + cell + tid;
         uint64_t t0 = 0;
         for (uint32_t spin = 1;; ++spin) {
-#if CMN_BARRIER_VARIANT == 2
-            const uint32_t v = ld_relaxed_sys(mine);
+#if CMN_BARRIER_VARIANT == 4
+            uint32_t v = ld_relaxed_sys(mine);
 #else
-            const uint32_t v = ld_acquire_sys(mine);
+            uint32_t v = ld_acquire_sys(mine);
 #endif
             if ((v & kTagMask) == kDeadTag) {   // the peer's communicator failed earlier
                 record_failure(bar, 3);
@@ -315,8 +340,9 @@ __device__ __forceinline__ bool cross_rank_barrier(const Barrier &bar, uint32_t 
                 break;
             }
             if (static_cast<int32_t>(v - value) >= 0) {
-#if CMN_BARRIER_VARIANT == 2
-                fence_acq_rel_sys();   // acquire: the peer's release store was observed
+#if CMN_BARRIER_VARIANT == 4
+                v = ld_acquire_sys(mine);   // acquire: synchronises with the peer's release
+                (void)v;
 #endif
                 break;
             }

@@ -6,8 +6,8 @@
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
 O=gpurun_out
-rm -f $O/barrier_ab.jsonl
-for rep in 1 2; do for v in 0 1 2; do
+rm -f $O/barrier_ab.jsonl $O/barrier_ab_ncu_v*.csv
+for rep in 1 2; do for v in ${VARIANTS:-0 1 2}; do
   export CMN_EXTRA_NVFLAGS="-DCMN_BARRIER_VARIANT=$v"
   python -c "from paper_1908_00213_b200 import build; build.build(force=True)" > $O/build_v$v.log 2>&1 || { echo "build $v failed"; continue; }
   timeout 600 python scripts/barrier_latency.py --variant v$v >> $O/barrier_ab.jsonl 2>> $O/barrier_ab.err
