@@ -12,3 +12,4 @@ tail -4 $O/r2s3v_pytest_gpu.txt
 timeout 600 python bench.py --gpus 1 --steps 20 --warmup 5 > $O/r2s3v_bench.json 2> $O/r2s3v_bench.err; echo "bench rc=$?"
 tail -c 600 $O/r2s3v_bench.json
 timeout 600 python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > $O/r2s3v_bench_ref.json 2> $O/r2s3v_bench_ref.err; echo "ref rc=$?"
+timeout 900 python scripts/emulated_bench.py --worlds 2,4,8 --algos twoshot > $O/r2s3v_emulated_bench.jsonl 2>/dev/null; echo "emul rc=$?"
