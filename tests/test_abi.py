@@ -98,6 +98,9 @@ def test_no_cpu_fallback(lib):
     assert e.value.status_name == "CMN_ERR_CUDA"
     with pytest.raises(cmn.CmnError):
         cmn.Comm.init(0, 1, 0)
+    with pytest.raises(cmn.CmnError) as e:
+        cmn.Comm.emulated_world(2)
+    assert e.value.status_name == "CMN_ERR_CUDA"
 
 
 def test_invalid_world(lib):
@@ -105,6 +108,8 @@ def test_invalid_world(lib):
     h = C.c_void_p()
     assert lib.cmn_init_simulated(9, 0, C.byref(h)) == 1
     assert lib.cmn_init_simulated(0, 0, C.byref(h)) == 1
+    assert lib.cmn_init_emulated(9, 0, C.byref(h)) == 1
+    assert lib.cmn_init_emulated(0, 0, C.byref(h)) == 1
 
 
 @pytest.mark.parametrize("bucket_mb", [0, 1, 4, 8, 16, 25, 1000])
