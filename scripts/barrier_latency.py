@@ -30,43 +30,47 @@ def main():
     ap.add_argument("--calls", type=int, default=20)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--variant", default=os.environ.get("CMN_EXTRA_NVFLAGS", "default"))
+    ap.add_argument("--ctas", default="0", help="collective CTAs per rank to try (0 = library default)")
+    ap.add_argument("--kinds", default="emulated,simulated")
     args = ap.parse_args()
     dev = "cuda:0"
     stream = torch.cuda.current_stream()
     for N in [int(x) for x in args.worlds.split(",")]:
         for n in [int(x) for x in args.elems.split(",")]:
             g = [torch.empty(n, device=dev).uniform_(-1e-2, 1e-2) for _ in range(N)]
-            for kind in ("emulated", "simulated"):
-                for algo in ("oneshot", "twoshot"):
-                    comm = Comm.emulated_world(N) if kind == "emulated" else Comm.simulated_world(N)
-                    try:
-                        w = torch.zeros(n, device=dev)
-                        comm.register_params([w])
-                        comm.set_algo(algo)
-                        table = comm.prepare(g)
-                        for _ in range(3):
-                            comm.allreduce_grads(table, "fp32")
-                        torch.cuda.synchronize()
-                        graph = torch.cuda.CUDAGraph()
-                        with torch.cuda.graph(graph):
-                            for _ in range(args.calls):
+            for kind in args.kinds.split(","):
+                for ctas in [int(x) for x in args.ctas.split(",")]:
+                    for algo in ("oneshot", "twoshot"):
+                        comm = Comm.emulated_world(N) if kind == "emulated" else Comm.simulated_world(N)
+                        try:
+                            w = torch.zeros(n, device=dev)
+                            comm.register_params([w])
+                            comm.set_algo(algo)
+                            comm.set_ctas(ctas, 0)
+                            table = comm.prepare(g)
+                            for _ in range(3):
                                 comm.allreduce_grads(table, "fp32")
-                        for _ in range(2):
-                            graph.replay()
-                        torch.cuda.synchronize()
-                        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                        a.record(stream)
-                        for _ in range(args.reps):
-                            graph.replay()
-                        b.record(stream)
-                        torch.cuda.synchronize()
-                        comm.poll_error()
-                        us = a.elapsed_time(b) / (args.reps * args.calls) * 1e3
-                        print(json.dumps({"variant": args.variant, "kind": kind, "N": N, "elems": n,
-                                          "algo": algo, "us_per_call": us}), flush=True)
-                        del graph
-                    finally:
-                        comm.finalize()
+                            torch.cuda.synchronize()
+                            graph = torch.cuda.CUDAGraph()
+                            with torch.cuda.graph(graph):
+                                for _ in range(args.calls):
+                                    comm.allreduce_grads(table, "fp32")
+                            for _ in range(2):
+                                graph.replay()
+                            torch.cuda.synchronize()
+                            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                            a.record(stream)
+                            for _ in range(args.reps):
+                                graph.replay()
+                            b.record(stream)
+                            torch.cuda.synchronize()
+                            comm.poll_error()
+                            us = a.elapsed_time(b) / (args.reps * args.calls) * 1e3
+                            print(json.dumps({"variant": args.variant, "kind": kind, "N": N, "elems": n,
+                                              "algo": algo, "ctas": ctas, "us_per_call": us}), flush=True)
+                            del graph
+                        finally:
+                            comm.finalize()
             del g
 
 
