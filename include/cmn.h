@@ -168,7 +168,10 @@ cmn_status cmn_init_simulated(int world_size, int cuda_device, cmn_comm **out);
  * epochs, call tags, timeouts and poison flags as cmn_init mode, exercised
  * on one GPU without separate launches that wait on one another.  G is the
  * collective grid (cmn_set_ctas) capped at the co-resident capacity / N.
- * The other collectives (fused pull / push, sharded, NVLS, NCCL) behave as in
+ * The fused pull step's reduce-scatter and all-gather + update and the
+ * sharded step's reduce-scatter and parameter all-gather run the same way
+ * (their blocks of every rank striding together over the one shared
+ * replica's items); the push form, NVLS and NCCL behave as in
  * cmn_init_simulated.  Test mode; fault injection through the environment:
  * CMN_TEST_EMUL_ABSENT_RANK=r (rank r's blocks never arrive: the others time
  * out), CMN_TEST_EMUL_MISMATCH_RANK=r (rank r posts another call tag),

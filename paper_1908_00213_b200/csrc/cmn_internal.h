@@ -159,7 +159,8 @@ cudaError_t launch_allreduce_oneshot(const PeerBufs &in, int world, void *out, i
 // rank's chunk from red[p] into red[rank].  With the barrier enabled and
 // both phases: start barrier, RS, mid barrier, AG in one kernel.
 // chunk_start/chunk_end give every rank's element range (within [e0, e1)).
-// emulate = true: one cooperative launch plays every rank (`rank` unused).
+// emulate = true: one cooperative launch plays every rank (`rank` unused;
+// phases 3, or 1 for the fused / sharded schedules' reduce-scatter).
 cudaError_t launch_allreduce_twoshot(const PeerBufs &in, const PeerBufs &red, int world, int rank,
                                      const int64_t *chunk_start, const int64_t *chunk_end,
                                      int dtype, int phases, const Barrier &bar, int blocks,
@@ -173,15 +174,19 @@ cudaError_t launch_update_chunk(const TensorDesc *td, const Item *items, int i0,
 
 // NEXT-4 all-gather of parameters: start barrier, then copy items [i0, i1)
 // minus [s0, s1) from the owner's exchange buffer (Item.reserved = owner).
+// emulate = true: one cooperative launch over every rank (barrier live), the
+// whole grid striding over the items of the shared replica.
 cudaError_t launch_gather_params(const TensorDesc *td, const Item *items, int i0, int i1, int s0,
                                  int s1, const PeerBufs &exch, int world, const Barrier &bar,
-                                 int blocks, cudaStream_t s);
+                                 int blocks, cudaStream_t s, bool emulate = false);
 
 // Fused all-gather + update: start barrier, then momentum SGD over the
 // chunk-clipped items [i0, i1) reading r from red.p[Item.reserved].
+// emulate = true: as launch_gather_params.
 cudaError_t launch_update_gather(const TensorDesc *td, const Item *items, int i0, int i1,
                                  const PeerBufs &red, int world, int dtype, float n_rep, float lr,
-                                 float mu, const Barrier &bar, int blocks, cudaStream_t s);
+                                 float mu, const Barrier &bar, int blocks, cudaStream_t s,
+                                 bool emulate = false);
 
 // Fused pack + reduce-scatter transfer (push): start barrier, then cast and
 // store the elements of the chunk-clipped items [i0, i1) (Item.reserved =

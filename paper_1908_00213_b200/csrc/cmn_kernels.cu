@@ -892,6 +892,9 @@ __global__ void __launch_bounds__(kThreads) k_gather_params(const TensorDesc *__
                                                             const __grid_constant__ PeerBufs exch,
                                                             int world,
                                                             const __grid_constant__ Barrier bar) {
+    // Emulated world: the one cooperative grid (every rank's blocks) strides
+    // over the items together, so each item of the shared replica is copied
+    // once; the barrier maps the block to its (rank, CTA) itself.
     const uint32_t bv = barrier_value(bar);
     if (!cross_rank_barrier(bar, bv, world, 0)) return;
     for (int i = i0 + blockIdx.x; i < i1; i += gridDim.x) {
@@ -929,6 +932,8 @@ __global__ void __launch_bounds__(kThreads) k_update_gather(const TensorDesc *__
                                                             int world, const Avg n_rep, float lr,
                                                             float mu,
                                                             const __grid_constant__ Barrier bar) {
+    // Emulated world: every rank's blocks stride over the shared replica's
+    // items together (each item updated once); barrier as in k_gather_params.
     const uint32_t bv = barrier_value(bar);
     if (!cross_rank_barrier(bar, bv, world, 0)) return;
     for (int i = i0 + blockIdx.x; i < i1; i += gridDim.x) {
@@ -1396,7 +1401,7 @@ cudaError_t launch_allreduce_twoshot(const PeerBufs &in, const PeerBufs &red, in
                                      int dtype, int phases, const Barrier &bar, int blocks,
                                      cudaStream_t s, bool emulate) {
     if (blocks <= 0 || blocks > kMaxBarrierBlocks) return cudaErrorInvalidValue;
-    if (emulate && (!bar.enabled || phases != 3)) return cudaErrorInvalidValue;
+    if (emulate && (!bar.enabled || (phases != 3 && phases != 1))) return cudaErrorInvalidValue;
     (void)cudaGetLastError();
     Chunks ch{};
     for (int p = 0; p < world; ++p) {
@@ -1428,27 +1433,28 @@ cudaError_t launch_update_chunk(const TensorDesc *td, const Item *items, int i0,
 
 cudaError_t launch_gather_params(const TensorDesc *td, const Item *items, int i0, int i1, int s0,
                                  int s1, const PeerBufs &exch, int world, const Barrier &bar,
-                                 int blocks, cudaStream_t s) {
+                                 int blocks, cudaStream_t s, bool emulate) {
     if (blocks <= 0 || blocks > kMaxBarrierBlocks) return cudaErrorInvalidValue;
+    if (emulate && !bar.enabled) return cudaErrorInvalidValue;
     (void)cudaGetLastError();
-    k_gather_params<<<blocks, kThreads, 0, s>>>(td, items, i0, i1, s0, s1, exch, world, bar);
-    return cudaGetLastError();
+    const cudaError_t e = launch_barrier_kernel(k_gather_params, world, blocks, emulate, bar, s, td, items,
+                                                i0, i1, s0, s1, exch, world);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_update_gather(const TensorDesc *td, const Item *items, int i0, int i1,
                                  const PeerBufs &red, int world, int dtype, float n_rep, float lr,
-                                 float mu, const Barrier &bar, int blocks, cudaStream_t s) {
+                                 float mu, const Barrier &bar, int blocks, cudaStream_t s, bool emulate) {
     if (blocks <= 0 || blocks > kMaxBarrierBlocks) return cudaErrorInvalidValue;
+    if (emulate && !bar.enabled) return cudaErrorInvalidValue;
     (void)cudaGetLastError();
     const Avg a = make_avg(n_rep);
     const bool div = needs_div(n_rep);
-    if (dtype == 0)
-        (div ? k_update_gather<0, true> : k_update_gather<0, false>)<<<blocks, kThreads, 0, s>>>(
-            td, items, i0, i1, red, world, a, lr, mu, bar);
-    else
-        (div ? k_update_gather<1, true> : k_update_gather<1, false>)<<<blocks, kThreads, 0, s>>>(
-            td, items, i0, i1, red, world, a, lr, mu, bar);
-    return cudaGetLastError();
+    const auto k = dtype == 0 ? (div ? k_update_gather<0, true> : k_update_gather<0, false>)
+                              : (div ? k_update_gather<1, true> : k_update_gather<1, false>);
+    const cudaError_t e = launch_barrier_kernel(k, world, blocks, emulate, bar, s, td, items, i0, i1, red,
+                                                world, a, lr, mu);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_pack_push(const GradTab &g, int t_lo, const Item *items, int i0, int i1,

@@ -462,8 +462,16 @@ cmn_status step_sharded(cmn_comm *c, const float *const *grads, int dtype, float
     int64_t cs[kMaxWorld], ce[kMaxWorld];
     chunk_plan(0, c->L, c->world, cs, ce);
     const int blocks = ar_blocks_for(c);
-    const Barrier bar = make_barrier(c, dtype, kBarTwoshot, 0, c->L);
-    for (int i = 0; i < nsim; ++i) {
+    Barrier bar = make_barrier(c, dtype, kBarTwoshot, 0, c->L);
+    if (c->emulated) {          // one cooperative reduce-scatter over every rank, barrier live
+        bar.enabled = 1;
+        cmn_status st = launched(c,
+                                 launch_allreduce_twoshot(in, red, c->world, 0, cs, ce, dtype, 1, bar,
+                                                          blocks, s, true),
+                                 "reduce_scatter (emulated world)");
+        if (st != CMN_OK) return st;
+    }
+    for (int i = 0; i < (c->emulated ? 0 : nsim); ++i) {
         const int r = c->simulated ? i : c->rank;
         cmn_status st = launched(c,
                                  launch_allreduce_twoshot(in, red, c->world, r, cs, ce, dtype, 1, bar,
@@ -483,9 +491,22 @@ cmn_status step_sharded(cmn_comm *c, const float *const *grads, int dtype, float
         if (st != CMN_OK) return st;
     }
     ++c->seq;
-    const Barrier bar2 = make_barrier(c, dtype, kBarGatherParams);
+    Barrier bar2 = make_barrier(c, dtype, kBarGatherParams);
     const int total = c->sitem_begin[c->world];
     const int gblocks = upd_blocks_for(c, total);
+    if (c->emulated) {
+        // every rank's blocks in one cooperative grid, barrier live; the
+        // shared replica's items are each copied once from their owner's
+        // exchange buffer (the owner's own chunk included: the same values)
+        bar2.enabled = 1;
+        cmn_status st = launched(c,
+                                 launch_gather_params(c->d_td, c->d_sitems, 0, total, 0, 0, exch, c->world,
+                                                      bar2, gblocks, s, true),
+                                 "gather_params (emulated world)");
+        if (st != CMN_OK) return st;
+        c->fresh = false;
+        return CMN_OK;
+    }
     for (int i = 0; i < nsim; ++i) {
         const int r = c->simulated ? i : c->rank;
         cmn_status st = launched(c,
@@ -551,7 +572,21 @@ cmn_status step_fused(cmn_comm *c, const float *const *grads, int dtype, float l
         st = pack_phase(c, 0, c->T, grads, dtype, par, s);
     }
     if (st != CMN_OK) return st;
+    // Emulated world, pull form: the reduce-scatter and the fused all-gather +
+    // update as cooperative launches over every rank, barriers live (the
+    // push form's per-rank inbox tables keep the simulated launches).
+    const bool emul = c->emulated && !push;
     st = timed(c, s, [&] {
+        if (emul) {
+            PeerBufs in{};
+            for (int p = 0; p < c->world; ++p) in.p[p] = c->rb[p].packed[par];
+            Barrier b = bar;
+            b.enabled = 1;
+            return launched(c,
+                            launch_allreduce_twoshot(in, red, c->world, 0, cs, ce, dtype, 1, b, blocks, s,
+                                                     true),
+                            "reduce_scatter (emulated world)");
+        }
         for (int i = 0; i < nsim; ++i) {
             const int r = c->simulated ? i : c->rank;
             PeerBufs in{};
@@ -567,15 +602,18 @@ cmn_status step_fused(cmn_comm *c, const float *const *grads, int dtype, float l
     });
     if (st != CMN_OK) return st;
     ++c->seq;
-    const Barrier bar2 = make_barrier(c, dtype, kBarUpdateGather);
+    Barrier bar2 = make_barrier(c, dtype, kBarUpdateGather);
+    if (emul) bar2.enabled = 1;
     const int gblocks = upd_blocks_for(c, total);
     // simulated ranks share one parameter replica: one launch updates it all
+    // (emulated: one cooperative launch whose blocks of every rank stride
+    // over the replica's items together, each item once)
     st = timed(c, s, [&] {
         return launched(c,
                         launch_update_gather(c->d_td, c->d_sitems, 0, total, red, c->world, dtype,
                                              static_cast<float>(c->world), lr, mu, bar2,
-                                             gblocks, s),
-                        "update_gather");
+                                             gblocks, s, emul),
+                        emul ? "update_gather (emulated world)" : "update_gather");
     });
     if (st != CMN_OK) return st;
     c->last = ArResult{0, dtype, false, false};   // rank r's chunk of reduced[0] (test hook)

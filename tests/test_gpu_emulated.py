@@ -109,27 +109,34 @@ def test_emulated_world_bitexact(cmn, orc, N, dtype, algo):
 
 @pytest.mark.slow
 @pytest.mark.parametrize("dtype", ["fp32", "fp16"])
-@pytest.mark.parametrize("pieces", [0, 4])
-def test_emulated_r50_n8_back_to_back(cmn, orc, dtype, pieces):
-    """The full ResNet-50 gradient set, 8 emulated ranks, two-shot with the
-    mid barrier live, 3 cmn_steps issued back to back (serial, or the
-    pipelined 4-piece schedule whose all-reduces run on the internal
-    stream), w and v bit-exact vs 3 oracle steps."""
+@pytest.mark.parametrize("sched", ["serial", "pipelined4", "fused", "sharded"])
+def test_emulated_r50_n8_back_to_back(cmn, orc, dtype, sched):
+    """The full ResNet-50 gradient set, 8 emulated ranks, barriers live, 3
+    steps issued back to back: serial two-shot (start + mid barrier), the
+    pipelined 4-piece schedule (all-reduces on the internal stream), the
+    fused pull schedule (reduce-scatter, then the fused all-gather + update
+    with its start barrier) and the sharded step (reduce-scatter, own-chunk
+    update, parameter all-gather).  w bit-exact vs 3 oracle steps, and v too
+    (the sharded step keeps v on the chunk owner: one replica holds all)."""
     shapes, N, lr, mu, K = synth.resnet50_shapes(), 8, 0.1, 0.9, 3
     w0 = synth.params(shapes)
     wo, vo = [x.copy() for x in w0], [np.zeros_like(x) for x in w0]
     for k in range(K):
         orc.step(synth.grads(shapes, workers=N, step=k), wo, vo, lr, mu, dtype)
-    comm = _emulated(cmn, N, "twoshot", pieces)
+    comm = _emulated(cmn, N, "twoshot", 4 if sched == "pipelined4" else 0)
     try:
+        comm.set_fused_update(1 if sched == "fused" else 0)
         w = [torch.from_numpy(p).to(DEV) for p in w0]
         comm.register_params(w)
         tables = [comm.prepare([g for gw in _dev_grads(shapes, N, k) for g in gw]) for k in range(K)]
         torch.cuda.synchronize()
+        n0 = comm.kernel_launches
         for k in range(K):
-            comm.step(tables[k], dtype, lr, mu)
+            (comm.step_sharded if sched == "sharded" else comm.step)(tables[k], dtype, lr, mu)
         torch.cuda.synchronize()
         comm.poll_error()
+        if sched == "fused":      # per step: N packs + ONE reduce-scatter + ONE all-gather/update
+            assert comm.kernel_launches - n0 == K * (N + 2)
         for t in range(len(w)):
             _same(w[t].cpu().numpy().reshape(-1), wo[t], f"w[{t}]")
             _same(comm.momentum(t).cpu().numpy().reshape(-1), vo[t], f"v[{t}]")
