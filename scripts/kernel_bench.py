@@ -38,6 +38,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=50)
     ap.add_argument("--worlds", default="1,2,4,8")
+    ap.add_argument("--emulated", action="store_true",
+                    help="N > 1 in the emulated world (cmn_init_emulated: the one-/two-shot, fused "
+                         "and sharded barrier kernels as cooperative launches, barriers live)")
     args = ap.parse_args()
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
@@ -53,7 +56,8 @@ def main():
         for dtype in ("fp32", "fp16"):
             c = 4 if dtype == "fp32" else 2
             for algo in (("oneshot", "twoshot") if N > 1 else ("identity",)):
-                comm = Comm.simulated_world(N) if N > 1 else Comm.init(0, 1, 0)
+                comm = ((Comm.emulated_world(N) if args.emulated else Comm.simulated_world(N))
+                        if N > 1 else Comm.init(0, 1, 0))
                 w = [torch.from_numpy(p.copy()).to(dev) for p in params0]
                 comm.register_params(w)
                 if N > 1:
@@ -138,6 +142,7 @@ def main():
                 else:
                     # simulated: N packs + N (oneshot) or 2N (twoshot) launches, all local HBM
                     rec["sim_note"] = "all N ranks' kernels on one GPU; local HBM stands in for NVLink"
+                    rec["world"] = "emulated (barriers live)" if args.emulated else "simulated (barriers off)"
                     if algo == "twoshot":
                         # whole-step schedules: in simulation every rank's pack and
                         # all-reduce kernels run on this one GPU from local HBM, while
