@@ -45,6 +45,10 @@ SCHEDULES = {
     "fused_2cta": (1, 0, 2, 2),
     "fused_push": (2, 0, 0, 0),
     "fused_push_2cta": (2, 0, 2, 2),
+    # one CTA per SM for every barrier kernel: a system-scope fence costs
+    # more once two CTAs fence on one SM (emulated world)
+    "fused_1cta": (1, 0, 1, 1),
+    "fused_push_1cta": (2, 0, 1, 1),
     "serial": (0, 0, 0, 0),
     "serial_2cta": (0, 0, 2, 0),
 }
