@@ -435,6 +435,18 @@ cmn_status cmn_get_adam_state(cmn_comm *comm, int tensor, float **m_ptr, float *
 cmn_status cmn_copy_packed(cmn_comm *comm, int rank, void *dst, void *stream);
 cmn_status cmn_copy_reduced(cmn_comm *comm, int rank, void *dst, void *stream);
 
+/* cmn_debug_fill_buffers -- test hook ("poisoned receive
+ * buffers"): fill this rank's library-owned packed and reduced buffers (every
+ * simulated / emulated rank's in those modes; both parities, the whole
+ * allocation incl. the push-form inbox slack, NOT the signal pad) with the
+ * 32-bit `pattern`, stream-ordered on `stream`.  With 0x7FC07FC0 -- a NaN
+ * as fp32 and as each fp16 half -- any later read of a location no kernel of
+ * the step wrote propagates NaN into the result, so a bit-exact step after
+ * the fill proves the step reads only what it wrote.  Discards any
+ * unconsumed all-reduce result (a following update returns STATE).
+ * Errors: INVALID_ARG (comm NULL), STATE (no registration), CUDA. */
+cmn_status cmn_debug_fill_buffers(cmn_comm *comm, uint32_t pattern, void *stream);
+
 /* cmn_poll_error -- non-blocking check of the device error word (timeouts,
  * sequence mismatches) without issuing work. */
 cmn_status cmn_poll_error(cmn_comm *comm);

@@ -32,6 +32,7 @@ SIGNATURES = [
     ("cmn_init", C.c_int, [C.c_int, C.c_int, C.c_int, AllgatherFn, _P, _PP]),
     ("cmn_init_simulated", C.c_int, [C.c_int, C.c_int, _PP]),
     ("cmn_init_emulated", C.c_int, [C.c_int, C.c_int, _PP]),
+    ("cmn_debug_fill_buffers", C.c_int, [_P, C.c_uint32, _P]),
     ("cmn_finalize", C.c_int, [_P]),
     ("cmn_register_params", C.c_int, [_P, C.c_int, C.POINTER(C.c_int), _I64P, _PP]),
     ("cmn_get_layout", C.c_int, [_P, _I64P, _I64P]),
@@ -448,6 +449,12 @@ class Comm:
 
     def copy_reduced(self, rank: int, dst, stream=None):
         _check(lib().cmn_copy_reduced(self._h, rank, dst.data_ptr(), _stream(stream)), "cmn_copy_reduced")
+
+    def debug_fill_buffers(self, pattern: int = 0x7FC07FC0, stream=None):
+        """cmn_debug_fill_buffers: poison the library's packed / reduced buffers
+        (default: NaN as fp32 and as fp16) -- test hook."""
+        _check(lib().cmn_debug_fill_buffers(self._h, C.c_uint32(pattern), _stream(stream)),
+               "cmn_debug_fill_buffers")
 
     def poll_error(self):
         _check(lib().cmn_poll_error(self._h), "cmn_poll_error")

@@ -753,6 +753,20 @@ cmn_status cmn_copy_reduced(cmn_comm *c, int rank, void *dst, void *stream) {
     return copy_buf(c, rank, dst, stream, true);
 }
 
+cmn_status cmn_debug_fill_buffers(cmn_comm *c, uint32_t pattern, void *stream) {
+    if (cmn_status st = require_registered(c); st != CMN_OK) return st;
+    if (cmn_status st = set_device(c); st != CMN_OK) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t words = static_cast<size_t>(buf_elems(c->L)) * 4;   // packed0..reduced1, fp32 words
+    const int own = c->simulated ? c->world : 1;
+    for (int i = 0; i < own; ++i) {
+        const int r = c->simulated ? i : c->rank;
+        CMN_CUDA(launch_fill_u32(static_cast<uint32_t *>(c->rb[r].packed[0]), words, pattern, s));
+    }
+    c->fresh = false;
+    return CMN_OK;
+}
+
 cmn_status cmn_poll_error(cmn_comm *c) {
     if (!c) return fail(CMN_ERR_INVALID_ARG, "comm is NULL");
     return check_async_error(c);

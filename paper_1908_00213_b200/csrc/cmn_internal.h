@@ -202,6 +202,9 @@ cudaError_t launch_nvls_allreduce(const void *mc_packed, void *mc_reduced, int64
                                   int world, int dtype, const Barrier &bar, int blocks,
                                   cudaStream_t s);
 
+// test hook: p[0, n) = pattern (cmn_debug_fill_buffers)
+cudaError_t launch_fill_u32(uint32_t *p, size_t n, uint32_t pattern, cudaStream_t s);
+
 int num_sms(int device);
 
 }  // namespace cmn

@@ -1485,6 +1485,21 @@ cudaError_t launch_nvls_allreduce(const void *mc_packed, void *mc_reduced, int64
     return cudaGetLastError();
 }
 
+namespace {
+__global__ void k_fill_u32(uint32_t *__restrict__ p, size_t n, uint32_t pattern) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        p[i] = pattern;
+}
+}  // namespace
+
+cudaError_t launch_fill_u32(uint32_t *p, size_t n, uint32_t pattern, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    (void)cudaGetLastError();
+    k_fill_u32<<<1184, 256, 0, s>>>(p, n, pattern);
+    return cudaGetLastError();
+}
+
 int num_sms(int device) {
     int n = 0;
     if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;

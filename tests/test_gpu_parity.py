@@ -1241,3 +1241,89 @@ def test_checkpoint_resume_bitwise(cmn, orc, N):
             assert_bitwise(w[t].cpu().numpy().reshape(-1), wa[t].reshape(-1), f"resumed adam w[{t}]")
     finally:
         comm.finalize()
+
+
+@pytest.mark.parametrize("sched", ["oneshot", "twoshot", "pipelined3", "fused", "push", "sharded",
+                                   "buckets", "adam"])
+@pytest.mark.parametrize("dtype", ["fp32", "fp16"])
+@pytest.mark.parametrize("N", [3, 8])
+def test_poisoned_buffers_every_schedule(cmn, orc, sched, dtype, N):
+    """SURVEY §5's poisoned receive buffers: before every step the library's
+    packed and reduced buffers of every rank (inbox slack included) are
+    filled with 0x7FC07FC0 -- NaN as fp32 and as each fp16 half -- so a
+    kernel that reads a location no kernel of the step wrote (a pad, a
+    chunk tail, an inbox slot, the other parity) puts NaN into w.  Every
+    schedule stays bit-exact with the oracle over 2 steps; in the emulated
+    pass the barriers are live."""
+    shapes = synth.mlp_shapes() + RAGGED
+    sizes = [synth.numel(s) for s in shapes]
+    off, L = orc.layout(sizes)
+    params0 = synth.params(shapes)
+    w_o = [p.copy() for p in params0]
+    m_o = [np.zeros_like(p) for p in params0]
+    v_o = [np.zeros_like(p) for p in params0]
+    comm = cmn.Comm.simulated_world(N)
+    try:
+        w = to_dev(params0)
+        comm.register_params(w)
+        comm.set_algo("oneshot" if sched == "oneshot" else "twoshot")
+        comm.set_pipeline(3 if sched == "pipelined3" else 0)
+        comm.set_fused_update({"fused": 1, "push": 2}.get(sched, 0))
+        nb = comm.plan_buckets(1 << 16) if sched == "buckets" else 0
+        for step in range(1, 3):
+            g = synth.grads(shapes, workers=N, step=step)
+            red = orc.reduce_tree([orc.pack(gw, off, L, dtype) for gw in g], dtype)
+            if sched == "adam":
+                orc.update_adam(red, dtype, N, 1e-3, 0.9, 0.999, 1e-8, step, off, w_o, m_o, v_o)
+            else:
+                orc.update_momentum_sgd(red, dtype, N, 0.1, 0.9, off, w_o, v_o)
+            gd = [to_dev(gw) for gw in g]
+            comm.debug_fill_buffers()
+            if sched == "adam":
+                comm.step_adam(gd, dtype, 1e-3, 0.9, 0.999, 1e-8, step)
+            elif sched == "sharded":
+                comm.step_sharded(gd, dtype, 0.1, 0.9)
+            elif sched == "buckets":
+                for b in range(nb):
+                    comm.allreduce_bucket(b, gd, dtype)
+                for b in range(nb):
+                    comm.update_bucket(b, 0.1, 0.9)
+            else:
+                comm.step(gd, dtype, 0.1, 0.9)
+            torch.cuda.synchronize()
+            comm.poll_error()
+            for t in range(len(w)):
+                assert_bitwise(w[t].cpu().numpy().reshape(-1), w_o[t], f"{sched} w[{t}] step {step}")
+                if sched == "adam":
+                    m, v = comm.adam_state(t)
+                    assert_bitwise(v.cpu().numpy().reshape(-1), v_o[t], f"adam v[{t}] step {step}")
+                else:
+                    assert_bitwise(comm.momentum(t).cpu().numpy().reshape(-1), v_o[t],
+                                   f"{sched} v[{t}] step {step}")
+    finally:
+        comm.finalize()
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "fp16"])
+def test_poison_hook_reaches_the_buffers(cmn, dtype):
+    """The poison test above is not vacuous: after a fill, every rank's
+    packed and reduced buffers (what the kernels read) hold the NaN pattern
+    in every element, and an update issued after the fill is refused."""
+    shapes, N = synth.mlp_shapes(), 3
+    comm = cmn.Comm.simulated_world(N)
+    try:
+        comm.register_params(to_dev(synth.params(shapes)))
+        comm.allreduce_grads([to_dev(gw) for gw in synth.grads(shapes, workers=N)], dtype)
+        comm.debug_fill_buffers()
+        L = comm.layout()[1]
+        tdt, pat = (torch.int32, 0x7FC07FC0) if dtype == "fp32" else (torch.int16, 0x7FC0)
+        for r in range(N):
+            for copy in (comm.copy_packed, comm.copy_reduced):
+                q = torch.zeros(L, dtype=tdt, device=DEV)
+                copy(r, q)
+                assert bool((q == pat).all()), f"rank {r}: {copy.__name__} not poisoned"
+        with pytest.raises(cmn.CmnError) as e:
+            comm.update_momentum_sgd(0.1, 0.9)
+        assert e.value.status_name == "CMN_ERR_STATE"
+    finally:
+        comm.finalize()
