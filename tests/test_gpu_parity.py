@@ -1327,3 +1327,74 @@ def test_poison_hook_reaches_the_buffers(cmn, dtype):
         assert e.value.status_name == "CMN_ERR_STATE"
     finally:
         comm.finalize()
+
+
+@pytest.mark.parametrize("sched", ["direct", "adam_direct", "oneshot", "twoshot", "pipelined3", "fused",
+                                   "push", "sharded", "buckets", "adam"])
+def test_guard_bands_untouched(cmn, orc, sched):
+    """Out-of-bounds writes (the other half of what compute-sanitizer's
+    memcheck would catch): every parameter tensor is a view into one
+    allocation with 64-element guard bands of a canary pattern before,
+    between and after the tensors (ragged sizes, so item tails end mid-band
+    alignment).  After 2 steps of the schedule (N = 1 direct kernels, else
+    N = 3) every canary word is intact and w is bit-exact with the oracle."""
+    shapes = synth.mlp_shapes() + RAGGED
+    sizes = [synth.numel(s) for s in shapes]
+    N = 1 if sched in ("direct", "adam_direct") else 3
+    off, L = orc.layout(sizes)
+    G = 64
+    starts, pos = [], G
+    for n in sizes:
+        starts.append(pos)
+        pos += -(-n // 8) * 8 + G          # 32-byte aligned starts, >= 64 canary words between
+    canary = np.uint32(0x7FBADBAD)
+    flat = torch.from_numpy(np.full(pos, canary, dtype=np.uint32).view(np.float32)).to(DEV)
+    params0 = synth.params(shapes)
+    w = []
+    for t, n in enumerate(sizes):
+        v = flat[starts[t]: starts[t] + n]
+        v.copy_(torch.from_numpy(params0[t]))
+        w.append(v.view(shapes[t]))
+    mask = np.ones(pos, dtype=bool)
+    for t, n in enumerate(sizes):
+        mask[starts[t]: starts[t] + n] = False
+    w_o = [p.copy() for p in params0]
+    m_o = [np.zeros_like(p) for p in params0]
+    v_o = [np.zeros_like(p) for p in params0]
+    comm = cmn.Comm.init(0, 1, 0) if N == 1 else cmn.Comm.simulated_world(N)
+    try:
+        comm.register_params(w)
+        if N > 1:
+            comm.set_algo("oneshot" if sched == "oneshot" else "twoshot")
+            comm.set_pipeline(3 if sched == "pipelined3" else 0)
+            comm.set_fused_update({"fused": 1, "push": 2}.get(sched, 0))
+        nb = comm.plan_buckets(1 << 16) if sched == "buckets" else 0
+        adam = sched in ("adam", "adam_direct")
+        for step in range(1, 3):
+            g = synth.grads(shapes, workers=N, step=step)
+            red = orc.reduce_tree([orc.pack(gw, off, L, "fp32") for gw in g], "fp32")
+            if adam:
+                orc.update_adam(red, "fp32", N, 1e-3, 0.9, 0.999, 1e-8, step, off, w_o, m_o, v_o)
+            else:
+                orc.update_momentum_sgd(red, "fp32", N, 0.1, 0.9, off, w_o, v_o)
+            gd = to_dev(g[0]) if N == 1 else [to_dev(gw) for gw in g]
+            if adam:
+                comm.step_adam(gd, "fp32", 1e-3, 0.9, 0.999, 1e-8, step)
+            elif sched == "sharded":
+                comm.step_sharded(gd, "fp32", 0.1, 0.9)
+            elif sched == "buckets":
+                for b in range(nb):
+                    comm.allreduce_bucket(b, gd, "fp32")
+                for b in range(nb):
+                    comm.update_bucket(b, 0.1, 0.9)
+            else:
+                comm.step(gd, "fp32", 0.1, 0.9)
+        torch.cuda.synchronize()
+        comm.poll_error()
+        bits = flat.cpu().numpy().view(np.uint32)
+        bad = np.flatnonzero(bits[mask] != canary)
+        assert bad.size == 0, f"{sched}: {bad.size} guard words overwritten"
+        for t in range(len(w)):
+            assert_bitwise(w[t].cpu().numpy().reshape(-1), w_o[t], f"{sched} w[{t}]")
+    finally:
+        comm.finalize()
