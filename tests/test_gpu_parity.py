@@ -1336,8 +1336,11 @@ def test_guard_bands_untouched(cmn, orc, sched):
     memcheck would catch): every parameter tensor is a view into one
     allocation with 64-element guard bands of a canary pattern before,
     between and after the tensors (ragged sizes, so item tails end mid-band
-    alignment).  After 2 steps of the schedule (N = 1 direct kernels, else
-    N = 3) every canary word is intact and w is bit-exact with the oracle."""
+    alignment).  The gradients sit between NaN canary bands the same way.
+    After 2 steps of the schedule (N = 1 direct kernels, else N = 3) every
+    canary word is intact, the gradients are unchanged (read-only) and w is
+    bit-exact with the oracle (an out-of-bounds gradient read that reached
+    the result would have made it NaN)."""
     shapes = synth.mlp_shapes() + RAGGED
     sizes = [synth.numel(s) for s in shapes]
     N = 1 if sched in ("direct", "adam_direct") else 3
@@ -1377,7 +1380,19 @@ def test_guard_bands_untouched(cmn, orc, sched):
                 orc.update_adam(red, "fp32", N, 1e-3, 0.9, 0.999, 1e-8, step, off, w_o, m_o, v_o)
             else:
                 orc.update_momentum_sgd(red, "fp32", N, 0.1, 0.9, off, w_o, v_o)
-            gd = to_dev(g[0]) if N == 1 else [to_dev(gw) for gw in g]
+            # gradients, too, live between NaN canary bands: an out-of-bounds
+            # read that reached the result would turn it into NaN
+            gflat = []
+            gd = []
+            for gw in g:
+                fb = torch.from_numpy(np.full(pos, canary, dtype=np.uint32).view(np.float32)).to(DEV)
+                views = []
+                for t, n in enumerate(sizes):
+                    fb[starts[t]: starts[t] + n].copy_(torch.from_numpy(gw[t]))
+                    views.append(fb[starts[t]: starts[t] + n].view(shapes[t]))
+                gflat.append((fb, fb.clone()))
+                gd.append(views)
+            gd = gd[0] if N == 1 else gd
             if adam:
                 comm.step_adam(gd, "fp32", 1e-3, 0.9, 0.999, 1e-8, step)
             elif sched == "sharded":
@@ -1389,7 +1404,9 @@ def test_guard_bands_untouched(cmn, orc, sched):
                     comm.update_bucket(b, 0.1, 0.9)
             else:
                 comm.step(gd, "fp32", 0.1, 0.9)
-        torch.cuda.synchronize()
+            torch.cuda.synchronize()
+            for fb, before in gflat:          # the gradients are read-only (include/cmn.h)
+                assert torch.equal(fb.view(torch.int32), before.view(torch.int32)), f"{sched}: grads written"
         comm.poll_error()
         bits = flat.cpu().numpy().view(np.uint32)
         bad = np.flatnonzero(bits[mask] != canary)
