@@ -39,6 +39,7 @@ def cmn_worlds(request):
     from paper_1908_00213_b200 import build
     build.build()
     from paper_1908_00213_b200 import cmn as m
+    m.TEST_WORLD_KIND = request.param
     if request.param == "simulated":
         yield m
         return
@@ -48,6 +49,14 @@ def cmn_worlds(request):
         yield m
     finally:
         m.Comm.simulated_world = saved
+        m.TEST_WORLD_KIND = "simulated"
+
+
+def single_rank_only(cmn):
+    """For tests that never build a simulated world (N = 1 only): run them
+    in the simulated pass of conftest.cmn_worlds, skip the emulated repeat."""
+    if getattr(cmn, "TEST_WORLD_KIND", "simulated") == "emulated":
+        pytest.skip("N = 1 only: nothing to emulate (runs in the simulated pass)")
 
 
 @pytest.fixture(scope="session")

@@ -20,6 +20,7 @@ import pytest
 import torch
 
 import synth
+from conftest import single_rank_only
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
@@ -81,6 +82,7 @@ def test_r50_back_to_back_n1_as_benched(cmn, orc, dtype):
     events (the bench's kernel-duration pass), then 3 replays of a captured
     graph of the step (torch.cuda.graph synchronises once before capturing;
     nothing else does) against 11 oracle steps on the same gradients."""
+    single_rank_only(cmn)
     shapes = synth.resnet50_shapes()
     params0 = synth.params(shapes)
     g = synth.grads(shapes, workers=1)
@@ -170,6 +172,7 @@ def test_fp16_cast_all_2pow32_patterns_on_gpu(cmn, orc):
     all 2^32 inputs on the host).  NaNs are compared by class: both sides
     must produce an fp16 NaN for exactly the fp32 NaNs.  16 chunks of 2^28;
     the oracle side runs on host threads (bit-identical, elementwise)."""
+    single_rank_only(cmn)
     chunk = 1 << 28
     comm = cmn.Comm.init(0, 1, 0)
     pool = ThreadPoolExecutor(max_workers=8)

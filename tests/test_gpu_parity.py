@@ -14,6 +14,7 @@ import pytest
 import torch
 
 import synth
+from conftest import single_rank_only
 
 pytestmark = pytest.mark.gpu
 
@@ -186,6 +187,7 @@ def test_tolerance_gate_vs_exact(cmn, orc, dtype):
 def test_step_n1_direct_equals_unfused(cmn, orc):
     """cmn_step at N = 1 (no pack, the bench's kernel) == allreduce+update ==
     oracle, bitwise, for fp32 and fp16, over 3 steps."""
+    single_rank_only(cmn)
     shapes = synth.mlp_shapes() + RAGGED
     for dtype in ("fp32", "fp16"):
         grads = [synth.grads(shapes, workers=1, step=s) for s in range(3)]
@@ -213,6 +215,7 @@ def test_r50_full_size_n1_bench_config(cmn, orc, dtype):
     each in the packed layout, a pre-marshalled pointer table, cmn_step on
     torch's current stream, 3 steps; all 25.6M elements of w and v vs the
     oracle after every step."""
+    single_rank_only(cmn)
     shapes = synth.resnet50_shapes()
     sizes = [synth.numel(s) for s in shapes]
     params0 = synth.params(shapes)
@@ -726,6 +729,7 @@ def test_fp16_conversion_exhaustive_on_gpu(cmn, orc):
     """The GPU path's fp32->fp16 cast (inside k_pack) over a dense sweep of
     fp32 bit patterns vs the oracle's hand-written RNE (itself pinned to
     the compiler over all 2^32 inputs)."""
+    single_rank_only(cmn)
     step = 4099  # coprime stride covering every exponent and many mantissas
     bits = (np.arange(0, 2 ** 32, step, dtype=np.uint64)).astype(np.uint32)
     x = bits.view(np.float32)
@@ -746,6 +750,7 @@ def test_fp16_conversion_exhaustive_on_gpu(cmn, orc):
 
 
 def test_launch_count(cmn):
+    single_rank_only(cmn)
     shapes = synth.resnet50_shapes()
     comm = cmn.Comm.init(0, 1, 0)
     try:
