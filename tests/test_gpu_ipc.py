@@ -329,7 +329,7 @@ def test_ipc_stress_random_schedules(orc, world, dtype):
     sizes redrawn every step (same draw on every rank): the per-CTA barrier
     epochs, buffer parities and inbox reuse stay paired; w and v bit-exact
     with 60 oracle steps on every rank."""
-    steps = int(os.environ.get("CMN_STRESS_STEPS", "60"))     # longer soak runs: scripts/gpu_r2_soak.sh
+    steps = int(os.environ.get("CMN_STRESS_STEPS", "60"))     # longer soak runs: set CMN_STRESS_STEPS
     res = _run(world, dtype, "twoshot", steps=steps, mode="stress")
     assert all(r[1] == "ok" for r in res), res
     shapes = synth.mlp_shapes()
