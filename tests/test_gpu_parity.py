@@ -1334,9 +1334,10 @@ def test_poison_hook_reaches_the_buffers(cmn, dtype):
         comm.finalize()
 
 
+@pytest.mark.parametrize("dtype", ["fp32", "fp16"])
 @pytest.mark.parametrize("sched", ["direct", "adam_direct", "oneshot", "twoshot", "pipelined3", "fused",
                                    "push", "sharded", "buckets", "adam"])
-def test_guard_bands_untouched(cmn, orc, sched):
+def test_guard_bands_untouched(cmn, orc, sched, dtype):
     """Out-of-bounds writes (the other half of what compute-sanitizer's
     memcheck would catch): every parameter tensor is a view into one
     allocation with 64-element guard bands of a canary pattern before,
@@ -1380,11 +1381,11 @@ def test_guard_bands_untouched(cmn, orc, sched):
         adam = sched in ("adam", "adam_direct")
         for step in range(1, 3):
             g = synth.grads(shapes, workers=N, step=step)
-            red = orc.reduce_tree([orc.pack(gw, off, L, "fp32") for gw in g], "fp32")
+            red = orc.reduce_tree([orc.pack(gw, off, L, dtype) for gw in g], dtype)
             if adam:
-                orc.update_adam(red, "fp32", N, 1e-3, 0.9, 0.999, 1e-8, step, off, w_o, m_o, v_o)
+                orc.update_adam(red, dtype, N, 1e-3, 0.9, 0.999, 1e-8, step, off, w_o, m_o, v_o)
             else:
-                orc.update_momentum_sgd(red, "fp32", N, 0.1, 0.9, off, w_o, v_o)
+                orc.update_momentum_sgd(red, dtype, N, 0.1, 0.9, off, w_o, v_o)
             # gradients, too, live between NaN canary bands: an out-of-bounds
             # read that reached the result would turn it into NaN
             gflat = []
@@ -1399,16 +1400,16 @@ def test_guard_bands_untouched(cmn, orc, sched):
                 gd.append(views)
             gd = gd[0] if N == 1 else gd
             if adam:
-                comm.step_adam(gd, "fp32", 1e-3, 0.9, 0.999, 1e-8, step)
+                comm.step_adam(gd, dtype, 1e-3, 0.9, 0.999, 1e-8, step)
             elif sched == "sharded":
-                comm.step_sharded(gd, "fp32", 0.1, 0.9)
+                comm.step_sharded(gd, dtype, 0.1, 0.9)
             elif sched == "buckets":
                 for b in range(nb):
-                    comm.allreduce_bucket(b, gd, "fp32")
+                    comm.allreduce_bucket(b, gd, dtype)
                 for b in range(nb):
                     comm.update_bucket(b, 0.1, 0.9)
             else:
-                comm.step(gd, "fp32", 0.1, 0.9)
+                comm.step(gd, dtype, 0.1, 0.9)
             torch.cuda.synchronize()
             for fb, before in gflat:          # the gradients are read-only (include/cmn.h)
                 assert torch.equal(fb.view(torch.int32), before.view(torch.int32)), f"{sched}: grads written"
