@@ -334,3 +334,49 @@ def test_emulated_negative_control_without_mid_barrier(cmn, orc, monkeypatch):
     bad = sum(int(np.count_nonzero(_u32(got[k][r]) != _u32(want[k]["reduced"])))
               for k in range(3) for r in range(N))
     assert bad > 0, "without the mid barrier the gathered chunks should be stale"
+
+
+def test_emulated_random_schedule_stress(cmn, orc):
+    """80 steps, 4 emulated ranks, barriers live, the schedule redrawn every
+    step from serial one-/two-shot, pipelined (2 / 3 pieces), fused pull,
+    fused push, sharded and bucketed, with the payload dtype and the
+    collective / update grids redrawn too (barrier kernels of different
+    kinds, tags and CTA counts interleave, so per-CTA epochs of different
+    indices advance at different rates): w and v bit-exact vs the oracle
+    replaying the same 80 steps."""
+    shapes, N, lr, mu = synth.mlp_shapes() + RAGGED, 4, 0.05, 0.9
+    w0 = synth.params(shapes)
+    wo, vo = [x.copy() for x in w0], [np.zeros_like(x) for x in w0]
+    comm = cmn.Comm.emulated_world(N)
+    try:
+        w = [torch.from_numpy(p).to(DEV) for p in w0]
+        comm.register_params(w)
+        nb = comm.plan_buckets(1 << 16)
+        rng = np.random.default_rng(20261018)
+        scheds = ["oneshot", "twoshot", "pipelined2", "pipelined3", "fused", "push", "sharded", "buckets"]
+        for k in range(80):
+            sched = scheds[rng.integers(len(scheds))]
+            dtype = ["fp32", "fp16"][rng.integers(2)]
+            ctas = [0, 16, 64][rng.integers(3)]
+            comm.set_ctas(ctas, [0, 148][rng.integers(2)])
+            comm.set_algo("oneshot" if sched == "oneshot" else "twoshot")
+            comm.set_pipeline({"pipelined2": 2, "pipelined3": 3}.get(sched, 0))
+            comm.set_fused_update({"fused": 1, "push": 2}.get(sched, 0))
+            gd = _dev_grads(shapes, N, k % 5)
+            if sched == "sharded":
+                comm.step_sharded(gd, dtype, lr, mu)
+            elif sched == "buckets":
+                for b in range(nb):
+                    comm.allreduce_bucket(b, gd, dtype)
+                for b in range(nb):
+                    comm.update_bucket(b, lr, mu)
+            else:
+                comm.step(gd, dtype, lr, mu)
+            orc.step(synth.grads(shapes, workers=N, step=k % 5), wo, vo, lr, mu, dtype)
+        torch.cuda.synchronize()
+        comm.poll_error()
+        for t in range(len(w)):
+            _same(w[t].cpu().numpy().reshape(-1), wo[t], f"w[{t}]")
+            _same(comm.momentum(t).cpu().numpy().reshape(-1), vo[t], f"v[{t}]")
+    finally:
+        comm.finalize()
