@@ -207,23 +207,28 @@ def test_emulated_graph_replay(cmn, orc):
 
 
 @pytest.mark.parametrize("fault,code", [("CMN_TEST_EMUL_ABSENT_RANK", 6), ("CMN_TEST_EMUL_MISMATCH_RANK", 5)])
-@pytest.mark.parametrize("algo", ["oneshot", "twoshot"])
+@pytest.mark.parametrize("algo", ["oneshot", "twoshot", "pipelined3", "fused", "sharded"])
 def test_emulated_fault_leaves_state_untouched(cmn, monkeypatch, fault, code, algo):
     """A rank that never arrives (its peers' barriers time out: CMN_ERR_TIMEOUT)
-    or posts another call tag (CMN_ERR_MISMATCH): the failed step leaves w
-    and v bit-identical (every CTA skips its stores, the update kernel sees
-    the device error word), the error surfaces on the next call, and the
-    communicator stays failed."""
+    or posts another call tag (CMN_ERR_MISMATCH) in the step's first
+    all-reduce kernel: the failed step leaves w and v bit-identical (every
+    CTA skips its stores; the later kernels of the step -- the update, the
+    fused all-gather + update, the sharded chunk update and parameter
+    all-gather -- see the device error word or post poison and touch
+    nothing), the error surfaces on the next call, and the communicator
+    stays failed."""
     from paper_1908_00213_b200.cmn import CmnError
     monkeypatch.setenv(fault, "2")
     shapes, N = RAGGED, 4
-    comm = _emulated(cmn, N, algo)
+    comm = _emulated(cmn, N, "oneshot" if algo == "oneshot" else "twoshot",
+                     3 if algo == "pipelined3" else 0)
     try:
         comm.set_timeout(300)
+        comm.set_fused_update(1 if algo == "fused" else 0)
         w = [torch.from_numpy(p).to(DEV) for p in synth.params(shapes)]
         comm.register_params(w)
         w_before = [x.clone() for x in w]
-        comm.step(_dev_grads(shapes, N, 0), "fp32", 0.1, 0.9)
+        (comm.step_sharded if algo == "sharded" else comm.step)(_dev_grads(shapes, N, 0), "fp32", 0.1, 0.9)
         torch.cuda.synchronize()
         for t in range(len(w)):
             assert torch.equal(w[t].view(torch.int32), w_before[t].view(torch.int32)), f"w[{t}] changed"
