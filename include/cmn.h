@@ -171,7 +171,8 @@ cmn_status cmn_init_simulated(int world_size, int cuda_device, cmn_comm **out);
  * The fused pull step's reduce-scatter and all-gather + update and the
  * sharded step's reduce-scatter and parameter all-gather run the same way
  * (their blocks of every rank striding together over the one shared
- * replica's items); the push form, NVLS and NCCL behave as in
+ * replica's items), and so does the push form while N * n_tensors <= 256
+ * (one launch's gradient-pointer table); NVLS and NCCL behave as in
  * cmn_init_simulated.  Test mode; fault injection through the environment:
  * CMN_TEST_EMUL_ABSENT_RANK=r (rank r's blocks never arrive: the others time
  * out), CMN_TEST_EMUL_MISMATCH_RANK=r (rank r posts another call tag),

@@ -161,10 +161,12 @@ cudaError_t launch_allreduce_oneshot(const PeerBufs &in, int world, void *out, i
 // chunk_start/chunk_end give every rank's element range (within [e0, e1)).
 // emulate = true: one cooperative launch plays every rank (`rank` unused;
 // phases 3, or 1 for the fused / sharded schedules' reduce-scatter).
+// inbox_slot_elems > 0 (emulated push form, phases 1): rank r reduces its
+// own inbox, slot i at in.p[r] + i * inbox_slot_elems payload elements.
 cudaError_t launch_allreduce_twoshot(const PeerBufs &in, const PeerBufs &red, int world, int rank,
                                      const int64_t *chunk_start, const int64_t *chunk_end,
                                      int dtype, int phases, const Barrier &bar, int blocks,
-                                     cudaStream_t s, bool emulate = false);
+                                     cudaStream_t s, bool emulate = false, int64_t inbox_slot_elems = 0);
 
 // NEXT-4 sharded update: momentum SGD on the items of the own chunk, also
 // writing w' into the fp32 exchange buffer (packed layout).
@@ -191,9 +193,13 @@ cudaError_t launch_update_gather(const TensorDesc *td, const Item *items, int i0
 // Fused pack + reduce-scatter transfer (push): start barrier, then cast and
 // store the elements of the chunk-clipped items [i0, i1) (Item.reserved =
 // owner; all tensors in [t_lo, t_lo + kGradCap)) to dst.p[owner] + base.
+// emulate = true: one cooperative launch over every rank: rank r's gradient
+// of tensor t at g.p[r * tstride + t - t_lo], its slot in owner o's inbox at
+// dst.p[o] + r * slot_bytes (dst = rank 0's view).
 cudaError_t launch_pack_push(const GradTab &g, int t_lo, const Item *items, int i0, int i1,
                              const PeerBufs &dst, int world, int dtype, const Barrier &bar,
-                             int blocks, cudaStream_t s);
+                             int blocks, cudaStream_t s, bool emulate = false, int tstride = 0,
+                             int64_t slot_bytes = 0);
 
 // NEXT-3 NVLS: this rank's chunk [e0, e1) (elements) reduced in the switch
 // from the multicast packed buffer and multicast-stored into every rank's

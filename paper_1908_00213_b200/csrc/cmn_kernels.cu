@@ -761,12 +761,17 @@ __global__ void __launch_bounds__(kThreads) k_oneshot(const __grid_constant__ Pe
 struct Chunks {
     int64_t s[kMaxWorld];   // 16-B units
     int64_t e[kMaxWorld];
+    int64_t inbox_slot;     // INBOX instances only: slot stride of the push-form inbox, 16-B units
 };
 
 // Two-shot.  Tile i of every chunk belongs to CTA (i mod gridDim.x) in both
 // phases, so the per-CTA mid barrier pairs each all-gather read with the
 // reduce-scatter write that produced it.
-template <int N, int DT>
+// INBOX (emulated world, push form only): the reduce-scatter reads rank r's
+// own inbox, slot i at in.p[r] + i * inbox_slot (rank r's packed[0]), in
+// place of the rank-independent table in.p[i]; the production instances
+// (INBOX = false) are unchanged.
+template <int N, int DT, bool INBOX = false>
 __global__ void __launch_bounds__(kThreads) k_twoshot(const __grid_constant__ PeerBufs in,
                                                       const __grid_constant__ PeerBufs red,
                                                       int rank,
@@ -790,7 +795,11 @@ __global__ void __launch_bounds__(kThreads) k_twoshot(const __grid_constant__ Pe
                 const int64_t idx = tile + threadIdx.x + u * kThreads;
                 if (idx < e) {
 #pragma unroll
-                    for (int i = 0; i < N; ++i) x[u][i] = ld_peer_u4(static_cast<const uint4 *>(in.p[i]) + idx);
+                    for (int i = 0; i < N; ++i) {
+                        const uint4 *src = INBOX ? static_cast<const uint4 *>(in.p[rank]) + i * ch.inbox_slot - s
+                                                 : static_cast<const uint4 *>(in.p[i]);
+                        x[u][i] = ld_peer_u4(src + idx);
+                    }
                 }
             }
 #pragma unroll
@@ -987,17 +996,23 @@ __global__ void __launch_bounds__(kThreads) k_update_gather(const TensorDesc *__
 // to local HBM.  Items are clipped to the chunks (Item.reserved = owner);
 // dst.p[o] is owner o's slot for this rank, offset so that packed index j
 // lands at dst.p[o] + j.  Pads after a tensor's last item are zeroed.
+// Emulated world (bar.emul_g > 0): block (r, b) packs rank r's gradients --
+// g.p[r * tstride + t - t_lo] -- into every owner's inbox slot for rank r,
+// dst.p[o] + r * slot_bytes (dst is rank 0's view); each rank's blocks
+// stride over all items.  On a real rank tstride / slot_bytes are unused.
 template <int DT, int CAP>
 __global__ void __launch_bounds__(kThreads) k_pack_push(const __grid_constant__ GradTabN<CAP> g, int t_lo,
                                                         const Item *__restrict__ items, int i0,
                                                         int i1, const __grid_constant__ PeerBufs dst,
-                                                        int world,
+                                                        int world, int tstride, int64_t slot_bytes,
                                                         const __grid_constant__ Barrier bar) {
+    const CtaRank cr = cta_rank(bar);
+    const int er = bar.emul_g > 0 ? cr.rank : 0;
     const uint32_t bv = barrier_value(bar);
     if (!cross_rank_barrier(bar, bv, world, 0)) return;
-    for (int i = i0 + blockIdx.x; i < i1; i += gridDim.x) {
+    for (int i = i0 + cr.b; i < i1; i += cr.n) {
         const Item it = items[i];
-        const float *__restrict__ src = g.p[it.t - t_lo] + it.k0;
+        const float *__restrict__ src = g.p[er * tstride + it.t - t_lo] + it.k0;
         const int nv = it.len >> 2;
         float4 x[kVecPerThread];
 #pragma unroll
@@ -1005,8 +1020,9 @@ __global__ void __launch_bounds__(kThreads) k_pack_push(const __grid_constant__ 
             const int v = threadIdx.x + u * kThreads;
             if (v < nv) x[u] = ld_cs_f4(src + 4 * v);
         }
+        char *dbase = static_cast<char *>(const_cast<void *>(dst.p[it.reserved])) + er * slot_bytes;
         if constexpr (DT == 0) {
-            float *d = const_cast<float *>(static_cast<const float *>(dst.p[it.reserved])) + it.base;
+            float *d = reinterpret_cast<float *>(dbase) + it.base;
 #pragma unroll
             for (int u = 0; u < kVecPerThread; ++u) {
                 const int v = threadIdx.x + u * kThreads;
@@ -1017,7 +1033,7 @@ __global__ void __launch_bounds__(kThreads) k_pack_push(const __grid_constant__ 
             for (int k = (nv << 2) + threadIdx.x; k < it.len; k += kThreads) d[k] = src[k];
             for (int k = threadIdx.x; k < it.pad; k += kThreads) d[it.len + k] = 0.0f;
         } else {
-            uint16_t *d = const_cast<uint16_t *>(static_cast<const uint16_t *>(dst.p[it.reserved])) + it.base;
+            uint16_t *d = reinterpret_cast<uint16_t *>(dbase) + it.base;
 #pragma unroll
             for (int u = 0; u < kVecPerThread; ++u) {
                 const int v = threadIdx.x + u * kThreads;
@@ -1349,6 +1365,9 @@ cudaError_t oneshot_n(const PeerBufs &in, void *out, const PeerBufs &outs, int64
 template <int N, int DT>
 cudaError_t twoshot_n(const PeerBufs &in, const PeerBufs &red, int rank, const Chunks &ch, int phases,
                       const Barrier &bar, int blocks, bool emulate, cudaStream_t s) {
+    if (ch.inbox_slot > 0)    // emulated push form: every rank reduces its own inbox
+        return launch_barrier_kernel(k_twoshot<N, DT, true>, N, blocks, emulate, bar, s, in, red, rank, ch,
+                                     phases);
     return launch_barrier_kernel(k_twoshot<N, DT>, N, blocks, emulate, bar, s, in, red, rank, ch, phases);
 }
 template <int DT>
@@ -1399,11 +1418,13 @@ cudaError_t launch_allreduce_oneshot(const PeerBufs &in, int world, void *out, i
 cudaError_t launch_allreduce_twoshot(const PeerBufs &in, const PeerBufs &red, int world, int rank,
                                      const int64_t *chunk_start, const int64_t *chunk_end,
                                      int dtype, int phases, const Barrier &bar, int blocks,
-                                     cudaStream_t s, bool emulate) {
+                                     cudaStream_t s, bool emulate, int64_t inbox_slot_elems) {
     if (blocks <= 0 || blocks > kMaxBarrierBlocks) return cudaErrorInvalidValue;
     if (emulate && (!bar.enabled || (phases != 3 && phases != 1))) return cudaErrorInvalidValue;
+    if (inbox_slot_elems > 0 && !(emulate && phases == 1)) return cudaErrorInvalidValue;
     (void)cudaGetLastError();
     Chunks ch{};
+    ch.inbox_slot = to_vec(inbox_slot_elems, dtype);
     for (int p = 0; p < world; ++p) {
         ch.s[p] = to_vec(chunk_start[p], dtype);
         ch.e[p] = to_vec(chunk_end[p], dtype);
@@ -1459,15 +1480,17 @@ cudaError_t launch_update_gather(const TensorDesc *td, const Item *items, int i0
 
 cudaError_t launch_pack_push(const GradTab &g, int t_lo, const Item *items, int i0, int i1,
                              const PeerBufs &dst, int world, int dtype, const Barrier &bar,
-                             int blocks, cudaStream_t s) {
+                             int blocks, cudaStream_t s, bool emulate, int tstride, int64_t slot_bytes) {
     if (blocks <= 0 || blocks > kMaxBarrierBlocks) return cudaErrorInvalidValue;
+    if (emulate && (!bar.enabled || tstride <= 0 || slot_bytes <= 0)) return cudaErrorInvalidValue;
     (void)cudaGetLastError();
     const auto t = shrink<kGradCap>(g);
-    if (dtype == 0)
-        k_pack_push<0, kGradCap><<<blocks, kThreads, 0, s>>>(t, t_lo, items, i0, i1, dst, world, bar);
-    else
-        k_pack_push<1, kGradCap><<<blocks, kThreads, 0, s>>>(t, t_lo, items, i0, i1, dst, world, bar);
-    return cudaGetLastError();
+    const cudaError_t e =
+        dtype == 0 ? launch_barrier_kernel(k_pack_push<0, kGradCap>, world, blocks, emulate, bar, s, t, t_lo,
+                                           items, i0, i1, dst, world, tstride, slot_bytes)
+                   : launch_barrier_kernel(k_pack_push<1, kGradCap>, world, blocks, emulate, bar, s, t, t_lo,
+                                           items, i0, i1, dst, world, tstride, slot_bytes);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_nvls_allreduce(const void *mc_packed, void *mc_reduced, int64_t e0, int64_t e1,

@@ -551,7 +551,24 @@ cmn_status step_fused(cmn_comm *c, const float *const *grads, int dtype, float l
         return reinterpret_cast<const void *>(a);
     };
     cmn_status st = CMN_OK;
-    if (push) {
+    // Emulated world: the barrier kernels as cooperative launches over every
+    // rank, barriers live -- the pull form always, the push form while every
+    // rank's gradient pointers fit one launch's table (N * T <= kGradCap)
+    const bool emul_push = c->emulated && push && c->world * c->T <= kGradCap;
+    const bool emul = c->emulated && (!push || emul_push);
+    if (emul_push) {
+        Barrier bar0 = make_barrier(c, dtype, kBarPackPush);
+        bar0.enabled = 1;
+        PeerBufs dst0{};
+        for (int o = 0; o < c->world; ++o) dst0.p[o] = inbox_view(o, 0);
+        st = timed(c, s, [&] {
+            return launched(c,
+                            launch_pack_push(make_tab(grads, 0, c->world * c->T), 0, c->d_sitems, 0, total,
+                                             dst0, c->world, dtype, bar0, upd_blocks_for(c, total), s, true,
+                                             c->T, cmax * static_cast<int64_t>(esz)),
+                            "pack_push (emulated world)");
+        });
+    } else if (push) {
         const Barrier bar0 = make_barrier(c, dtype, kBarPackPush);
         st = timed(c, s, [&] {
             for (int i = 0; i < nsim; ++i) {
@@ -572,19 +589,17 @@ cmn_status step_fused(cmn_comm *c, const float *const *grads, int dtype, float l
         st = pack_phase(c, 0, c->T, grads, dtype, par, s);
     }
     if (st != CMN_OK) return st;
-    // Emulated world, pull form: the reduce-scatter and the fused all-gather +
-    // update as cooperative launches over every rank, barriers live (the
-    // push form's per-rank inbox tables keep the simulated launches).
-    const bool emul = c->emulated && !push;
     st = timed(c, s, [&] {
         if (emul) {
+            // pull: every rank's packed buffer; push: every rank reduces its
+            // own inbox (rank p's packed[0], slot i at + i * cmax elements)
             PeerBufs in{};
-            for (int p = 0; p < c->world; ++p) in.p[p] = c->rb[p].packed[par];
+            for (int p = 0; p < c->world; ++p) in.p[p] = push ? c->rb[p].packed[0] : c->rb[p].packed[par];
             Barrier b = bar;
             b.enabled = 1;
             return launched(c,
                             launch_allreduce_twoshot(in, red, c->world, 0, cs, ce, dtype, 1, b, blocks, s,
-                                                     true),
+                                                     true, push ? cmax : 0),
                             "reduce_scatter (emulated world)");
         }
         for (int i = 0; i < nsim; ++i) {

@@ -385,3 +385,35 @@ def test_emulated_random_schedule_stress(cmn, orc):
             _same(comm.momentum(t).cpu().numpy().reshape(-1), vo[t], f"v[{t}]")
     finally:
         comm.finalize()
+
+
+@pytest.mark.parametrize("N", [2, 4, 8])
+@pytest.mark.parametrize("dtype", ["fp32", "fp16"])
+def test_emulated_push_form(cmn, orc, N, dtype):
+    """The fused push step in the emulated world (every rank's gradient
+    pointers fit one launch: N * T <= 256): ONE cooperative pack + push
+    launch (each rank's blocks cast its gradients into every owner's inbox
+    slot), ONE cooperative inbox reduce-scatter, ONE cooperative all-gather
+    + update -- 3 launches per step, barriers live -- and w, v bit-exact vs
+    3 oracle steps."""
+    shapes, lr, mu = synth.mlp_shapes() + RAGGED, 0.1, 0.9
+    w0 = synth.params(shapes)
+    wo, vo = [x.copy() for x in w0], [np.zeros_like(x) for x in w0]
+    for k in range(3):
+        orc.step(synth.grads(shapes, workers=N, step=k), wo, vo, lr, mu, dtype)
+    comm = _emulated(cmn, N, "twoshot")
+    try:
+        comm.set_fused_update(2)
+        w = [torch.from_numpy(p).to(DEV) for p in w0]
+        comm.register_params(w)
+        for k in range(3):
+            n0 = comm.kernel_launches
+            comm.step(_dev_grads(shapes, N, k), dtype, lr, mu)
+            assert comm.kernel_launches - n0 == 3
+        torch.cuda.synchronize()
+        comm.poll_error()
+        for t in range(len(w)):
+            _same(w[t].cpu().numpy().reshape(-1), wo[t], f"w[{t}]")
+            _same(comm.momentum(t).cpu().numpy().reshape(-1), vo[t], f"v[{t}]")
+    finally:
+        comm.finalize()
