@@ -554,7 +554,7 @@ cmn_status step_fused(cmn_comm *c, const float *const *grads, int dtype, float l
     // Emulated world: the barrier kernels as cooperative launches over every
     // rank, barriers live -- the pull form always, the push form while every
     // rank's gradient pointers fit one launch's table (N * T <= kGradCap)
-    const bool emul_push = c->emulated && push && c->world * c->T <= kGradCap;
+    const bool emul_push = c->emulated && push && c->world * c->T <= kGradCap && cmax > 0;
     const bool emul = c->emulated && (!push || emul_push);
     if (emul_push) {
         Barrier bar0 = make_barrier(c, dtype, kBarPackPush);
