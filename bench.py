@@ -452,7 +452,9 @@ def run_nvls_child(args):
             out["unavailable"] = str(e)[:200]
             ok = False
         try:
-            if ok:
+            if ok and os.environ.get("CMN_TEST_NVLS_SETUP_ONLY") == "1":
+                out["setup_only"] = True      # tests: stop before any barrier kernel runs
+            elif ok:
                 _nvls_child_measure(comm, wl, args, stream, dev, world, algo, out)
             comm.poll_error()
         except CmnError as e:

@@ -191,3 +191,53 @@ def test_reference_arm_same_config_as_gpu_arm():
         outs.append(json.loads(p.stdout.strip().splitlines()[-1]))
     assert outs[0]["config"] == outs[1]["config"]
     assert outs[1]["steps"] == 4 and outs[1]["details"]["timed_region_s"] > 0
+
+
+def _probe_parent(rank, world, port, q):
+    import types
+
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["CMN_TEST_NVLS_SETUP_ONLY"] = "1"      # inherited by the child processes
+    sys.path.insert(0, ROOT)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import bench
+        res, adopted = bench.nvls_probe(types.SimpleNamespace(dtype="fp32"), rank, world,
+                                        rank % torch.cuda.device_count(), timeout_s=240)
+        q.put((rank, res, adopted))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_nvls_probe_two_ranks_setup_only():
+    """The isolated NVLS probe across 2 ranks up to the NVLS setup and no
+    further (CMN_TEST_NVLS_SETUP_ONLY: no barrier kernel runs, so both ranks
+    may share the one GPU): two parent processes (gloo) spawn their child
+    processes, which rendezvous on their own port, build the communicator
+    (CUDA-IPC exchange), register the ResNet-50 set and set NVLS up
+    collectively -- refused on a box without a multicast fabric.  Each
+    child must come back with its JSON report (the algorithm it tried and
+    why it is unavailable, or that setup succeeded), and the parents must
+    agree not to adopt NVLS (a setup-only probe never passes the gate)."""
+    import socket
+
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_probe_parent, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = sorted([q.get(timeout=400) for _ in range(2)], key=lambda r: r[0])
+    for p in ps:
+        p.join(timeout=60)
+    for rank, r, adopted in res:
+        assert adopted is False
+        assert r.get("algo") == "nvls", r                 # the child's own report, not a crash
+        assert "unavailable" in r or r.get("setup_only") is True, r
