@@ -45,3 +45,16 @@ def test_reference_arm_one_json_line():
 
 def test_reference_arm_nonzero_ranks_are_silent():
     assert _run({"RANK": "1", "WORLD_SIZE": "2"}, ("--gpus", "2")) == []
+
+
+def test_gpu_arm_refuses_more_ranks_than_gpus():
+    """One process per GPU: bench.py never time-slices ranks whose kernels
+    wait on one another on one GPU (B200_PROFILING.md) -- WORLD_SIZE larger
+    than the visible GPU count (0 here) stops before any CUDA work with a
+    message saying why."""
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "2",
+                        "--warmup", "1"], capture_output=True, text=True, env=env, timeout=300, cwd=ROOT)
+    assert p.returncode != 0
+    assert "2 ranks need 2 GPUs" in p.stderr
+    assert not p.stdout.strip()
